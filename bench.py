@@ -1,0 +1,333 @@
+"""Benchmark: simulated MIPS of the SimNet parallel sub-trace simulation path.
+
+Workload (BASELINE.json configs[1], "c2"): C3 CNN latency predictor, synthetic
+10M-instruction trace, 1024 sub-traces per GPU.  One "step" = one complete
+simulation of the trace (all 9,766 rounds of K1 context -> K2 inference ->
+K3 decode/clock) with the trace resident in HBM.  N>1 (torchrun, one process
+per GPU): weak scaling, each rank simulates its own 10M-instruction slice as
+1024 sub-traces; the cycle/instruction totals are summed with one NCCL
+all-reduce at the end (the only collective on this path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation of the path
+(oracle/_ref: the reference sources compiled from /root/reference, with the
+Eigen-free restated forward) on the host cores, on a bounded sample of the
+same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MFLOP_C3 = 2 * 1_073_408  # 2 x model_flops(preset_c3), cnn.cpp:319-333
+N_INSTR = 10_000_000
+K_SUB = 1024
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--precision", default=os.environ.get("SIMNET_PRECISION", "fp32"))
+    p.add_argument("--n", type=int, default=N_INSTR)
+    p.add_argument("--k", type=int, default=K_SUB)
+    p.add_argument("--regime", default="default", choices=["default", "memory"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-rounds", type=int, default=0, help="rounds in the CPU-baseline sample (0 = auto)")
+    return p.parse_args()
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+def workload(rank: int, n: int, regime: str):
+    from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace
+
+    kind = "memory" if regime == "memory" else "mix"
+    trace = synthetic_trace(n, seed=101 + rank, kind=kind)
+    model = synthetic_model(synthetic_trace(200_000, seed=101, kind=kind), seed=1, regime=regime)
+    return trace, model
+
+
+def pinned_trace(trace):
+    """Copy the trace arrays into page-locked host memory (e2e H2D source)."""
+    import torch
+
+    from paper_2105_05821_b200.formats import Trace
+
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    return Trace(pin(trace.pc), pin(trace.op), pin(trace.src), pin(trace.dst), pin(trace.has_data),
+                 pin(trace.data_addr), pin(trace.data_size), pin(trace.hist), pin(trace.truth), trace.fetch_tick)
+
+
+def trace_h2d_bytes(t) -> int:
+    return int(t.pc.nbytes + t.op.nbytes + t.src.nbytes + t.dst.nbytes + t.data_addr.nbytes + t.hist.nbytes
+               + t.truth.nbytes)
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref, else the oracle port) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference(trace, model, k: int, rounds: int, repeats: int = 1):
+    """Times the reference's simulate_parallel on the first rounds*k
+    instructions as k sub-traces (same batch shape as the GPU run)."""
+    from oracle.oracle import Port, Ref, ref_available
+
+    from paper_2105_05821_b200.formats import write_model, write_trace
+
+    n = rounds * k
+    sample = trace.slice(0, n)
+    threads = os.cpu_count() or 1
+    secs = []
+    if ref_available():
+        kind = "reference"
+        R = Ref()
+        with tempfile.TemporaryDirectory() as td:
+            tp, mp = Path(td) / "s.trace", Path(td) / "m.model"
+            write_trace(tp, sample)
+            write_model(mp, model)
+            for _ in range(repeats):
+                r = R.simulate(tp, mp, k=k, workers=threads, n_hint=n)
+                secs.append(r["seconds"])
+    else:
+        kind = "port"
+        P = Port()
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            P.simulate(sample, model, k=k, threads=threads)
+            secs.append(time.perf_counter() - t0)
+    mips = n / statistics.median(secs) / 1e6
+    return {"value": mips, "unit": "MIPS", "cores": threads, "kind": kind,
+            "sample": f"{rounds} rounds x {k} sub-traces = {n} instructions of the same trace/model "
+                      f"(simulate_parallel, OpenMP threads={threads}, timing scope as cmd_simulate)"}, secs
+
+
+def run_reference_impl(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    trace, model = workload(0, max(args.k * 64, 200_000), args.regime)
+    rounds = args.cpu_rounds or 48
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        base, secs = cpu_reference(trace, model, args.k, rounds)
+        if i >= args.warmup:
+            per_step.append(secs[0])
+    n = rounds * args.k
+    mips = n * len(per_step) / sum(per_step) / 1e6
+    line = {
+        "metric": "simulated MIPS", "value": mips, "unit": "MIPS", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(per_step), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"c2: C3 CNN, {args.k} sub-traces, {args.regime} regime (bounded CPU sample)",
+                   "sub_traces": args.k, "instructions_per_step": n},
+        "cpu_baseline": dict(base, value=mips),
+        "e2e": {"value": mips, "unit": "MIPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_impl(args)
+        return
+    rank, world, local = dist_info()
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig
+
+    trace, model = workload(rank, args.n, args.regime)
+    g = GpuSimulator(local, args.precision)
+    g.load_model(model)
+    pc = ParallelConfig(k=args.k, sim=SimConfig(max_context=model.config.max_context))
+    g.load_trace(trace, pc)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        g.run(pc)
+    barrier()
+    dev_ms, launches, results = [], 0, []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = g.run(pc)
+            dev_ms.append(r.device_ms)
+            launches += r.launches
+            results.append(r)
+        barrier()
+        wall = time.perf_counter() - t0
+    step_ms = sum(dev_ms) / len(dev_ms)
+    # max over ranks of the device time, and the one collective: totals
+    totals = torch.tensor([r.total_cycles, r.instructions, sum(s.sum_fetch for s in r.sub_results),
+                           sum(s.delta for s in r.sub_results), sum(s.drain_cycles for s in r.sub_results),
+                           sum(s.overflow_stall_cycles for s in r.sub_results)], dtype=torch.int64, device="cuda")
+    tmax = torch.tensor([step_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(totals)
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+    step_ms_max = float(tmax.item())
+    n_all = int(totals[1].item())
+    value = n_all / (step_ms_max / 1e3) / 1e6
+
+    # kernel breakdown + roofline of the dominant kernel (instrumented pass)
+    prof = g.run(pc, profile=True)
+    rounds = max(prof.rounds, 1)
+    k_ms = {"context": prof.kernel_ms[0], "inference": prof.kernel_ms[1], "decode": prof.kernel_ms[2]}
+    infer_ms_round = prof.kernel_ms[1] / rounds
+    flops_round = MFLOP_C3 * args.k
+    pk = peaks()
+    tc = args.precision != "fp32"
+    if tc:
+        peak_val, peak_src = pk.get("bf16_tflops_sustained", 1400.0) / (1.0 if args.precision == "bf16" else 2.0), \
+            "MEASURED_PEAKS.json bf16_tflops_sustained" + ("" if args.precision == "bf16" else " / 2 (tf32 rate)")
+    else:
+        sm_mhz = pk.get("sm_max_mhz", 1965.0)
+        peak_val, peak_src = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "derived FFMA peak 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
+    achieved = flops_round / (infer_ms_round / 1e3) / 1e12
+    roofline = {"bound": "tensor" if tc else "fp32-ffma", "kernel": "K2 inference (per round, all layers)",
+                "achieved": achieved, "peak": peak_val, "unit": "TFLOP/s", "frac": achieved / peak_val,
+                "peak_source": peak_src, "traffic": None}
+
+    # e2e through the public C-ABI with host buffers (pinned), copies inside
+    e2e_line = None
+    if rank == 0 or world > 1:
+        ptrace = pinned_trace(trace)
+        e2e_s = []
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            g.simulate_parallel(ptrace, pc)
+            e2e_s.append(time.perf_counter() - t1)
+        e2e_t = torch.tensor([statistics.median(e2e_s)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+        h2d = trace_h2d_bytes(trace)
+        d2h = args.k * 56 + trace.n * 4
+        e2e_line = {"value": n_all / e2e_t.item() / 1e6, "unit": "MIPS", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "scope": "ilsim_gpu_simulate_parallel: H2D trace + pack + rounds + "
+                                                        "D2H sub-results and predicted fetch series (wall clock)"}
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu_base, _ = cpu_reference(trace, model, args.k, args.cpu_rounds or 48)
+        except Exception as e:  # the baseline is reported, never the product
+            cpu_base = {"value": None, "error": str(e)}
+    if world > 1:
+        torch.distributed.barrier()
+    if rank != 0:
+        return
+    r0 = results[-1]
+    line = {
+        "metric": "simulated MIPS", "value": value, "unit": "MIPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision in ("fp32", "tf32x3") else args.precision,
+        "data": "synthetic trace + random-init C3 weights (reference init rule), resident in HBM",
+        "config": {"workload": f"c2: C3 CNN predictor, {args.n} instructions x {world} GPU(s), {args.k} sub-traces per GPU",
+                   "precision": args.precision, "regime": args.regime, "sub_traces": args.k * world,
+                   "instructions": n_all, "rounds": r0.rounds,
+                   "l2": "trace+state > 126 MB L2 per step (no flush needed)"},
+        "cpi": int(totals[0].item()) / max(n_all, 1),
+        "wall_ms_per_step": 1e3 * wall / args.steps,
+        "kernels_ms_per_step": k_ms,
+        "roofline": roofline,
+        "cpu_baseline": cpu_base,
+        "e2e": e2e_line,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

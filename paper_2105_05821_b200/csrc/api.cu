@@ -1,0 +1,603 @@
+// Host driver behind include/ilsim_gpu.h: validation with the reference's
+// error texts, partition / sharding, device layout, the round loop (CUDA
+// graphs of K1 -> K2 -> K3 per round), result collection.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ilsim_gpu.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "host_util.cuh"
+#include "model.cuh"
+#include "sim_kernels.cuh"
+
+using namespace simnet;
+
+namespace {
+
+uint32_t next_pow2(uint32_t v) {
+  uint32_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+std::vector<uint64_t> partition_starts(uint64_t n, uint64_t k) {  // parallel.cpp:9-24
+  if (k < 1 || k > std::max<uint64_t>(n, 1))
+    throw ApiError("sub-trace count " + std::to_string(k) + " out of range for trace of " +
+                   std::to_string(n));
+  std::vector<uint64_t> s(k);
+  const uint64_t base = n / k, rem = n % k;
+  uint64_t at = 0;
+  for (uint64_t i = 0; i < k; ++i) {
+    s[i] = at;
+    at += base + (i < rem ? 1 : 0);
+  }
+  return s;
+}
+
+// Sub-trace count per parallel.cpp:28-41 (the sequential driver is K=1).
+uint64_t derive_k(const ilsim_sim_config& c, uint64_t n) {
+  if (c.sequential) return 1;
+  uint64_t k = c.k;
+  if (c.subtrace_size > 0) {
+    const uint64_t derived = n == 0 ? 1 : (n + c.subtrace_size - 1) / c.subtrace_size;
+    if (k == 0)
+      k = derived;
+    else if (k != derived)
+      throw ApiError("inconsistent partition: k=" + std::to_string(k) + " but subtrace size " +
+                     std::to_string(c.subtrace_size) + " implies k=" + std::to_string(derived));
+  }
+  if (k == 0) k = 1;
+  if (c.batch_max == 0) throw ApiError("batch_max must be >= 1");
+  return k;
+}
+
+struct Plan {
+  uint64_t n = 0, k = 0, sb = 0, se = 0;  // trace length, sub-traces, shard range
+  std::vector<uint64_t> starts;
+  uint64_t g0 = 0, g1 = 0;                 // device trace slice [g0, g1)
+  uint64_t own0 = 0, own1 = 0;             // owned instructions of the shard
+};
+
+Plan make_plan(const ilsim_sim_config& c, uint64_t n) {
+  Plan p;
+  p.n = n;
+  p.k = derive_k(c, n);
+  if (n == 0) return p;
+  p.starts = partition_starts(n, p.k);
+  p.sb = c.shard_begin;
+  p.se = c.shard_end;
+  if (p.sb == 0 && p.se == 0) p.se = p.k;
+  if (p.sb >= p.se || p.se > p.k) throw ApiError("invalid shard range");
+  auto end_of = [&](uint64_t i) { return i + 1 < p.k ? p.starts[i + 1] : n; };
+  p.own0 = p.starts[p.sb];
+  p.own1 = end_of(p.se - 1);
+  p.g0 = p.own0 - std::min<uint64_t>(c.warmup, p.own0);
+  p.g1 = p.own1;
+  return p;
+}
+
+}  // namespace
+
+struct ilsim_gpu_ctx {
+  int device = 0;
+  int precision = ILSIM_PREC_FP32;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  std::string err;
+
+  // model
+  bool has_model = false;
+  ilsim_cnn_config cfg{};
+  std::vector<double> norm;
+  DevModel model;
+  NormConsts nc_host{};
+  DevBuf nc_dev;
+  uint64_t model_gen = 0;
+
+  // trace (device slice [g0, g1) of a trace of t_total instructions)
+  bool has_trace = false;
+  uint64_t t_total = 0, g0 = 0, g1 = 0;
+  bool has_truth = false;
+  uint64_t packed_gen = ~0ull;  // model_gen the static table was packed with
+  DevBuf pc, addr, op, src, dst, hist, truth, stat, iflags;
+
+  // run buffers
+  DevBuf state, proc, wq, x, y, act, pred_fetch;
+
+  // capture hook
+  uint32_t cap_round = UINT32_MAX;
+  float* cap_host = nullptr;
+  uint64_t cap_rows = 0;
+};
+
+namespace {
+
+void set_norm(ilsim_gpu_ctx* c, const double* norm) {
+  NormConsts& h = c->nc_host;
+  for (int k = 0; k < kSlots; ++k) {
+    h.mean[k] = norm ? norm[k] : 0.0;
+    h.sd[k] = norm ? norm[50 + k] : 1.0;
+    h.zero[k] = norm_slot(0, h.mean[k], h.sd[k]);
+    h.one[k] = norm_slot(1, h.mean[k], h.sd[k]);
+  }
+  for (int j = 0; j < 3; ++j) {
+    h.label_mean[j] = norm ? norm[100 + j] : 0.0;
+    h.label_sd[j] = norm ? norm[103 + j] : 1.0;
+  }
+  c->nc_dev.need(sizeof(NormConsts));
+  CUDA_OK(cudaMemcpy(c->nc_dev.p, &h, sizeof(NormConsts), cudaMemcpyHostToDevice));
+}
+
+template <typename T>
+void upload(DevBuf& b, const T* src, uint64_t count, cudaStream_t s) {
+  b.need(count * sizeof(T));
+  if (count) CUDA_OK(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// Effective max_context for a run (cmd_simulate: the model's, ilsim_main.cpp:141).
+int effective_mc(const ilsim_gpu_ctx* c, const ilsim_sim_config& cfg) {
+  if (cfg.max_context > 0) return cfg.max_context;
+  return c->has_model ? c->cfg.max_context : 110;
+}
+
+void pack_if_needed(ilsim_gpu_ctx* c, bool needs_input) {
+  const uint64_t n = c->g1 - c->g0;
+  if (c->packed_gen == c->model_gen && (!needs_input || c->stat.bytes >= n * kStatStride * 4)) return;
+  PackParams pp{};
+  pp.n = n;
+  pp.op = c->op.as<uint8_t>();
+  pp.src = c->src.as<uint16_t>();
+  pp.dst = c->dst.as<uint16_t>();
+  pp.hist = c->hist.as<uint16_t>();
+  pp.nc = c->nc_dev.as<NormConsts>();
+  pp.stat = needs_input ? static_cast<float*>(c->stat.need(n * kStatStride * sizeof(float))) : nullptr;
+  pp.iflags = static_cast<uint8_t*>(c->iflags.need(n));
+  launch_pack(pp, c->stream);
+  CUDA_OK(cudaGetLastError());
+  if (needs_input) c->packed_gen = c->model_gen;
+}
+
+void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* subs, uint64_t sub_cap,
+              uint32_t* predicted_fetch, ilsim_totals* tot) {
+  if (!c->has_trace) throw ApiError("no trace loaded");
+  const uint64_t n = c->t_total;
+  const bool oracle = cfg.oracle != 0;
+  const bool needs_input = !oracle || cfg.reserved[1] != 0;
+  const Plan P = make_plan(cfg, n);
+  const int mc = effective_mc(c, cfg);
+  std::memset(tot, 0, sizeof(*tot));
+
+  if (n == 0) {  // parallel.cpp:44-50 / simcore.cpp:167-174: one empty result
+    if (sub_cap < 1) throw ApiError("sub_cap too small");
+    subs[0] = ilsim_sub_result{0, 0, 0, 0, 0, 0, 1};
+    tot->sub_traces = 1;
+    return;
+  }
+  // SimCore ctor checks (simcore.cpp:13-18)
+  if (mc < 1) throw ApiError("max_context must be >= 1");
+  if (cfg.retire_bandwidth < 1) throw ApiError("retire_bandwidth must be >= 1");
+  if (needs_input && !c->has_model)
+    throw ApiError("predictor requires inputs but provides no normalization stats");
+  if (oracle && !c->has_truth) throw ApiError("oracle mode requires truth latencies");
+  if (needs_input && !oracle && mc != c->cfg.max_context) throw ApiError("max_context differs from the model's");
+  if (needs_input && mc + 1 > kMaxCols) throw ApiError("max_context too large for the GPU gather");
+  if (P.g0 != c->g0 || P.g1 != c->g1) throw ApiError("loaded trace slice does not match this configuration");
+
+  const uint64_t K = P.se - P.sb;
+  if (K > sub_cap) throw ApiError("sub_cap too small");
+  const uint32_t pcap = next_pow2(static_cast<uint32_t>(mc));
+  const uint32_t wcap = next_pow2(cfg.write_ring > 0 ? static_cast<uint32_t>(cfg.write_ring) : 2048u);
+
+  // per-sub-trace initial state
+  std::vector<SubState> hs(K);
+  uint32_t rounds = 0;
+  for (uint64_t j = 0; j < K; ++j) {
+    const uint64_t i = P.sb + j;
+    const uint64_t s = P.starts[i];
+    const uint64_t e = i + 1 < P.k ? P.starts[i + 1] : n;
+    const uint64_t w = std::min<uint64_t>(cfg.warmup, s);
+    SubState& st = hs[j];
+    std::memset(&st, 0, sizeof(st));
+    st.begin = s - w - P.g0;
+    st.len = static_cast<uint32_t>(e - s + w);
+    st.warm = static_cast<uint32_t>(w);
+    st.fetch_off = s - P.own0;
+    st.count_drain = (cfg.drain_trim && i + 1 < P.k) ? 0u : 1u;
+    rounds = std::max(rounds, st.len);
+  }
+  if (needs_input) pack_if_needed(c, true);
+  else if (c->packed_gen == ~0ull || c->iflags.bytes < (P.g1 - P.g0)) pack_if_needed(c, false);
+
+  SubState* d_state = static_cast<SubState*>(c->state.need(K * sizeof(SubState)));
+  CUDA_OK(cudaMemcpyAsync(d_state, hs.data(), K * sizeof(SubState), cudaMemcpyHostToDevice, c->stream));
+  RingEntry* d_proc = static_cast<RingEntry*>(c->proc.need(K * pcap * sizeof(RingEntry)));
+  RingEntry* d_wq = static_cast<RingEntry*>(c->wq.need(K * wcap * sizeof(RingEntry)));
+  const uint64_t owned = P.own1 - P.own0;
+  uint32_t* d_pf = cfg.record_fetch ? static_cast<uint32_t*>(c->pred_fetch.need(owned * 4)) : nullptr;
+
+  // chunking of the batch (bounds activation memory; results are batch-independent)
+  const uint64_t chunk = std::min<uint64_t>(K, 65536);
+  const uint32_t x_stride = needs_input ? input_row_floats(mc) : 0;
+  float* d_x = needs_input ? static_cast<float*>(c->x.need(chunk * x_stride * sizeof(float))) : nullptr;
+  ForwardBuffers fb{};
+  if (!oracle) fb = forward_buffers(c->model, chunk, c->act, c->y);
+
+  auto do_ctx = [&](uint64_t f, uint64_t l, bool gather) {
+    CtxParams cp{};
+    cp.state = d_state;
+    cp.proc = d_proc;
+    cp.wq = d_wq;
+    cp.pmask = pcap - 1;
+    cp.wmask = wcap - 1;
+    cp.first = f;
+    cp.last = l;
+    cp.stat = c->stat.as<float>();
+    cp.pc = c->pc.as<uint64_t>();
+    cp.addr = c->addr.as<uint64_t>();
+    cp.iflags = c->iflags.as<uint8_t>();
+    cp.nc = c->nc_dev.as<NormConsts>();
+    cp.x = d_x;
+    cp.x_stride = x_stride;
+    cp.max_context = mc;
+    cp.bw = cfg.retire_bandwidth;
+    cp.line = cfg.line_size;
+    cp.page = cfg.page_size;
+    cp.per_cycle = cfg.per_cycle_advance;
+    cp.gather = gather && needs_input;
+    launch_ctx(cp, c->stream);
+    return uint64_t{1};
+  };
+  auto do_forward = [&](uint64_t f, uint64_t l) -> uint64_t {
+    if (oracle) return 0;
+    return forward_launch(c->model, c->precision, d_x, x_stride, l - f, fb, c->stream);
+  };
+  auto do_decode = [&](uint64_t f, uint64_t l) {
+    DecodeParams dp{};
+    dp.state = d_state;
+    dp.first = f;
+    dp.last = l;
+    dp.y = fb.y;
+    dp.y_stride = fb.y_stride;
+    dp.truth = oracle ? c->truth.as<uint32_t>() : nullptr;
+    dp.iflags = c->iflags.as<uint8_t>();
+    dp.nc = c->nc_dev.as<NormConsts>();
+    dp.pred_fetch = d_pf;
+    dp.class_fetch = c->cfg.class_fetch;
+    dp.class_exec = c->cfg.class_exec;
+    dp.class_store = c->cfg.class_store;
+    dp.per_cycle = cfg.per_cycle_advance;
+    launch_decode(dp, c->stream);
+    return uint64_t{1};
+  };
+  auto launch_round = [&]() -> uint64_t {
+    uint64_t launches = 0;
+    for (uint64_t f = 0; f < K; f += chunk) {
+      const uint64_t l = std::min(K, f + chunk);
+      launches += do_ctx(f, l, true);
+      launches += do_forward(f, l);
+      launches += do_decode(f, l);
+    }
+    return launches;
+  };
+
+  const bool capture_mode = c->cap_round != UINT32_MAX;
+  if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
+  const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs
+  constexpr uint32_t kGraphRounds = 16;
+  cudaGraphExec_t g1 = nullptr, gN = nullptr;
+  uint64_t launches_per_round = 0;
+  if (!capture_mode && !profile) {
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t reps = which == 0 ? 1 : kGraphRounds;
+      if (which == 1 && rounds < kGraphRounds) break;
+      cudaGraph_t g;
+      CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      for (uint32_t r = 0; r < reps; ++r) launches_per_round = launch_round();
+      CUDA_OK(cudaStreamEndCapture(c->stream, &g));
+      CUDA_OK(cudaGraphInstantiate(which == 0 ? &g1 : &gN, g, 0));
+      cudaGraphDestroy(g);
+    }
+  }
+
+  CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+  uint64_t launches = 0;
+  double kms[4] = {0, 0, 0, 0};
+  if (capture_mode || profile) {
+    for (uint32_t r = 0; r < rounds; ++r) {
+      for (uint64_t f = 0; f < K; f += chunk) {
+        const uint64_t l = std::min(K, f + chunk);
+        if (profile) CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
+        launches += do_ctx(f, l, true);
+        if (profile) CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
+        if (capture_mode && r == c->cap_round && needs_input) {
+          const uint32_t width = static_cast<uint32_t>(kSlots * (mc + 1));
+          const uint64_t rows = std::min<uint64_t>(c->cap_rows, l - f);
+          CUDA_OK(cudaMemcpy2DAsync(c->cap_host, width * sizeof(float), d_x, x_stride * sizeof(float),
+                                    width * sizeof(float), rows, cudaMemcpyDeviceToHost, c->stream));
+        }
+        launches += do_forward(f, l);
+        if (profile) CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
+        launches += do_decode(f, l);
+        if (profile) {
+          CUDA_OK(cudaEventRecord(c->ev[5], c->stream));
+          CUDA_OK(cudaEventSynchronize(c->ev[5]));
+          float a = 0, b = 0, d = 0;
+          CUDA_OK(cudaEventElapsedTime(&a, c->ev[2], c->ev[3]));
+          CUDA_OK(cudaEventElapsedTime(&b, c->ev[3], c->ev[4]));
+          CUDA_OK(cudaEventElapsedTime(&d, c->ev[4], c->ev[5]));
+          kms[0] += a;
+          kms[1] += b;
+          kms[2] += d;
+        }
+      }
+    }
+  } else {
+    uint32_t r = 0;
+    while (gN && r + kGraphRounds <= rounds) {
+      CUDA_OK(cudaGraphLaunch(gN, c->stream));
+      r += kGraphRounds;
+    }
+    for (; r < rounds; ++r) CUDA_OK(cudaGraphLaunch(g1, c->stream));
+    launches += launches_per_round * rounds;
+  }
+  for (uint64_t f = 0; f < K; f += chunk) launches += do_ctx(f, std::min(K, f + chunk), false);  // apply final step, drain
+  CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaEventSynchronize(c->ev[1]));
+  if (g1) cudaGraphExecDestroy(g1);
+  if (gN) cudaGraphExecDestroy(gN);
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+
+  CUDA_OK(cudaMemcpy(hs.data(), d_state, K * sizeof(SubState), cudaMemcpyDeviceToHost));
+  if (predicted_fetch && d_pf)
+    CUDA_OK(cudaMemcpy(predicted_fetch, d_pf, owned * 4, cudaMemcpyDeviceToHost));
+
+  for (uint64_t j = 0; j < K; ++j) {
+    const SubState& st = hs[j];
+    const uint64_t i = P.sb + j;
+    if (st.status == kErrStall)
+      throw ApiError("processor queue stalled without progress at tick " + std::to_string(st.err_tick) +
+                     " (sub-trace " + std::to_string(i) + ")");
+    if (st.status == kErrDrain)
+      throw ApiError("drain made no progress at tick " + std::to_string(st.err_tick) + " (sub-trace " +
+                     std::to_string(i) + ")");
+    if (st.status == kErrWriteRing)
+      throw ApiError("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
+                     std::to_string(i) + "; raise write_ring");
+    if (st.pos != st.len) throw ApiError("internal: sub-trace did not finish");
+    ilsim_sub_result& r = subs[j];
+    r.instructions = st.len - st.warm;
+    r.total_cycles = st.cur - st.base_cur;
+    r.sum_fetch = st.sum_fetch;
+    r.delta = r.total_cycles - r.sum_fetch;
+    r.drain_cycles = st.drain;
+    r.overflow_stall_cycles = st.overflow - st.base_overflow;
+    r.empty = r.instructions == 0;
+    tot->total_cycles += r.total_cycles;
+    tot->sum_fetch += r.sum_fetch;
+    tot->delta += r.delta;
+    tot->drain_cycles += r.drain_cycles;
+    tot->overflow_stall_cycles += r.overflow_stall_cycles;
+    tot->instructions += r.instructions;
+  }
+  tot->sub_traces = K;
+  tot->rounds = rounds;
+  tot->cpi = tot->instructions ? static_cast<double>(tot->total_cycles) / tot->instructions : 0.0;
+  tot->device_ms = ms;
+  for (int q = 0; q < 4; ++q) tot->kernel_ms[q] = kms[q];
+  tot->launches = launches;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+// C-ABI
+// --------------------------------------------------------------------------
+namespace {
+void put_err(char* err, int n, const std::string& m) {
+  if (err && n > 0) {
+    std::strncpy(err, m.c_str(), static_cast<size_t>(n) - 1);
+    err[n - 1] = 0;
+  }
+}
+
+template <typename F>
+int guard(ilsim_gpu_ctx* c, F&& f) {
+  try {
+    if (c) CUDA_OK(cudaSetDevice(c->device));
+    f();
+    if (c) c->err.clear();
+    return 0;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ilsim_gpu_abi_version(void) { return ILSIM_GPU_ABI_VERSION; }
+
+int ilsim_gpu_create(const ilsim_gpu_options* o, ilsim_gpu_ctx** out, char* err, int errlen) {
+  try {
+    auto c = std::make_unique<ilsim_gpu_ctx>();
+    c->device = o ? o->device : 0;
+    c->precision = o ? o->precision : ILSIM_PREC_FP32;
+    if (c->precision < ILSIM_PREC_FP32 || c->precision > ILSIM_PREC_BF16)
+      throw ApiError("unknown precision");
+    int count = 0;
+    CUDA_OK(cudaGetDeviceCount(&count));
+    if (c->device < 0 || c->device >= count) throw ApiError("CUDA device out of range");
+    CUDA_OK(cudaSetDevice(c->device));
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major != 10) throw ApiError("this build targets sm_100a (B200); found sm_" +
+                                         std::to_string(prop.major) + std::to_string(prop.minor));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CUDA_OK(cudaEventCreate(&e));
+    set_norm(c.get(), nullptr);
+    *out = c.release();
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+void ilsim_gpu_destroy(ilsim_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* ilsim_gpu_last_error(const ilsim_gpu_ctx* c) { return c ? c->err.c_str() : ""; }
+
+int ilsim_gpu_load_model(ilsim_gpu_ctx* c, const ilsim_cnn_config* cfg, const double* norm,
+                         const float* params, uint64_t n_params) {
+  return guard(c, [&] {
+    validate_config(*cfg);
+    if (n_params != param_count_of(*cfg)) throw ApiError("model parameter count mismatch");
+    c->cfg = *cfg;
+    c->norm.assign(norm, norm + 106);
+    set_norm(c, norm);
+    model_upload(c->model, *cfg, params, c->precision, c->stream);
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->has_model = true;
+    ++c->model_gen;
+  });
+}
+
+int ilsim_gpu_load_trace(ilsim_gpu_ctx* c, const ilsim_trace_view* t, const ilsim_sim_config* cfg) {
+  return guard(c, [&] {
+    const Plan P = make_plan(*cfg, t->n);
+    c->has_trace = false;
+    c->t_total = t->n;
+    c->g0 = P.g0;
+    c->g1 = P.g1;
+    const uint64_t g0 = P.g0, m = P.g1 - P.g0;
+    upload(c->pc, t->pc + g0, m, c->stream);
+    upload(c->addr, t->data_addr + g0, m, c->stream);
+    upload(c->op, t->op + 13 * g0, 13 * m, c->stream);
+    upload(c->src, t->src + 8 * g0, 8 * m, c->stream);
+    upload(c->dst, t->dst + 6 * g0, 6 * m, c->stream);
+    upload(c->hist, t->hist + 14 * g0, 14 * m, c->stream);
+    c->has_truth = t->truth != nullptr;
+    if (c->has_truth) upload(c->truth, t->truth + 3 * g0, 3 * m, c->stream);
+    c->packed_gen = ~0ull;
+    c->iflags.need(m);
+    // static slots depend on the model's NormStats: pack now if a model is loaded
+    if (m) {
+      PackParams pp{};
+      pp.n = m;
+      pp.op = c->op.as<uint8_t>();
+      pp.src = c->src.as<uint16_t>();
+      pp.dst = c->dst.as<uint16_t>();
+      pp.hist = c->hist.as<uint16_t>();
+      pp.nc = c->nc_dev.as<NormConsts>();
+      pp.stat = c->has_model ? static_cast<float*>(c->stat.need(m * kStatStride * sizeof(float))) : nullptr;
+      pp.iflags = c->iflags.as<uint8_t>();
+      launch_pack(pp, c->stream);
+      CUDA_OK(cudaGetLastError());
+      if (c->has_model) c->packed_gen = c->model_gen;
+    }
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->has_trace = true;
+  });
+}
+
+int ilsim_gpu_run(ilsim_gpu_ctx* c, const ilsim_sim_config* cfg, ilsim_sub_result* subs, uint64_t sub_cap,
+                  uint32_t* predicted_fetch, ilsim_totals* totals) {
+  return guard(c, [&] { run_impl(c, *cfg, subs, sub_cap, predicted_fetch, totals); });
+}
+
+int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, const ilsim_sim_config* cfg,
+                                ilsim_sub_result* subs, uint64_t sub_cap, uint32_t* predicted_fetch,
+                                ilsim_totals* totals) {
+  if (ilsim_gpu_load_trace(c, t, cfg) != 0) return 1;
+  return ilsim_gpu_run(c, cfg, subs, sub_cap, predicted_fetch, totals);
+}
+
+int ilsim_gpu_predict(ilsim_gpu_ctx* c, const float* inputs, uint64_t n, const uint8_t* is_store,
+                      float* outputs, uint32_t* triples) {
+  return guard(c, [&] {
+    if (!c->has_model) throw ApiError("no model loaded");
+    if (n == 0) return;
+    const int mc = c->cfg.max_context;
+    const uint32_t width = static_cast<uint32_t>(kSlots * (mc + 1));
+    const uint32_t x_stride = input_row_floats(mc);
+    const uint64_t chunk = std::min<uint64_t>(n, 65536);
+    float* d_x = static_cast<float*>(c->x.need(chunk * x_stride * sizeof(float)));
+    ForwardBuffers fb = forward_buffers(c->model, chunk, c->act, c->y);
+    DevBuf d_store, d_trip;
+    uint8_t* ds = static_cast<uint8_t*>(d_store.need(chunk));
+    uint32_t* dt = static_cast<uint32_t*>(d_trip.need(chunk * 12));
+    for (uint64_t f = 0; f < n; f += chunk) {
+      const uint64_t m = std::min(chunk, n - f);
+      CUDA_OK(cudaMemsetAsync(d_x, 0, m * x_stride * sizeof(float), c->stream));
+      CUDA_OK(cudaMemcpy2DAsync(d_x, x_stride * sizeof(float), inputs + f * width, width * sizeof(float),
+                                width * sizeof(float), m, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(ds, is_store + f, m, cudaMemcpyHostToDevice, c->stream));
+      forward_launch(c->model, c->precision, d_x, x_stride, m, fb, c->stream);
+      launch_decode_only(fb.y, fb.y_stride, m, ds, c->nc_dev.as<NormConsts>(), c->cfg.class_fetch,
+                         c->cfg.class_exec, c->cfg.class_store, dt, c->stream);
+      CUDA_OK(cudaGetLastError());
+      const int od = output_dim_of(c->cfg);
+      if (outputs)
+        CUDA_OK(cudaMemcpy2DAsync(outputs + f * od, od * sizeof(float), fb.y, fb.y_stride * sizeof(float),
+                                  od * sizeof(float), m, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaMemcpyAsync(triples + 3 * f, dt, m * 12, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaStreamSynchronize(c->stream));
+    }
+  });
+}
+
+int ilsim_gpu_set_capture(ilsim_gpu_ctx* c, uint32_t round, float* inputs, uint64_t rows) {
+  return guard(c, [&] {
+    c->cap_round = round;
+    c->cap_host = inputs;
+    c->cap_rows = rows;
+  });
+}
+
+int ilsim_gpu_partition(uint64_t n, uint64_t k, uint64_t* starts, char* err, int errlen) {
+  try {
+    const auto s = partition_starts(n, k);
+    std::copy(s.begin(), s.end(), starts);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+uint64_t ilsim_gpu_model_flops(const ilsim_cnn_config* cfg) { return model_flops_of(*cfg); }
+uint64_t ilsim_gpu_param_count(const ilsim_cnn_config* cfg) { return param_count_of(*cfg); }
+
+int ilsim_gpu_init_weights(const ilsim_cnn_config* cfg, uint64_t seed, float* params, uint64_t n, char* err,
+                           int errlen) {
+  try {
+    validate_config(*cfg);
+    if (n != param_count_of(*cfg)) throw ApiError("parameter buffer size mismatch");
+    init_weights_into(*cfg, seed, params);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,28 @@
+// K2 (latency-predictor inference) layer GEMM interfaces.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace simnet {
+
+// One CNN layer as a GEMM over (sample, position) rows: the k2/s2 window of
+// output position p is input rows 2p, 2p+1 laid end to end, so every layer's
+// input is the previous output viewed as [rows/2 x 2*channels] (cnn.cpp:97-98).
+struct LayerGemm {
+  const float* a;          // input activations
+  uint64_t m;              // output rows = samples * rows_per_sample
+  int rows_per_sample;     // output positions per sample
+  int valid_rows;          // rows stored per sample; rows >= valid_rows read as 0
+  int kdim;                // 2 * input channels (or flat dim for FC)
+  uint64_t sample_stride;  // floats between samples in `a`
+  const float* w;          // [kdim][n], n contiguous (reference column-major)
+  const float* w2;         // residual projection, same layout (or null)
+  const float* bias;       // [n]
+  float* c;                // [m][ldc]
+  int n, ldc;
+  int relu;
+};
+
+void launch_sgemm(const LayerGemm& g, cudaStream_t stream);
+
+}  // namespace simnet

@@ -1,0 +1,96 @@
+// FP32 SIMT path of K2 (precision ILSIM_PREC_FP32): one tiled FFMA GEMM per
+// layer, C = act(A * W + b) with the reference's parameter layout
+// (column-major W[o + k*rows] == [K x N] N-contiguous, cnn.cpp:99-124).
+// The fp32 correctness anchor for the tensor-core paths; products are exact
+// fp32 FMAs accumulated k-ascending per output, then bias, then ReLU.
+#include "gemm.cuh"
+
+namespace simnet {
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN];
+  __shared__ float Ps[BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const uint64_t row0 = static_cast<uint64_t>(blockIdx.x) * BM;
+  const int col0 = blockIdx.y * BN;
+
+  // A-tile loader: row (tid / 4), k chunk (tid % 4) * 4
+  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  const uint64_t gr = row0 + lr;
+  const float* arow = nullptr;
+  if (gr < g.m) {
+    const uint64_t sidx = gr / g.rows_per_sample;
+    const int pidx = static_cast<int>(gr - sidx * g.rows_per_sample);
+    if (pidx < g.valid_rows) arow = g.a + sidx * g.sample_stride + static_cast<uint64_t>(pidx) * g.kdim;
+  }
+  // B-tile loader: k (tid / 16), n chunk (tid % 16) * 4
+  const int bk = tid >> 4, bn = (tid & 15) * 4;
+
+  float acc[4][4] = {};
+  float acp[4][4] = {};
+  for (int k0 = 0; k0 < g.kdim; k0 += BK) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = k0 + lk + t;
+      As[lk + t][lr] = (arow && k < g.kdim) ? arow[k] : 0.0f;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = k0 + bk, n = col0 + bn + t;
+      const bool ok = k < g.kdim && n < g.n;
+      Bs[bk][bn + t] = ok ? g.w[static_cast<uint64_t>(k) * g.n + n] : 0.0f;
+      if (g.w2) Ps[bk][bn + t] = ok ? g.w2[static_cast<uint64_t>(k) * g.n + n] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      if (g.w2) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Ps[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acp[i][j] = fmaf(a[i], b[j], acp[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t r = row0 + ty + 16 * i;
+    if (r >= g.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = col0 + tx + 16 * j;
+      if (n >= g.n) continue;
+      float v = acc[i][j];
+      if (g.w2) v += acp[i][j];
+      v += g.bias[n];
+      if (g.relu) v = fmaxf(v, 0.0f);
+      g.c[r * g.ldc + n] = v;
+    }
+  }
+}
+}  // namespace
+
+void launch_sgemm(const LayerGemm& g, cudaStream_t stream) {
+  if (g.m == 0) return;
+  dim3 grid(static_cast<unsigned>((g.m + BM - 1) / BM), (g.n + BN - 1) / BN);
+  sgemm_kernel<<<grid, 256, 0, stream>>>(g);
+}
+
+}  // namespace simnet

@@ -1,0 +1,64 @@
+// Latency-predictor model on the device: CnnConfig checks and parameter
+// layout (cnn.cpp:44-86, 229-352), weight upload in the operand layouts each
+// K2 precision needs, and the per-chunk forward dispatch.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/ilsim_gpu.h"
+#include "host_util.cuh"
+
+namespace simnet {
+
+struct ParamLayout {
+  std::vector<uint64_t> w, b, p;  // per conv layer (p: residual projection)
+  uint64_t fc1_w = 0, fc1_b = 0, fc2_w = 0, fc2_b = 0, total = 0;
+  int out_dim = 0, flat = 0;
+};
+
+ParamLayout param_layout(const ilsim_cnn_config& c);
+void validate_config(const ilsim_cnn_config& c);
+uint64_t param_count_of(const ilsim_cnn_config& c);
+uint64_t model_flops_of(const ilsim_cnn_config& c);
+int output_dim_of(const ilsim_cnn_config& c);
+void init_weights_into(const ilsim_cnn_config& c, uint64_t seed, float* params);
+
+// Floats per gathered sample row on the device: the 50*(mc+1) model input
+// rounded up to whole conv0 windows (2 columns = 100 floats per row).
+inline uint32_t input_row_floats(int max_context) {
+  return 100u * static_cast<uint32_t>((max_context + 2) / 2);
+}
+
+struct TcModel;  // tensor-core operand copies (gemm_tc.cu)
+
+struct DevModel {
+  ilsim_cnn_config cfg{};
+  ParamLayout L;
+  DevBuf params;          // reference layout, f32
+  TcModel* tc = nullptr;  // owned; null for the FP32 SIMT path
+  DevModel() = default;
+  DevModel(const DevModel&) = delete;
+  DevModel& operator=(const DevModel&) = delete;
+  ~DevModel();
+};
+
+struct ForwardBuffers {
+  float* act[9];       // conv outputs (act[0..n_conv-1]), hidden (act[n_conv])
+  float* y;            // head outputs
+  uint32_t y_stride;
+};
+
+void model_upload(DevModel& m, const ilsim_cnn_config& c, const float* params, int precision,
+                  cudaStream_t s);
+ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, DevBuf& y);
+// Runs the forward for `samples` gathered rows; returns kernels launched.
+uint64_t forward_launch(const DevModel& m, int precision, const float* x, uint32_t x_stride,
+                        uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
+
+// tensor-core path (gemm_tc.cu)
+TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s);
+void tc_model_destroy(TcModel* t);
+uint64_t tc_forward(const DevModel& m, int precision, const float* x, uint32_t x_stride,
+                    uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
+
+}  // namespace simnet

@@ -1,0 +1,376 @@
+// K1 (context-queue), K3 (decode + clock) and the trace pack kernel.
+//
+// K1 replaces, per sub-trace and per round, SimCore::apply_step's retire /
+// stall / push half (simcore.cpp:112-150 after the fetch advance), drain
+// (simcore.cpp:152-159) and next_request (simcore.cpp:25-66).  One warp owns
+// one sub-trace: ring heads are scanned 32 entries at a time with ballots
+// (in-order retirement = the run of leading ready entries), store moves to
+// the write queue are a ballot/popc compaction, and the gathered context is
+// staged per column in shared memory and written as coalesced float4 rows.
+//
+// K3 replaces decode_hybrid (cnn.cpp:388-417) plus the clock half of
+// apply_step (advance_cycles(F, bw*F), simcore.cpp:117-123, 147-149).
+#include "common.cuh"
+#include "sim_kernels.cuh"
+
+namespace simnet {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint32_t leading_run(uint32_t mask) {
+  return mask == kFull ? 32u : static_cast<uint32_t>(__ffs(~mask) - 1);
+}
+
+struct Rings {
+  RingEntry* proc;
+  RingEntry* wq;
+  uint32_t pmask, wmask, wcap;
+};
+
+// SimCore::retire (simcore.cpp:68-84).  Warp-uniform in/out; returns the
+// number of queue transitions.  Sets *err on write-ring overflow.
+__device__ uint32_t warp_retire(uint64_t cur, uint64_t budget, const Rings& r, uint32_t& ph,
+                                uint32_t pt, uint32_t& wh, uint32_t& wt, uint32_t* err) {
+  const uint32_t lane = lane_id();
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t events = 0;
+  while (budget > 0 && ph != pt) {
+    const uint32_t n = min(pt - ph, 32u);
+    RingEntry e;
+    bool ready = false;
+    if (lane < n) {
+      e = r.proc[(ph + lane) & r.pmask];
+      ready = (cur - e.push) >= e.exec;
+    }
+    const uint32_t run = leading_run(__ballot_sync(kFull, ready));
+    const uint32_t take = static_cast<uint32_t>(min(static_cast<uint64_t>(run), budget));
+    const bool mv = lane < take && e.is_store;
+    const uint32_t sm = __ballot_sync(kFull, mv);
+    const uint32_t nmv = __popc(sm);
+    if (wt + nmv - wh > r.wcap) {
+      *err = kErrWriteRing;
+      return events;
+    }
+    if (mv) r.wq[(wt + __popc(sm & lt)) & r.wmask] = e;
+    wt += nmv;
+    ph += take;
+    budget -= take;
+    events += take;
+    if (take < n) break;
+  }
+  while (wh != wt) {
+    const uint32_t n = min(wt - wh, 32u);
+    bool ready = false;
+    if (lane < n) {
+      const RingEntry& e = r.wq[(wh + lane) & r.wmask];
+      ready = (cur - e.push) >= e.store;
+    }
+    const uint32_t run = leading_run(__ballot_sync(kFull, ready));
+    wh += run;
+    events += run;
+    if (run < n) break;
+  }
+  __syncwarp();
+  return events;
+}
+
+// readiness gap of a head entry (simcore.cpp:95-110 per queue)
+__device__ __forceinline__ uint64_t head_gap(uint64_t cur, uint64_t push, uint32_t lat) {
+  const uint64_t res = cur - push;
+  return lat > res ? lat - res : 1;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// K1: apply the pending step, drain finished sub-traces, gather the next input.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCtxWarps * 32)
+ctx_kernel(CtxParams p) {
+  __shared__ uint32_t s_inst[kCtxWarps][kMaxCols];
+  __shared__ float s_res[kCtxWarps][kMaxCols];
+  __shared__ float s_exe[kCtxWarps][kMaxCols];
+  __shared__ float s_sto[kCtxWarps][kMaxCols];
+  __shared__ uint8_t s_flg[kCtxWarps][kMaxCols];
+
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kCtxWarps + warp + p.first;
+  if (s >= p.last) return;
+
+  SubState* sp = p.state + s;
+  SubState st = *sp;  // every lane holds a copy; lane 0 writes back
+  if (st.status != kOk) return;
+  const NormConsts& nc = *p.nc;
+  Rings r{p.proc + s * (p.pmask + 1ull), p.wq + s * (p.wmask + 1ull), p.pmask, p.wmask, p.wmask + 1u};
+  uint32_t err = kOk;
+
+  if (st.has_pend) {
+    const uint32_t F = st.pend_f;
+    // fetch advance: K3 already moved cur by F (lumped); retire with budget bw*F
+    if (F > 0) {
+      if (p.per_cycle) {
+        for (uint32_t c = 0; c < F && err == kOk; ++c) {
+          st.cur += 1;
+          warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+        }
+      } else {
+        warp_retire(st.cur, static_cast<uint64_t>(p.bw) * F, r, st.ph, st.pt, st.wh, st.wt, &err);
+      }
+    }
+    // forced stall (simcore.cpp:127-136): budget bw, not bw*gap
+    while (err == kOk && st.pt - st.ph >= static_cast<uint32_t>(p.max_context)) {
+      const uint32_t before = st.pt - st.ph;
+      const RingEntry& h = r.proc[st.ph & r.pmask];
+      const uint64_t gap = head_gap(st.cur, h.push, h.exec);
+      st.cur += gap;
+      st.overflow += gap;
+      warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+      if (err == kOk && st.pt - st.ph >= before) {
+        err = kErrStall;
+        st.err_tick = st.cur;
+      }
+    }
+    if (err == kOk) {  // push (simcore.cpp:138-145)
+      if (lane == 0) {
+        RingEntry e;
+        e.push = st.cur;
+        e.idx = st.pos;
+        e.exec = st.pend_e;
+        e.store = st.pend_s;
+        e.nexec = norm_slot(static_cast<int32_t>(st.pend_e), nc.mean[kSlotExecution], nc.sd[kSlotExecution]);
+        e.nstore = norm_slot(static_cast<int32_t>(st.pend_s), nc.mean[kSlotStore], nc.sd[kSlotStore]);
+        e.is_store = (p.iflags[st.begin + st.pos] & kFlagStore) ? 1u : 0u;
+        r.proc[st.pt & r.pmask] = e;
+      }
+      st.pt += 1;
+      st.pos += 1;
+      st.has_pend = 0;
+      if (st.pos == st.warm) {  // warm-up extension: counting starts after this step
+        st.base_cur = st.cur;
+        st.base_overflow = st.overflow;
+      }
+      // drain right after the last step (parallel.cpp:79, simcore.cpp:152-159)
+      if (st.pos == st.len && st.count_drain) {
+        while (err == kOk && (st.ph != st.pt || st.wh != st.wt)) {
+          uint64_t gap = ~uint64_t{0};
+          if (st.ph != st.pt) {
+            const RingEntry& h = r.proc[st.ph & r.pmask];
+            { const uint64_t g = head_gap(st.cur, h.push, h.exec); gap = g < gap ? g : gap; }
+          }
+          if (st.wh != st.wt) {
+            const RingEntry& h = r.wq[st.wh & r.wmask];
+            { const uint64_t g = head_gap(st.cur, h.push, h.store); gap = g < gap ? g : gap; }
+          }
+          if (gap < 1) gap = 1;
+          st.cur += gap;
+          st.drain += gap;
+          const uint32_t ev = warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+          if (err == kOk && ev == 0) {
+            err = kErrDrain;
+            st.err_tick = st.cur;
+          }
+        }
+      }
+    }
+    if (err != kOk) st.status = err;
+    __syncwarp();
+    if (lane == 0) *sp = st;
+    __syncwarp();
+  }
+
+  if (!p.gather || st.status != kOk || st.pos >= st.len) return;
+
+  // ---- gather (simcore.cpp:25-66) --------------------------------------
+  const uint64_t tgt = st.begin + st.pos;
+  const uint32_t nproc = st.pt - st.ph;
+  const uint32_t nwq = st.wt - st.wh;
+  const uint32_t ncols = min(static_cast<uint32_t>(p.max_context), nproc + nwq);
+  const uint64_t tpc = p.pc[tgt];
+  const uint64_t taddr = p.addr[tgt];
+  const bool tmem = (p.iflags[tgt] & kFlagMem) != 0;
+  for (uint32_t c = lane; c <= ncols; c += 32) {
+    if (c == 0) {
+      s_inst[warp][0] = static_cast<uint32_t>(tgt);
+      s_res[warp][0] = nc.zero[kSlotResidence];
+      s_exe[warp][0] = nc.zero[kSlotExecution];
+      s_sto[warp][0] = nc.zero[kSlotStore];
+      s_flg[warp][0] = 0;
+      continue;
+    }
+    const uint32_t j = c - 1;  // newest first: proc queue, then write queue
+    const RingEntry e = j < nproc ? r.proc[(st.pt - 1 - j) & r.pmask]
+                                  : r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
+    const uint64_t inst = st.begin + e.idx;
+    const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e.push));
+    s_inst[warp][c] = static_cast<uint32_t>(inst);
+    s_res[warp][c] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
+    s_exe[warp][c] = e.nexec;
+    s_sto[warp][c] = e.nstore;
+    // memory_dependency_flags (dataset.cpp:47-60)
+    const uint64_t cpc = p.pc[inst];
+    uint32_t f = (tpc / p.line) == (cpc / p.line) ? 1u : 0u;
+    if (tmem && (p.iflags[inst] & kFlagMem)) {
+      const uint64_t ca = p.addr[inst];
+      f |= (taddr == ca) ? 2u : 0u;
+      f |= (taddr / p.line) == (ca / p.line) ? 4u : 0u;
+      f |= (taddr / p.page) == (ca / p.page) ? 8u : 0u;
+    }
+    f |= (tpc / p.page) == (cpc / p.page) ? 16u : 0u;
+    s_flg[warp][c] = static_cast<uint8_t>(f);
+  }
+  __syncwarp();
+
+  // Coalesced write of the whole sample row: columns > ncols are exactly 0.
+  float4* out = reinterpret_cast<float4*>(p.x + (s - p.first) * static_cast<uint64_t>(p.x_stride));
+  const uint32_t n4 = p.x_stride / 4;
+  const uint32_t live = (ncols + 1) * kSlots;
+  for (uint32_t q = lane; q < n4; q += 32) {
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t jf = 4 * q + t;
+      float val = 0.0f;
+      if (jf < live) {
+        const uint32_t col = jf / kSlots;
+        const uint32_t slot = jf - col * kSlots;
+        if (slot < kStatic) {
+          val = __ldg(p.stat + static_cast<uint64_t>(s_inst[warp][col]) * kStatStride + slot);
+        } else if (slot == kSlotResidence) {
+          val = s_res[warp][col];
+        } else if (slot == kSlotExecution) {
+          val = s_exe[warp][col];
+        } else if (slot == kSlotStore) {
+          val = s_sto[warp][col];
+        } else if (slot < kSlotReserved) {
+          val = (s_flg[warp][col] >> (slot - kSlotFlag0)) & 1u ? nc.one[slot] : nc.zero[slot];
+        } else {
+          val = nc.zero[kSlotReserved];
+        }
+      }
+      v[t] = val;
+    }
+    out[q] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: hybrid decode (or truth in oracle mode) and the fetch-clock advance.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t decode_head(const float* y, int base, int n, float r,
+                                                double mu, double sigma) {
+  int best = 0;
+  float bv = y[base];
+  for (int i = 1; i < n; ++i) {
+    const float v = y[base + i];
+    if (v > bv) {  // strict: first maximum wins, NaN never wins (cnn.cpp:388-393)
+      bv = v;
+      best = i;
+    }
+  }
+  if (best < n - 1) return static_cast<uint32_t>(best);
+  // overflow class: de-normalise out of log1p space (cnn.cpp:399-401); the
+  // reference's -march=native build contracts r*sigma+mu into one fp64 FMA.
+  const double z = fmin(fma(static_cast<double>(r), sigma, mu), 22.0);
+  const double raw = fmax(0.0, expm1(z));
+  const long long v = llround(fmin(raw, 4.0e9));
+  return static_cast<uint32_t>(v > 0xffffffffLL ? 0xffffffffLL : v);
+}
+
+__device__ void decode_triple(const float* y, const NormConsts& nc, int cf, int ce, int cs,
+                              bool is_store, uint32_t* out) {
+  out[0] = decode_head(y, 3, cf, y[0], nc.label_mean[0], nc.label_sd[0]);
+  const uint32_t e = decode_head(y, 3 + cf, ce, y[1], nc.label_mean[1], nc.label_sd[1]);
+  out[1] = e < 1u ? 1u : e;
+  out[2] = is_store ? decode_head(y, 3 + cf + ce, cs, y[2], nc.label_mean[2], nc.label_sd[2]) : 0u;
+}
+
+__global__ void decode_kernel(DecodeParams p) {
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x + p.first;
+  if (s >= p.last) return;
+  SubState* sp = p.state + s;
+  if (sp->status != kOk) return;
+  const uint32_t pos = sp->pos, len = sp->len;
+  if (pos >= len) return;
+  const uint64_t idx = sp->begin + pos;
+  uint32_t t[3];
+  if (p.truth) {
+    t[0] = p.truth[3 * idx + 0];
+    t[1] = p.truth[3 * idx + 1];
+    t[2] = p.truth[3 * idx + 2];
+  } else {
+    const float* y = p.y + (s - p.first) * static_cast<uint64_t>(p.y_stride);
+    decode_triple(y, *p.nc, p.class_fetch, p.class_exec, p.class_store,
+                  (p.iflags[idx] & kFlagStore) != 0, t);
+  }
+  sp->pend_f = t[0];
+  sp->pend_e = t[1];
+  sp->pend_s = t[2];
+  sp->has_pend = 1;
+  if (!p.per_cycle && t[0] > 0) sp->cur += t[0];  // advance_cycles(F, ...): cur += F
+  if (pos >= sp->warm) {
+    sp->sum_fetch += t[0];
+    if (p.pred_fetch) p.pred_fetch[sp->fetch_off + (pos - sp->warm)] = t[0];
+  }
+}
+
+// Teacher-forced decode of caller logits (ilsim_gpu_predict).
+__global__ void decode_only_kernel(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
+                                   const NormConsts* nc, int cf, int ce, int cs, uint32_t* out) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  decode_triple(y + i * y_stride, *nc, cf, ce, cs, is_store[i] != 0, out + 3 * i);
+}
+
+// ---------------------------------------------------------------------------
+// Pack: normalise the 41 static slots once per instruction and derive flags.
+// ---------------------------------------------------------------------------
+__global__ void pack_kernel(PackParams p) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  if (i >= p.n) return;
+  const uint32_t k = threadIdx.x;  // 0..63
+  if (k < kStatic && p.stat) {
+    int32_t raw;
+    if (k < 13) raw = p.op[i * 13 + k];
+    else if (k < 21) raw = p.src[i * 8 + (k - 13)];
+    else if (k < 27) raw = p.dst[i * 6 + (k - 21)];
+    else raw = p.hist[i * 14 + (k - 27)];
+    p.stat[i * kStatStride + k] = norm_slot(raw, p.nc->mean[k], p.nc->sd[k]);
+  } else if (k == 63) {
+    const uint8_t ld = p.op[i * 13 + 1], stv = p.op[i * 13 + 2];
+    p.iflags[i] = static_cast<uint8_t>(((ld | stv) ? kFlagMem : 0) | (stv ? kFlagStore : 0));
+  }
+}
+
+void launch_ctx(const CtxParams& p, cudaStream_t stream) {
+  const uint64_t n = p.last - p.first;
+  if (n == 0) return;
+  const unsigned blocks = static_cast<unsigned>((n + kCtxWarps - 1) / kCtxWarps);
+  ctx_kernel<<<blocks, kCtxWarps * 32, 0, stream>>>(p);
+}
+
+void launch_decode(const DecodeParams& p, cudaStream_t stream) {
+  const uint64_t n = p.last - p.first;
+  if (n == 0) return;
+  decode_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(p);
+}
+
+void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
+                        const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
+                        cudaStream_t stream) {
+  if (n == 0) return;
+  decode_only_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(
+      y, y_stride, n, is_store, nc, cf, ce, cs, out);
+}
+
+void launch_pack(const PackParams& p, cudaStream_t stream) {
+  if (p.n == 0) return;
+  dim3 block(64, 4);
+  pack_kernel<<<static_cast<unsigned>((p.n + 3) / 4), block, 0, stream>>>(p);
+}
+
+}  // namespace simnet

@@ -1,0 +1,62 @@
+// Launch interfaces of the simulation kernels (K1 context-queue, K3 decode,
+// pack).  Parameter blocks are passed by value so launches capture cleanly
+// into CUDA graphs.
+#pragma once
+#include "common.cuh"
+
+namespace simnet {
+
+constexpr int kCtxWarps = 8;    // sub-traces per K1 block (one warp each)
+constexpr int kMaxCols = 256;   // max_context + 1 supported by the gather
+
+struct CtxParams {
+  SubState* state;
+  RingEntry* proc;
+  RingEntry* wq;
+  uint32_t pmask, wmask;     // ring capacities - 1 (powers of two)
+  uint64_t first, last;      // sub-trace range of this launch (chunk)
+  const float* stat;         // [n][kStatStride] normalised static slots
+  const uint64_t* pc;
+  const uint64_t* addr;
+  const uint8_t* iflags;
+  const NormConsts* nc;
+  float* x;                  // [last-first][x_stride] gathered inputs
+  uint32_t x_stride;         // floats per sample row (multiple of 4, >= 50*(mc+1))
+  int32_t max_context;
+  uint32_t bw, line, page;
+  int32_t per_cycle;
+  int32_t gather;
+};
+
+struct DecodeParams {
+  SubState* state;
+  uint64_t first, last;
+  const float* y;            // [last-first][y_stride] head outputs (null in oracle mode)
+  uint32_t y_stride;
+  const uint32_t* truth;     // oracle mode: [n][3]
+  const uint8_t* iflags;
+  const NormConsts* nc;
+  uint32_t* pred_fetch;      // owned predicted fetch series (may be null)
+  int32_t class_fetch, class_exec, class_store;
+  int32_t per_cycle;
+};
+
+struct PackParams {
+  uint64_t n;
+  const uint8_t* op;
+  const uint16_t* src;
+  const uint16_t* dst;
+  const uint16_t* hist;
+  const NormConsts* nc;
+  float* stat;               // may be null (oracle mode)
+  uint8_t* iflags;
+};
+
+void launch_ctx(const CtxParams& p, cudaStream_t stream);
+void launch_decode(const DecodeParams& p, cudaStream_t stream);
+void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
+                        const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
+                        cudaStream_t stream);
+void launch_pack(const PackParams& p, cudaStream_t stream);
+
+}  // namespace simnet

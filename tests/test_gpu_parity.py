@@ -1,0 +1,242 @@
+"""CUDA path (through the C-ABI) vs the CPU oracle port and the reference
+goldens.  Integer work (queues, clocks, gathered inputs) must be bit-exact;
+the fp32 CNN is checked teacher-forced (per-instruction triples equal except
+at documented near-ties) and free-running (total cycles within 0.1%)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import SUB, gpu_subs, instr_trace, random_trace, small_config
+from paper_2105_05821_b200 import IlsimError, ParallelConfig, SimConfig, init_weights
+from paper_2105_05821_b200.formats import CnnConfig, Model, read_model, read_trace
+
+pytestmark = pytest.mark.gpu
+GOLD = __import__("conftest").GOLDEN
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def pcfg(k=1, subtrace_size=0, batch_max=4096, mc=110, bw=8, per_cycle=False, warmup=0, drain_trim=False,
+         write_ring=0):
+    return ParallelConfig(k=k, subtrace_size=subtrace_size, batch_max=batch_max,
+                          sim=SimConfig(max_context=mc, retire_bandwidth=bw, per_cycle_advance=per_cycle),
+                          warmup=warmup, drain_trim=drain_trim, write_ring=write_ring)
+
+
+def run_gpu(g, t, pc, *, oracle=True, sequential=False, shard=None):
+    g.load_trace(t, pc, sequential=sequential, oracle=oracle, shard=shard)
+    return g.run(pc, sequential=sequential, oracle=oracle, shard=shard)
+
+
+# ---- scripted goldens (test_simcore.cpp:63-174) on the GPU -------------------
+def test_scripted_goldens(gpu):
+    g = gpu("fp32")
+    r = g.simulate_trace(instr_trace([False], [(5, 2, 0)]), oracle=True)
+    assert (r.sum_fetch, r.total_cycles, r.delta) == (5, 7, 2)
+    r = g.simulate_trace(instr_trace([False] * 3, [(5, 2, 0), (0, 3, 0), (1, 3, 0)]), oracle=True)
+    assert (r.sum_fetch, r.drain_cycles, r.delta, r.total_cycles) == (6, 3, 3, 9)
+    for k, b, want in [(5, 2, 3), (8, 8, 1), (9, 8, 2), (16, 4, 4), (1, 3, 1)]:
+        r = g.simulate_trace(instr_trace([False] * k, [(0, 0, 0)] * k), SimConfig(retire_bandwidth=b), oracle=True)
+        assert r.drain_cycles == want
+    r = g.simulate_trace(instr_trace([False], [(0, 4, 0)]), oracle=True)
+    assert r.drain_cycles == 4
+    r = g.simulate_trace(instr_trace([True, False], [(1, 2, 6), (0, 1, 0)]), oracle=True)
+    assert (r.total_cycles, r.sum_fetch, r.delta) == (7, 1, 6)
+    r = g.simulate_trace(instr_trace([False] * 6, [(0, 100, 0)] * 6), SimConfig(max_context=4), oracle=True)
+    assert r.overflow_stall_cycles == 100
+    r = g.simulate_trace(instr_trace([], []), oracle=True)
+    assert r.empty and r.total_cycles == 0 and r.cpi == 0.0
+
+
+# ---- golden.json oracle cases (made by the reference) -------------------------
+def test_golden_oracle_cases(gpu, golden):
+    g = gpu("fp32")
+    traces = {name: read_trace(GOLD / f"{name}.trace") for name in golden["traces"]}
+    for c in golden["oracle"]:
+        t = traces[c["trace"]]
+        pc = pcfg(c["k"], c["subtrace_size"], mc=c["max_context"], bw=c["retire_bandwidth"], per_cycle=c["per_cycle"])
+        r = run_gpu(g, t, pc, sequential=c["sequential"])
+        assert gpu_subs(r).tolist() == c["subs"], c
+        assert sha(r.predicted_fetch) == c["predicted_fetch_sha256"], c
+
+
+# ---- random traces / configurations vs the port (bit-exact) -------------------
+def store_heavy(seed, n, lat_hi=1500):
+    """Memory-heavy trace with scripted store-heavy truth latencies (the c4
+    regime of SURVEY.md §6: long queues, frequent retire)."""
+    t = random_trace(seed, n)
+    rng = np.random.default_rng(seed + 1)
+    st = rng.random(n) < 0.25
+    t.op[:, 0] = np.where(st, 8, t.op[:, 0])
+    t.op[:, 2] = st
+    t.op[:, 1] = np.where(st, 0, t.op[:, 1])
+    mem = (t.op[:, 1] | t.op[:, 2]) != 0
+    t.has_data = mem.astype(np.uint8)
+    t.data_addr = np.where(mem, 0x10000000 + rng.integers(0, 1 << 16, n) * 8, 0).astype(np.uint64)
+    t.truth[:, 0] = np.where(rng.random(n) < 0.5, 0, rng.integers(1, 4, n))
+    t.truth[:, 1] = rng.integers(1, 41, n)
+    t.truth[:, 2] = np.where(st, rng.integers(100, lat_hi, n), 0)
+    return t
+
+
+CASES = [
+    dict(k=1), dict(k=4), dict(k=33), dict(k=128), dict(k=7, mc=16, bw=2), dict(k=5, mc=4, bw=1),
+    dict(k=9, mc=64, bw=3, per_cycle=True), dict(k=6, warmup=40), dict(k=6, warmup=300, drain_trim=True),
+    dict(k=12, drain_trim=True), dict(subtrace_size=97), dict(k=3, mc=200),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_oracle_mode_vs_port(gpu, port, case):
+    g = gpu("fp32")
+    c = dict(CASES[case])
+    for t in (random_trace(100 + case, 2500), store_heavy(200 + case, 2500)):
+        pc = pcfg(**c)
+        r = run_gpu(g, t, pc)
+        want = port.simulate(t, oracle=True, k=pc.k, subtrace_size=pc.subtrace_size, max_context=pc.sim.max_context,
+                             retire_bandwidth=pc.sim.retire_bandwidth, per_cycle=pc.sim.per_cycle_advance,
+                             warmup=pc.warmup, drain_trim=pc.drain_trim)
+        assert np.array_equal(gpu_subs(r), want["subs"]), c
+        assert np.array_equal(r.predicted_fetch, want["predicted_fetch"]), c
+
+
+def test_sequential_equals_k1_and_shards_compose(gpu, port):
+    g = gpu("fp32")
+    t = store_heavy(7, 4000)
+    seq = run_gpu(g, t, pcfg(1), sequential=True)
+    k1 = run_gpu(g, t, pcfg(1))
+    assert np.array_equal(gpu_subs(seq), gpu_subs(k1))
+    full = run_gpu(g, t, pcfg(7, warmup=100))
+    parts = [run_gpu(g, t, pcfg(7, warmup=100), shard=s) for s in ((0, 3), (3, 5), (5, 7))]
+    assert np.array_equal(np.concatenate([gpu_subs(p) for p in parts]), gpu_subs(full))
+    assert np.array_equal(np.concatenate([p.predicted_fetch for p in parts]), full.predicted_fetch)
+
+
+def test_errors_and_validation(gpu):
+    g = gpu("fp32")
+    t = store_heavy(9, 3000, lat_hi=100000)
+    with pytest.raises(IlsimError, match="write queue ring overflow"):
+        run_gpu(g, t, pcfg(2, write_ring=4))
+    with pytest.raises(IlsimError, match="batch_max must be >= 1"):
+        run_gpu(g, t, pcfg(2, batch_max=0))
+    with pytest.raises(IlsimError, match="inconsistent partition: k=4 but subtrace size 1000 implies k=3"):
+        run_gpu(g, t, pcfg(4, subtrace_size=1000))
+    with pytest.raises(IlsimError, match="retire_bandwidth must be >= 1"):
+        run_gpu(g, t, pcfg(2, bw=0))
+    with pytest.raises(IlsimError, match="out of range"):
+        run_gpu(g, t.slice(0, 5), pcfg(6))
+    g2 = gpu("fp32")
+    t2 = random_trace(1, 100)
+    r = run_gpu(g2, t2, pcfg(3))  # the context is still usable after an error
+    assert r.instructions == 100
+
+
+# ---- gathered input tensor: bit-exact vs the reference's next_request ----------
+def c3_model(port, golden) -> Model:
+    gm = golden["models"]["c3_mix_seed1"]
+    cfg = CnnConfig.preset_c3()
+    return Model(cfg, np.array(gm["norm"]), port.init_params(cfg, gm["seed"]))
+
+
+@pytest.mark.parametrize("trace_name,k", [("mix_3000_s4", 5), ("pointer_chase_2000_s3", 16)])
+def test_input_tensor_bit_exact(gpu, port, golden, trace_name, k):
+    g = gpu("fp32")
+    m = c3_model(port, golden)
+    g.load_model(m)
+    t = read_trace(GOLD / f"{trace_name}.trace")
+    want = port.simulate(t, m, k=k, truth_with_inputs=True, capture=t.n, capture_inputs=True)
+    rounds = want["cap_round"]
+    for r in (0, 1, 7, 50, int(rounds.max())):
+        rows = np.nonzero(rounds == r)[0]
+        buf = g.capture_round(r, k)
+        pc = pcfg(k)
+        g.load_trace(t, pc, oracle=True)
+        g.run(pc, truth_inputs=True)
+        g.clear_capture()
+        assert np.array_equal(buf[: rows.size], want["cap_inputs"][rows]), f"round {r}"
+
+
+def test_input_tensor_store_heavy(gpu, port, golden):
+    """Long queues (write queue > 110 entries): truncation + newest-first order."""
+    g = gpu("fp32")
+    m = c3_model(port, golden)
+    g.load_model(m)
+    t = store_heavy(31, 1500)
+    k = 3
+    want = port.simulate(t, m, k=k, truth_with_inputs=True, capture=t.n, capture_inputs=True)
+    for r in (10, 200, 480):
+        rows = np.nonzero(want["cap_round"] == r)[0]
+        buf = g.capture_round(r, k)
+        pc = pcfg(k)
+        g.load_trace(t, pc, oracle=True)
+        g.run(pc, truth_inputs=True)
+        g.clear_capture()
+        assert np.array_equal(buf[: rows.size], want["cap_inputs"][rows]), f"round {r}"
+
+
+# ---- CNN: teacher-forced and free-running ------------------------------------
+def near_tie(y, tri_a, tri_b, cfg, norm):
+    """True when a decode disagreement is attributable to a near-tie: top-2
+    logit gap below 1e-4 relative, or regression within 1e-3 of a .5."""
+    heads = [(3, cfg.class_fetch, 0), (3 + cfg.class_fetch, cfg.class_exec, 1),
+             (3 + cfg.class_fetch + cfg.class_exec, cfg.class_store, 2)]
+    for h, (base, n, j) in enumerate(heads):
+        if tri_a[h] == tri_b[h]:
+            continue
+        lg = np.sort(y[base: base + n].astype(np.float64))
+        if lg[-1] - lg[-2] <= 1e-4 * max(1.0, abs(lg[-1])):
+            continue
+        z = min(float(y[j]) * norm[103 + j] + norm[100 + j], 22.0)
+        v = max(0.0, np.expm1(z))
+        if abs(v - np.floor(v) - 0.5) < 1e-3 * max(1.0, v):
+            continue
+        return False
+    return True
+
+
+@pytest.mark.parametrize("precision,rtol", [("fp32", 2e-5)])
+def test_teacher_forced_predict(gpu, port, golden, precision, rtol):
+    g = gpu(precision)
+    m = c3_model(port, golden)
+    g.load_model(m)
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    want = port.simulate(t, m, k=16, capture=1200, capture_inputs=True, capture_outputs=True)
+    out, tri = g.predict(want["cap_inputs"], want["cap_is_store"])
+    ref = want["cap_outputs"]
+    err = np.abs(out - ref) / np.maximum(1.0, np.abs(ref))
+    assert err.max() <= rtol, err.max()
+    bad = [i for i in range(tri.shape[0]) if not np.array_equal(tri[i], want["cap_triples"][i])]
+    for i in bad:
+        assert near_tie(ref[i], tri[i], want["cap_triples"][i], m.config, m.norm), i
+
+
+def test_free_running_cnn(gpu, port, golden):
+    g = gpu("fp32")
+    models = {"small_identity": read_model(GOLD / "small_identity.model"),
+              "small_dataset": read_model(GOLD / "small_dataset.model"), "c3": c3_model(port, golden)}
+    for name, m in models.items():
+        g.load_model(m)
+        for tname, k in (("mix_3000_s4", 5), ("branchy_2000_s8", 16), ("pointer_chase_2000_s3", 1)):
+            t = read_trace(GOLD / f"{tname}.trace")
+            pc = pcfg(k)
+            r = run_gpu(g, t, pc, oracle=False)
+            want = port.simulate(t, m, k=k)
+            tot, wtot = r.total_cycles, want["total_cycles"]
+            assert abs(tot - wtot) <= 1e-3 * wtot, (name, tname, tot, wtot)
+            same = np.mean(r.predicted_fetch == want["predicted_fetch"])
+            assert same >= 0.999, (name, tname, same)
+
+
+def test_batch_and_chunk_invariance(gpu):
+    """Per-request results must not depend on batch composition
+    (predictor.hpp:25-26, test_parallel.cpp:114-146)."""
+    g = gpu("fp32")
+    cfg = small_config()
+    g.load_model(init_weights(cfg, np.r_[np.zeros(50), np.ones(50), np.zeros(3), np.ones(3)], 33))
+    t = random_trace(3, 4000)
+    a = run_gpu(g, t, pcfg(5), oracle=False)
+    b = run_gpu(g, t, pcfg(5, batch_max=2), oracle=False)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)

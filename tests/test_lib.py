@@ -1,0 +1,113 @@
+"""The C-ABI library loads without a GPU and exports every symbol the header
+declares; host-only entry points work on CPU; formats round-trip."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2105_05821_b200 import _lib, build
+from paper_2105_05821_b200.errors import IlsimError
+from paper_2105_05821_b200.formats import CnnConfig, read_model, read_trace, write_model, write_trace
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLD = ROOT / "tests" / "golden"
+
+
+@pytest.fixture(scope="module")
+def L():
+    build.build()
+    return _lib.lib()
+
+
+def header_symbols():
+    text = (ROOT / "include" / "ilsim_gpu.h").read_text()
+    return sorted(set(re.findall(r"\b(ilsim_gpu_\w+)\s*\(", text)))
+
+
+def test_exports_every_header_symbol(L):
+    syms = header_symbols()
+    assert set(syms) == set(_lib.EXPORTS)
+    for s in syms:
+        assert hasattr(L, s), s
+    assert L.ilsim_gpu_abi_version() == 1
+
+
+STRUCTS = {"ilsim_gpu_options": _lib.Options, "ilsim_trace_view": _lib.TraceView, "ilsim_cnn_config": _lib.CnnCfg,
+           "ilsim_sim_config": _lib.SimCfg, "ilsim_sub_result": _lib.SubResult, "ilsim_totals": _lib.Totals}
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors vs the C compiler's sizeof/offsetof of every field."""
+    import shutil
+    import subprocess
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc unavailable")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ilsim_gpu.h"', "int main(void){"]
+    for cname, py in STRUCTS.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for cname, py in STRUCTS.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)
+
+
+def test_host_helpers_without_gpu(L, port):
+    from paper_2105_05821_b200 import api
+
+    assert api.partition_starts(10, 3) == [0, 4, 7]
+    with pytest.raises(IlsimError, match="out of range"):
+        api.partition_starts(10, 11)
+    assert api.model_flops("c3") == 1_073_408  # cnn.cpp:319-333 for preset_c3
+    cfg = CnnConfig.preset_c3()
+    m = api.init_weights(cfg, np.zeros(106), 1)
+    assert np.array_equal(m.params, port.init_params(cfg, 1))
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2105_05821_b200 import GpuSimulator
+
+    with pytest.raises(IlsimError):
+        GpuSimulator(0, "fp32")
+
+
+def test_trace_roundtrip(tmp_path):
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    p = tmp_path / "x.trace"
+    write_trace(p, t)
+    assert p.read_bytes() == (GOLD / "mix_3000_s4.trace").read_bytes()
+
+
+def test_model_roundtrip(tmp_path):
+    m = read_model(GOLD / "small_dataset.model")
+    p = tmp_path / "x.model"
+    write_model(p, m)
+    assert p.read_bytes() == (GOLD / "small_dataset.model").read_bytes()
+    assert m.config.hash() == CnnConfig(conv_channels=[16, 16, 16], fc_hidden=32).hash()
+
+
+def test_format_errors(tmp_path):
+    p = tmp_path / "bad"
+    p.write_bytes(b"XXXX" + bytes(40))
+    with pytest.raises(IlsimError, match="bad trace magic"):
+        read_trace(p)
+    with pytest.raises(IlsimError, match="bad model magic"):
+        read_model(p)
+    raw = (GOLD / "mix_3000_s4.trace").read_bytes()
+    p.write_bytes(raw[:-5])
+    with pytest.raises(IlsimError, match="trace truncated"):
+        read_trace(p)
