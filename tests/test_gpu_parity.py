@@ -85,7 +85,7 @@ def store_heavy(seed, n, lat_hi=1500):
 CASES = [
     dict(k=1), dict(k=4), dict(k=33), dict(k=128), dict(k=7, mc=16, bw=2), dict(k=5, mc=4, bw=1),
     dict(k=9, mc=64, bw=3, per_cycle=True), dict(k=6, warmup=40), dict(k=6, warmup=300, drain_trim=True),
-    dict(k=12, drain_trim=True), dict(subtrace_size=97), dict(k=3, mc=200),
+    dict(k=12, drain_trim=True), dict(k=0, subtrace_size=97), dict(k=3, mc=200),
 ]
 
 
