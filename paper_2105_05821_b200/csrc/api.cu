@@ -225,8 +225,13 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
 
   // chunking of the batch (bounds activation memory; results are batch-independent)
   const uint64_t chunk = std::min<uint64_t>(K, 65536);
-  const uint32_t x_stride = needs_input ? input_row_floats(mc) : 0;
-  float* d_x = needs_input ? static_cast<float*>(c->x.need(chunk * x_stride * sizeof(float))) : nullptr;
+  // gathered inputs: f32 rows of 100, or (bf16 inference) bf16 rows of 104
+  const int xprec = oracle ? ILSIM_PREC_FP32 : c->precision;
+  const uint32_t x_stride = needs_input ? input_stride(mc, xprec) : 0;
+  const uint32_t x_floats = needs_input ? input_row_floats(mc) : 0;
+  const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(xprec);
+  void* d_x = needs_input ? c->x.need(x_bytes) : nullptr;
+  if (needs_input) CUDA_OK(cudaMemsetAsync(d_x, 0, x_bytes, c->stream));  // bf16 row padding stays 0
   ForwardBuffers fb{};
   if (!oracle) fb = forward_buffers(c->model, chunk, c->act, c->y);
 
@@ -246,6 +251,8 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     cp.nc = c->nc_dev.as<NormConsts>();
     cp.x = d_x;
     cp.x_stride = x_stride;
+    cp.x_floats = x_floats;
+    cp.x_bf16 = xprec == ILSIM_PREC_BF16;
     cp.max_context = mc;
     cp.bw = cfg.retire_bandwidth;
     cp.line = cfg.line_size;
@@ -290,6 +297,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
 
   const bool capture_mode = c->cap_round != UINT32_MAX;
   if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
+  if (capture_mode && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
   const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs
   constexpr uint32_t kGraphRounds = 16;
   cudaGraphExec_t g1 = nullptr, gN = nullptr;
@@ -538,18 +546,21 @@ int ilsim_gpu_predict(ilsim_gpu_ctx* c, const float* inputs, uint64_t n, const u
     if (n == 0) return;
     const int mc = c->cfg.max_context;
     const uint32_t width = static_cast<uint32_t>(kSlots * (mc + 1));
-    const uint32_t x_stride = input_row_floats(mc);
+    const uint32_t x_stride = input_stride(mc, c->precision);
     const uint64_t chunk = std::min<uint64_t>(n, 65536);
-    float* d_x = static_cast<float*>(c->x.need(chunk * x_stride * sizeof(float)));
+    const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(c->precision);
+    void* d_x = c->x.need(x_bytes);
     ForwardBuffers fb = forward_buffers(c->model, chunk, c->act, c->y);
-    DevBuf d_store, d_trip;
+    DevBuf d_store, d_trip, d_in;
     uint8_t* ds = static_cast<uint8_t*>(d_store.need(chunk));
     uint32_t* dt = static_cast<uint32_t*>(d_trip.need(chunk * 12));
+    float* din = static_cast<float*>(d_in.need(chunk * width * sizeof(float)));
     for (uint64_t f = 0; f < n; f += chunk) {
       const uint64_t m = std::min(chunk, n - f);
-      CUDA_OK(cudaMemsetAsync(d_x, 0, m * x_stride * sizeof(float), c->stream));
-      CUDA_OK(cudaMemcpy2DAsync(d_x, x_stride * sizeof(float), inputs + f * width, width * sizeof(float),
-                                width * sizeof(float), m, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemsetAsync(d_x, 0, x_bytes, c->stream));
+      CUDA_OK(cudaMemcpyAsync(din, inputs + f * width, m * width * sizeof(float), cudaMemcpyHostToDevice,
+                              c->stream));
+      launch_pack_inputs(din, m, width, d_x, x_stride, c->precision == ILSIM_PREC_BF16, c->stream);
       CUDA_OK(cudaMemcpyAsync(ds, is_store + f, m, cudaMemcpyHostToDevice, c->stream));
       forward_launch(c->model, c->precision, d_x, x_stride, m, fb, c->stream);
       launch_decode_only(fb.y, fb.y_stride, m, ds, c->nc_dev.as<NormConsts>(), c->cfg.class_fetch,

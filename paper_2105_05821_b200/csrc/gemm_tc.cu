@@ -1,14 +1,611 @@
-// Tensor-core (tcgen05) path of K2 — placeholder until the kernels land.
+// K2 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Each conv layer of the reference CNN (cnn.cpp:90-125) is one GEMM over
+// (sample, position) rows: out[m, n] = ReLU(sum_k A[m, k] W[n, k] + b[n]) with
+// A the previous activation viewed as [rows/2 x 2C] (kernel-2/stride-2
+// windows are adjacent rows, so no im2col).  FC1 is the same GEMM over
+// [samples x flat] with split-K partials; FC2 + the FC1 epilogue run in a
+// small fp32 tail kernel.
+//
+// One CTA computes one 128 x BN output tile:
+//   warp 0      TMA producer: every K chunk of A (and W) into SWIZZLE_128B smem
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  (tf32x3) hi/lo operand split in smem; then the epilogue:
+//               tcgen05.ld accumulator -> bias/ReLU -> global (f32 or bf16)
+// Precisions: kind::f16 with bf16 operands; kind::tf32; 3xTF32 (A = hi + lo,
+// W = hi + lo, D += Alo*Whi + Ahi*Wlo + Ahi*Whi, fp32-faithful).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <mutex>
+#include <deque>
+#include <vector>
+
 #include "model.cuh"
 
 namespace simnet {
-struct TcModel {};
-TcModel* tc_model_create(const DevModel&, const float*, int, cudaStream_t) {
-  throw ApiError("tensor-core precisions are not built yet");
+
+enum TcMode : int { kBF16 = 0, kTF32 = 1, kTF32x3 = 2 };
+
+constexpr int kMaxChunks = 4;    // K chunks (128 B each) resident per CTA
+constexpr int kBM = 128;
+constexpr int kThreads = 192;    // 6 warps
+
+// --------------------------------------------------------------------------
+// PTX helpers
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row x 128 B atoms,
+// SBO = 1024 B between 8-row groups, version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;                  // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;          // SBO
+  d |= static_cast<uint64_t>(1) << 46;                  // descriptor version
+  d |= static_cast<uint64_t>(2) << 61;                  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t instr_desc(int fmt, int n) {
+  return (1u << 4) | (static_cast<uint32_t>(fmt) << 7) | (static_cast<uint32_t>(fmt) << 10) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+template <int kMode>
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  if constexpr (kMode == kBF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  }
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// --------------------------------------------------------------------------
+// The layer GEMM kernel
+// --------------------------------------------------------------------------
+struct TcGemmParams {
+  int m;              // valid output rows
+  int n;              // BN (output columns of this tile), multiple of 16
+  int chunks;         // K chunks of 128 B for this CTA
+  int ksteps;         // MMA k-steps (32 B each) actually needed
+  int a3d;            // A map is 3-D (conv0 over the gathered input)
+  int a_rows_per_box; // 3-D: positions per sample in one box (rows = box_rows * box_samples)
+  int a_samples_box;
+  int kc0;            // first K chunk index (split-K)
+  const float* bias;  // [n_total] (null: none)
+  int relu;
+  void* out;          // row-major [m][ldo] f32 or bf16
+  int ldo;
+  int out_bf16;
+  int col0;           // output column offset of this tile (N tiling)
+  uint64_t out_split_stride;  // elements between split-K partial planes (0: none)
+};
+
+template <int kMode>
+__global__ void __launch_bounds__(kThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmBlo, TcGemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // carve: A[chunks] | Alo[chunks] | B[chunks] | Blo[chunks] (each 1024-aligned)
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kABytes = kBM * 128;
+  const uint32_t bBytes = static_cast<uint32_t>(p.n) * 128;
+  uint8_t* sA = base;
+  uint8_t* sAlo = sA + kMaxChunks * kABytes;
+  uint8_t* sB = (kMode == kTF32x3) ? sAlo + kMaxChunks * kABytes : sAlo;
+  uint8_t* sBlo = sB + p.chunks * bBytes;
+
+  __shared__ __align__(8) uint64_t bar_full;    // all TMA bytes landed
+  __shared__ __align__(8) uint64_t bar_split;   // hi/lo split done (tf32x3)
+  __shared__ __align__(8) uint64_t bar_mma;     // accumulator ready
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tile_m = blockIdx.x;
+  const int tile_n = blockIdx.y;
+  const int ks = blockIdx.z;  // split-K plane
+  const uint32_t tcols = p.n <= 32 ? 32u : (p.n <= 64 ? 64u : (p.n <= 128 ? 128u : 256u));
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_full, 1);
+    mbar_init(&bar_split, 128);
+    mbar_init(&bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int kc_base = p.kc0 * ks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes =
+          p.chunks * (kABytes + bBytes * (kMode == kTF32x3 ? 2u : 1u));
+      mbar_expect_tx(&bar_full, bytes);
+      for (int c = 0; c < p.chunks; ++c) {
+        const int kc = kc_base + c;
+        const int kx = kc * (kMode == kBF16 ? 64 : 32);  // element offset along K
+        if (p.a3d)
+          tma_load_3d(sA + c * kABytes, &tmA, &bar_full, kx, 0, tile_m * p.a_samples_box);
+        else
+          tma_load_2d(sA + c * kABytes, &tmA, &bar_full, kx, tile_m * kBM);
+        tma_load_2d(sB + c * bBytes, &tmB, &bar_full, kx, tile_n * p.n);
+        if (kMode == kTF32x3) tma_load_2d(sBlo + c * bBytes, &tmBlo, &bar_full, kx, tile_n * p.n);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(&bar_full, 0);
+      if (kMode == kTF32x3) mbar_wait(&bar_split, 0);
+      tc_fence_after();
+      const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, p.n);
+      uint32_t acc = 0;
+      for (int s = 0; s < p.ksteps; ++s) {
+        const int c = s >> 2, j = s & 3;  // 4 k-steps of 32 B per 128 B chunk
+        const uint32_t aoff = c * kABytes + j * 32, boff = c * bBytes + j * 32;
+        const uint64_t ad = smem_desc_sw128(su32(sA) + aoff);
+        const uint64_t bd = smem_desc_sw128(su32(sB) + boff);
+        if (kMode == kTF32x3) {
+          const uint64_t adl = smem_desc_sw128(su32(sAlo) + aoff);
+          const uint64_t bdl = smem_desc_sw128(su32(sBlo) + boff);
+          mma<kMode>(tmem, adl, bd, idesc, acc);  // small terms first
+          mma<kMode>(tmem, ad, bdl, idesc, 1);
+          mma<kMode>(tmem, ad, bd, idesc, 1);
+        } else {
+          mma<kMode>(tmem, ad, bd, idesc, acc);
+        }
+        acc = 1;
+      }
+      mma_commit(&bar_mma);
+    }
+    __syncwarp();
+  } else {
+    // warps 2..5
+    const int t = threadIdx.x - 64;  // 0..127
+    if (kMode == kTF32x3) {
+      mbar_wait(&bar_full, 0);
+      const int nflt = p.chunks * (kABytes / 4);
+      float* a = reinterpret_cast<float*>(sA);
+      float* alo = reinterpret_cast<float*>(sAlo);
+      for (int i = t * 4; i < nflt; i += 128 * 4) {
+        float4 v = *reinterpret_cast<float4*>(a + i);
+        float4 h, l;
+        h.x = __uint_as_float(tf32_rna(v.x));
+        h.y = __uint_as_float(tf32_rna(v.y));
+        h.z = __uint_as_float(tf32_rna(v.z));
+        h.w = __uint_as_float(tf32_rna(v.w));
+        l.x = __uint_as_float(tf32_rna(v.x - h.x));
+        l.y = __uint_as_float(tf32_rna(v.y - h.y));
+        l.z = __uint_as_float(tf32_rna(v.z - h.z));
+        l.w = __uint_as_float(tf32_rna(v.w - h.w));
+        *reinterpret_cast<float4*>(a + i) = h;
+        *reinterpret_cast<float4*>(alo + i) = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&bar_split);
+    }
+    // epilogue: TMEM lane quadrant = warp % 4
+    mbar_wait(&bar_mma, 0);
+    tc_fence_after();
+    const int quad = warp & 3;
+    const int row = tile_m * kBM + quad * 32 + lane;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    for (int c0 = 0; c0 < p.n; c0 += 16) {
+      float v[16];
+      tmem_ld16(tl + c0, v);
+      if (row < p.m) {
+        const int col = p.col0 + tile_n * p.n + c0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (p.bias) v[i] += p.bias[col + i];
+          if (p.relu) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (p.out_bf16) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<uint64_t>(row) * p.ldo + col;
+          uint4 pk[2];
+          uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          reinterpret_cast<uint4*>(o)[0] = pk[0];
+          reinterpret_cast<uint4*>(o)[1] = pk[1];
+        } else {
+          float* o = static_cast<float*>(p.out) + ks * p.out_split_stride + static_cast<uint64_t>(row) * p.ldo + col;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+  }
+}
+
+// FC tail: h = ReLU(sum of split-K partials + b1) (fixed order), then
+// y = W2 h + b2 in fp32 (k-ascending, cnn.cpp:117-124).
+__global__ void __launch_bounds__(256) fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride,
+                                                      int hidden, const float* b1, const float* w2,
+                                                      const float* b2, int od, float* y, int samples) {
+  extern __shared__ float h[];
+  const int s = blockIdx.x;
+  if (s >= samples) return;
+  for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
+    float acc = 0.0f;
+    for (int q = 0; q < nsplit; ++q) acc += part[q * split_stride + static_cast<uint64_t>(s) * hidden + j];
+    h[j] = fmaxf(acc + b1[j], 0.0f);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < od; o += blockDim.x) {
+    float acc = 0.0f;
+    for (int k = 0; k < hidden; ++k) acc = fmaf(w2[o + static_cast<uint64_t>(k) * od], h[k], acc);
+    y[static_cast<uint64_t>(s) * od + o] = acc + b2[o];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Host side
+// --------------------------------------------------------------------------
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw ApiError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(const void* ptr, bool bf16, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                     const uint32_t* box) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t gd[3];
+  cuuint64_t gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  const CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 rank, const_cast<void*>(ptr), gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ApiError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+float tf32_round_host(float x) {  // cvt.rna.tf32.f32: round half away from zero to 10 mantissa bits
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;
+  u += 0x1000u;
+  u &= 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+uint16_t bf16_rn_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>(u >> 16);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+struct TcWeights {
+  DevBuf hi, lo;  // K-major [npad][kpad] (f32 or bf16)
+  int n = 0, npad = 0, k = 0, kpad = 0;
+  CUtensorMap map_hi{}, map_lo{};
+};
+
+int mode_of(int precision) {
+  return precision == ILSIM_PREC_BF16 ? kBF16 : (precision == ILSIM_PREC_TF32 ? kTF32 : kTF32x3);
+}
+
+}  // namespace
+
+struct TcModel {
+  int mode = kTF32x3;
+  std::deque<TcWeights> conv;
+  TcWeights fc1;
+  DevBuf part;  // split-K partials
+};
+
+namespace {
+
+// Reference column-major W[o + k*N] -> K-major [npad][kpad], split per mode.
+void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int n_tile, cudaStream_t s) {
+  const int elem_per_chunk = mode == kBF16 ? 64 : 32;
+  w.n = n;
+  w.k = k;
+  w.npad = ((n + n_tile - 1) / n_tile) * n_tile;
+  w.kpad = ((k + elem_per_chunk - 1) / elem_per_chunk) * elem_per_chunk;
+  const size_t cnt = static_cast<size_t>(w.npad) * w.kpad;
+  if (mode == kBF16) {
+    std::vector<uint16_t> h(cnt, 0);
+    for (int o = 0; o < n; ++o)
+      for (int q = 0; q < k; ++q) h[static_cast<size_t>(o) * w.kpad + q] = bf16_rn_host(src[o + static_cast<size_t>(q) * n]);
+    w.hi.need(cnt * 2);
+    CUDA_OK(cudaMemcpyAsync(w.hi.p, h.data(), cnt * 2, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+  } else {
+    std::vector<float> h(cnt, 0.0f), l(cnt, 0.0f);
+    for (int o = 0; o < n; ++o)
+      for (int q = 0; q < k; ++q) {
+        const float x = src[o + static_cast<size_t>(q) * n];
+        const float hi = tf32_round_host(x);
+        h[static_cast<size_t>(o) * w.kpad + q] = hi;
+        l[static_cast<size_t>(o) * w.kpad + q] = tf32_round_host(x - hi);
+      }
+    w.hi.need(cnt * 4);
+    w.lo.need(cnt * 4);
+    CUDA_OK(cudaMemcpyAsync(w.hi.p, h.data(), cnt * 4, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(w.lo.p, l.data(), cnt * 4, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+  }
+  const uint64_t dims[2] = {static_cast<uint64_t>(w.kpad), static_cast<uint64_t>(w.npad)};
+  const uint64_t strides[1] = {static_cast<uint64_t>(w.kpad) * (mode == kBF16 ? 2 : 4)};
+  const uint32_t box[2] = {static_cast<uint32_t>(elem_per_chunk), static_cast<uint32_t>(n_tile)};
+  w.map_hi = make_map(w.hi.p, mode == kBF16, 2, dims, strides, box);
+  w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
+}
+
+size_t smem_bytes(int mode, int n, int chunks) {
+  size_t a = static_cast<size_t>(chunks) * kBM * 128;
+  size_t b = static_cast<size_t>(chunks) * n * 128;
+  size_t tot = a + b;
+  if (mode == kTF32x3) tot = 2 * (kMaxChunks * kBM * 128) + 2 * b;
+  else tot = kMaxChunks * kBM * 128 + b;
+  return tot + 1024;
+}
+
+template <int kMode>
+void launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const TcGemmParams& p,
+               dim3 grid, cudaStream_t s) {
+  const size_t sm = smem_bytes(kMode, p.n, p.chunks);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
+  tc_gemm_kernel<kMode><<<grid, kThreads, sm, s>>>(a, b, blo, p);
+}
+
+void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
+                 const TcGemmParams& p, dim3 grid, cudaStream_t s) {
+  if (mode == kBF16) launch_tc<kBF16>(a, b, blo, p, grid, s);
+  else if (mode == kTF32) launch_tc<kTF32>(a, b, blo, p, grid, s);
+  else launch_tc<kTF32x3>(a, b, blo, p, grid, s);
+}
+
+}  // namespace
+
+TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s) {
+  const ilsim_cnn_config& c = m.cfg;
+  const int mode = mode_of(precision);
+  const int esz = mode == kBF16 ? 2 : 4;
+  // constraints of this kernel family (the FP32 SIMT path has none)
+  int cin = c.input_channels;
+  for (int l = 0; l < c.n_conv; ++l) {
+    const int k = 2 * cin;
+    if (c.conv[l] % 16 != 0 || c.conv[l] > 256) throw ApiError("tensor-core path: conv channels must be multiples of 16 <= 256");
+    if ((k * esz + 127) / 128 > kMaxChunks) throw ApiError("tensor-core path: conv input width too large");
+    if (c.residual) throw ApiError("tensor-core path: residual blocks not supported yet");
+    cin = c.conv[l];
+  }
+  if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
+  if (c.fc_hidden % 16 != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 16");
+  auto* t = new TcModel();
+  t->mode = mode;
+  try {
+    cin = c.input_channels;
+    for (int l = 0; l < c.n_conv; ++l) t->conv.emplace_back();
+    for (int l = 0; l < c.n_conv; ++l) {
+      upload_weights(t->conv[l], host_params + m.L.w[l], c.conv[l], 2 * cin, mode, c.conv[l], s);
+      cin = c.conv[l];
+    }
+    const int fc_tile = c.fc_hidden >= 64 ? 64 : c.fc_hidden;
+    if (c.fc_hidden % fc_tile != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 64 (or <= 64)");
+    upload_weights(t->fc1, host_params + m.L.fc1_w, c.fc_hidden, m.L.flat, mode, fc_tile, s);
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  return t;
+}
+
 void tc_model_destroy(TcModel* t) { delete t; }
-uint64_t tc_forward(const DevModel&, int, const float*, uint32_t, uint64_t, const ForwardBuffers&,
-                    cudaStream_t) {
-  throw ApiError("tensor-core precisions are not built yet");
+
+uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride, uint64_t samples,
+                    const ForwardBuffers& fb, cudaStream_t s) {
+  (void)precision;
+  TcModel& t = *m.tc;
+  const ilsim_cnn_config& c = m.cfg;
+  const int mode = t.mode;
+  const bool bf = mode == kBF16;
+  const int esz = bf ? 2 : 4;
+  const int chunk_elems = bf ? 64 : 32;
+  const float* P = m.params.as<float>();
+  uint64_t launches = 0;
+
+  int len = c.sequence_length;
+  int cin = c.input_channels;
+  const void* in = x;
+  for (int l = 0; l < c.n_conv; ++l) {
+    const int olen = len / 2, cout = c.conv[l], k = 2 * cin;
+    const uint64_t m_rows = samples * olen;
+    CUtensorMap amap;
+    TcGemmParams p{};
+    if (l == 0) {
+      // gathered input: [samples][rows][row_elems]; row_elems = 100 (f32) / 104 (bf16)
+      const uint64_t row_elems = bf ? 104 : 100;
+      const uint64_t rows = x_stride / (bf ? 104 : 100);
+      const uint64_t dims[3] = {static_cast<uint64_t>(k), rows, samples};
+      const uint64_t strides[2] = {row_elems * esz, static_cast<uint64_t>(x_stride) * esz};
+      const uint32_t box[3] = {static_cast<uint32_t>(chunk_elems), static_cast<uint32_t>(olen),
+                               static_cast<uint32_t>(kBM / olen)};
+      amap = make_map(in, bf, 3, dims, strides, box);
+      p.a3d = 1;
+      p.a_rows_per_box = olen;
+      p.a_samples_box = kBM / olen;
+    } else {
+      const uint64_t dims[2] = {static_cast<uint64_t>(k), m_rows};
+      const uint64_t strides[1] = {static_cast<uint64_t>(k) * esz};
+      const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
+      amap = make_map(in, bf, 2, dims, strides, box);
+    }
+    p.m = static_cast<int>(m_rows);
+    p.n = cout;
+    p.chunks = (k * esz + 127) / 128;
+    p.ksteps = (k * esz + 31) / 32;
+    p.kc0 = 0;
+    p.bias = P + m.L.b[l];
+    p.relu = 1;
+    p.out = fb.act[l];
+    p.ldo = cout;
+    p.out_bf16 = bf;
+    p.col0 = 0;
+    const dim3 grid(static_cast<unsigned>((m_rows + kBM - 1) / kBM), 1, 1);
+    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, p, grid, s);
+    ++launches;
+    in = fb.act[l];
+    cin = cout;
+    len = olen;
+  }
+  // FC1 split-K partials
+  const int flat = m.L.flat;
+  const int total_chunks = (flat * esz + 127) / 128;
+  const int per = kMaxChunks;
+  const int nsplit = (total_chunks + per - 1) / per;
+  const int fc_tile = t.fc1.npad >= 64 ? 64 : t.fc1.npad;
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(flat), samples};
+    const uint64_t strides[1] = {static_cast<uint64_t>(flat) * esz};
+    const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
+    const CUtensorMap amap = make_map(in, bf, 2, dims, strides, box);
+    const uint64_t plane = samples * static_cast<uint64_t>(c.fc_hidden);
+    float* part = static_cast<float*>(t.part.need(plane * nsplit * sizeof(float)));
+    TcGemmParams p{};
+    p.m = static_cast<int>(samples);
+    p.n = fc_tile;
+    p.chunks = per;
+    p.ksteps = per * 4;
+    p.kc0 = per;
+    p.bias = nullptr;
+    p.relu = 0;
+    p.out = part;
+    p.ldo = c.fc_hidden;
+    p.out_bf16 = 0;
+    p.col0 = 0;
+    p.out_split_stride = plane;
+    if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
+    const dim3 grid(static_cast<unsigned>((samples + kBM - 1) / kBM), static_cast<unsigned>(t.fc1.npad / fc_tile),
+                    static_cast<unsigned>(nsplit));
+    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, grid, s);
+    ++launches;
+    const int od = m.L.out_dim;
+    fc_tail_kernel<<<static_cast<unsigned>(samples), 256, c.fc_hidden * sizeof(float), s>>>(
+        part, nsplit, plane, c.fc_hidden, P + m.L.fc1_b, P + m.L.fc2_w, P + m.L.fc2_b, od, fb.y,
+        static_cast<int>(samples));
+    ++launches;
+  }
+  return launches;
 }
+
 }  // namespace simnet

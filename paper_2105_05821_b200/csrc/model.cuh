@@ -28,6 +28,13 @@ void init_weights_into(const ilsim_cnn_config& c, uint64_t seed, float* params);
 inline uint32_t input_row_floats(int max_context) {
   return 100u * static_cast<uint32_t>((max_context + 2) / 2);
 }
+// Device row layout of the gathered input per precision: bf16 rows are padded
+// to 104 elements (208 B) so TMA row strides stay 16-B multiples.
+inline uint32_t input_row_elems(int precision) { return precision == ILSIM_PREC_BF16 ? 104u : 100u; }
+inline uint32_t input_stride(int max_context, int precision) {
+  return input_row_elems(precision) * static_cast<uint32_t>((max_context + 2) / 2);
+}
+inline uint32_t input_elem_bytes(int precision) { return precision == ILSIM_PREC_BF16 ? 2u : 4u; }
 
 struct TcModel;  // tensor-core operand copies (gemm_tc.cu)
 
@@ -52,13 +59,13 @@ void model_upload(DevModel& m, const ilsim_cnn_config& c, const float* params, i
                   cudaStream_t s);
 ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, DevBuf& y);
 // Runs the forward for `samples` gathered rows; returns kernels launched.
-uint64_t forward_launch(const DevModel& m, int precision, const float* x, uint32_t x_stride,
+uint64_t forward_launch(const DevModel& m, int precision, const void* x, uint32_t x_stride,
                         uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
 
 // tensor-core path (gemm_tc.cu)
 TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s);
 void tc_model_destroy(TcModel* t);
-uint64_t tc_forward(const DevModel& m, int precision, const float* x, uint32_t x_stride,
+uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride,
                     uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
 
 }  // namespace simnet

@@ -10,6 +10,8 @@
 //
 // K3 replaces decode_hybrid (cnn.cpp:388-417) plus the clock half of
 // apply_step (advance_cycles(F, bw*F), simcore.cpp:117-123, 147-149).
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "sim_kernels.cuh"
 
@@ -226,9 +228,10 @@ ctx_kernel(CtxParams p) {
   __syncwarp();
 
   // Coalesced write of the whole sample row: columns > ncols are exactly 0.
-  float4* out = reinterpret_cast<float4*>(p.x + (s - p.first) * static_cast<uint64_t>(p.x_stride));
-  const uint32_t n4 = p.x_stride / 4;
+  const uint32_t n4 = p.x_floats / 4;
   const uint32_t live = (ncols + 1) * kSlots;
+  float4* out4 = reinterpret_cast<float4*>(static_cast<float*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride));
+  __nv_bfloat16* outb = static_cast<__nv_bfloat16*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride);
   for (uint32_t q = lane; q < n4; q += 32) {
     float v[4];
 #pragma unroll
@@ -254,7 +257,16 @@ ctx_kernel(CtxParams p) {
       }
       v[t] = val;
     }
-    out[q] = make_float4(v[0], v[1], v[2], v[3]);
+    if (p.x_bf16) {
+      const uint32_t row = (4 * q) / 100, within = 4 * q - 100 * row;
+      __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&a);
+      w.y = *reinterpret_cast<uint32_t*>(&b);
+      *reinterpret_cast<uint2*>(outb + row * 104 + within) = w;
+    } else {
+      out4[q] = make_float4(v[0], v[1], v[2], v[3]);
+    }
   }
 }
 
@@ -344,6 +356,28 @@ __global__ void pack_kernel(PackParams p) {
     const uint8_t ld = p.op[i * 13 + 1], stv = p.op[i * 13 + 2];
     p.iflags[i] = static_cast<uint8_t>(((ld | stv) ? kFlagMem : 0) | (stv ? kFlagStore : 0));
   }
+}
+
+__global__ void pack_inputs_kernel(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride,
+                                   int x_bf16) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * width) return;
+  const uint64_t smp = i / width;
+  const uint32_t j = static_cast<uint32_t>(i - smp * width);
+  if (x_bf16) {
+    const uint32_t row = j / 100, within = j - 100 * row;
+    static_cast<__nv_bfloat16*>(x)[smp * x_stride + row * 104 + within] = __float2bfloat16_rn(in[i]);
+  } else {
+    static_cast<float*>(x)[smp * x_stride + j] = in[i];
+  }
+}
+
+void launch_pack_inputs(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride, int x_bf16,
+                        cudaStream_t stream) {
+  const uint64_t tot = n * width;
+  if (tot == 0) return;
+  pack_inputs_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(in, n, width, x, x_stride,
+                                                                                    x_bf16);
 }
 
 void launch_ctx(const CtxParams& p, cudaStream_t stream) {

@@ -20,8 +20,10 @@ struct CtxParams {
   const uint64_t* addr;
   const uint8_t* iflags;
   const NormConsts* nc;
-  float* x;                  // [last-first][x_stride] gathered inputs
-  uint32_t x_stride;         // floats per sample row (multiple of 4, >= 50*(mc+1))
+  void* x;                   // [last-first][x_stride] gathered inputs (f32 or bf16)
+  uint32_t x_stride;         // elements per sample in x
+  uint32_t x_floats;         // logical floats per sample (100 per conv0 row, multiple of 4)
+  int32_t x_bf16;            // 1: rows of 104 bf16 (100 + zero pad, TMA-aligned)
   int32_t max_context;
   uint32_t bw, line, page;
   int32_t per_cycle;
@@ -58,5 +60,8 @@ void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t*
                         const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
                         cudaStream_t stream);
 void launch_pack(const PackParams& p, cudaStream_t stream);
+// Caller inputs [n][width] f32 -> gathered-input layout (ilsim_gpu_predict).
+void launch_pack_inputs(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride, int x_bf16,
+                        cudaStream_t stream);
 
 }  // namespace simnet

@@ -197,8 +197,9 @@ def near_tie(y, tri_a, tri_b, cfg, norm):
     return True
 
 
-@pytest.mark.parametrize("precision,rtol", [("fp32", 2e-5)])
-def test_teacher_forced_predict(gpu, port, golden, precision, rtol):
+@pytest.mark.parametrize("precision,rtol,exact", [("fp32", 2e-5, True), ("tf32x3", 1e-4, True),
+                                                  ("tf32", 3e-2, False), ("bf16", 1.5e-1, False)])
+def test_teacher_forced_predict(gpu, port, golden, precision, rtol, exact):
     g = gpu(precision)
     m = c3_model(port, golden)
     g.load_model(m)
@@ -209,12 +210,16 @@ def test_teacher_forced_predict(gpu, port, golden, precision, rtol):
     err = np.abs(out - ref) / np.maximum(1.0, np.abs(ref))
     assert err.max() <= rtol, err.max()
     bad = [i for i in range(tri.shape[0]) if not np.array_equal(tri[i], want["cap_triples"][i])]
-    for i in bad:
-        assert near_tie(ref[i], tri[i], want["cap_triples"][i], m.config, m.norm), i
+    if exact:
+        for i in bad:
+            assert near_tie(ref[i], tri[i], want["cap_triples"][i], m.config, m.norm), i
+    else:  # reduced precision: decode agreement is reported, not required exact
+        assert len(bad) <= 0.05 * tri.shape[0], len(bad)
 
 
-def test_free_running_cnn(gpu, port, golden):
-    g = gpu("fp32")
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
+def test_free_running_cnn(gpu, port, golden, precision):
+    g = gpu(precision)
     models = {"small_identity": read_model(GOLD / "small_identity.model"),
               "small_dataset": read_model(GOLD / "small_dataset.model"), "c3": c3_model(port, golden)}
     for name, m in models.items():
@@ -240,3 +245,18 @@ def test_batch_and_chunk_invariance(gpu):
     a = run_gpu(g, t, pcfg(5), oracle=False)
     b = run_gpu(g, t, pcfg(5, batch_max=2), oracle=False)
     assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_tensor_core_batch_tail_and_small_model(gpu, port, precision):
+    """Ragged batches (samples not a multiple of the 128-row tile) and the
+    16/16/16 model (one K chunk per conv) through the tcgen05 kernels."""
+    g = gpu(precision)
+    m = read_model(GOLD / "small_dataset.model")
+    g.load_model(m)
+    t = read_trace(GOLD / "branchy_2000_s8.trace")
+    for k in (1, 3, 130):
+        want = port.simulate(t, m, k=k, capture=min(t.n, 700), capture_inputs=True, capture_outputs=True)
+        out, _ = g.predict(want["cap_inputs"], want["cap_is_store"])
+        err = np.abs(out - want["cap_outputs"]) / np.maximum(1.0, np.abs(want["cap_outputs"]))
+        assert err.max() <= (1e-4 if precision == "tf32x3" else 1.5e-1), (k, err.max())
