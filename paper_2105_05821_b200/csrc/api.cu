@@ -306,12 +306,20 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     for (int which = 0; which < 2; ++which) {
       const uint32_t reps = which == 0 ? 1 : kGraphRounds;
       if (which == 1 && rounds < kGraphRounds) break;
-      cudaGraph_t g;
+      cudaGraph_t g = nullptr;
       CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      for (uint32_t r = 0; r < reps; ++r) launches_per_round = launch_round();
+      try {
+        for (uint32_t r = 0; r < reps; ++r) launches_per_round = launch_round();
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);  // leave the stream usable
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+      }
       CUDA_OK(cudaStreamEndCapture(c->stream, &g));
-      CUDA_OK(cudaGraphInstantiate(which == 0 ? &g1 : &gN, g, 0));
+      const cudaError_t ie = cudaGraphInstantiate(which == 0 ? &g1 : &gN, g, 0);
       cudaGraphDestroy(g);
+      CUDA_OK(ie);
     }
   }
 

@@ -459,11 +459,6 @@ template <int kMode>
 void launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const TcGemmParams& p,
                dim3 grid, cudaStream_t s) {
   const size_t sm = smem_bytes(kMode, p.n, p.chunks);
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
-  }
   tc_gemm_kernel<kMode><<<grid, kThreads, sm, s>>>(a, b, blo, p);
 }
 
@@ -491,6 +486,9 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   }
   if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
   if (c.fc_hidden % 16 != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 16");
+  CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   auto* t = new TcModel();
   t->mode = mode;
   try {
@@ -511,6 +509,15 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
 }
 
 void tc_model_destroy(TcModel* t) { delete t; }
+
+// Allocations the forward needs, done before any graph capture.
+void tc_prepare(const DevModel& m, uint64_t samples) {
+  TcModel& t = *m.tc;
+  const int esz = t.mode == kBF16 ? 2 : 4;
+  const int total_chunks = (m.L.flat * esz + 127) / 128;
+  const int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
+  t.part.need(samples * static_cast<uint64_t>(m.cfg.fc_hidden) * nsplit * sizeof(float));
+}
 
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride, uint64_t samples,
                     const ForwardBuffers& fb, cudaStream_t s) {
@@ -580,7 +587,8 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
     const CUtensorMap amap = make_map(in, bf, 2, dims, strides, box);
     const uint64_t plane = samples * static_cast<uint64_t>(c.fc_hidden);
-    float* part = static_cast<float*>(t.part.need(plane * nsplit * sizeof(float)));
+    if (t.part.bytes < plane * nsplit * sizeof(float)) throw ApiError("internal: split-K buffer not prepared");
+    float* part = t.part.as<float>();
     TcGemmParams p{};
     p.m = static_cast<int>(samples);
     p.n = fc_tile;

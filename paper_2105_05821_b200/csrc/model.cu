@@ -155,6 +155,7 @@ ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, D
   for (size_t i = 0; i < off.size(); ++i) fb.act[i] = base + off[i];
   fb.y_stride = static_cast<uint32_t>(m.L.out_dim);
   fb.y = static_cast<float*>(y.need(chunk * fb.y_stride * sizeof(float)));
+  if (m.tc) tc_prepare(m, chunk);
   return fb;
 }
 

@@ -65,6 +65,7 @@ uint64_t forward_launch(const DevModel& m, int precision, const void* x, uint32_
 // tensor-core path (gemm_tc.cu)
 TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s);
 void tc_model_destroy(TcModel* t);
+void tc_prepare(const DevModel& m, uint64_t samples);
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride,
                     uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
 
