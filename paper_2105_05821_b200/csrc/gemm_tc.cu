@@ -133,56 +133,71 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 }
 
 // --------------------------------------------------------------------------
-// The layer GEMM kernel
 // --------------------------------------------------------------------------
+// Persistent, warp-specialised layer GEMM
+// --------------------------------------------------------------------------
+// CTA (gx, ny, nz) owns weight slice (N tile ny, K split nz), resident in smem
+// for the whole launch, and loops over M tiles gx, gx + gridDim.x, ...
+//   warp 0     TMA producer: A chunks (128 rows x 128 B) into a 4-stage ring
+//   warp 1     TMEM allocation + single-thread tcgen05.mma issue
+//   warps 2-5  (3xTF32) split each landed chunk into hi / lo in place
+//   warps 6-9  epilogue: tcgen05.ld -> bias / ReLU -> global; two TMEM
+//              accumulators so tile t's epilogue overlaps tile t+1's MMAs
+constexpr int kStages = 4;
+constexpr int kWarps = 10;
+constexpr int kLayerThreads = kWarps * 32;
+constexpr uint32_t kAChunk = kBM * 128;  // 16 KB
+
 struct TcGemmParams {
   int m;              // valid output rows
-  int n;              // BN (output columns of this tile), multiple of 16
-  int chunks;         // K chunks of 128 B for this CTA
-  int ksteps;         // MMA k-steps (32 B each) actually needed
+  int m_tiles;
+  int n;              // BN: output columns per tile (multiple of 16, <= 128)
+  int chunks;         // K chunks (128 B) per tile for this CTA's split
+  int ksteps_last;    // MMA k-steps in the last chunk (1..4)
   int a3d;            // A map is 3-D (conv0 over the gathered input)
-  int a_rows_per_box; // 3-D: positions per sample in one box (rows = box_rows * box_samples)
-  int a_samples_box;
-  int kc0;            // first K chunk index (split-K)
+  int a_samples_box;  // 3-D: samples per 128-row box
   const float* bias;  // [n_total] (null: none)
   int relu;
   void* out;          // row-major [m][ldo] f32 or bf16
   int ldo;
   int out_bf16;
-  int col0;           // output column offset of this tile (N tiling)
-  uint64_t out_split_stride;  // elements between split-K partial planes (0: none)
+  uint64_t out_split_stride;  // elements between split-K partial planes
 };
 
 template <int kMode>
-__global__ void __launch_bounds__(kThreads, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmBlo, TcGemmParams p) {
+__global__ void __launch_bounds__(kLayerThreads, 1)
+tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmBlo, TcGemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // carve: A[chunks] | Alo[chunks] | B[chunks] | Blo[chunks] (each 1024-aligned)
+  constexpr bool kSplit = kMode == kTF32x3;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t kABytes = kBM * 128;
   const uint32_t bBytes = static_cast<uint32_t>(p.n) * 128;
-  uint8_t* sA = base;
-  uint8_t* sAlo = sA + kMaxChunks * kABytes;
-  uint8_t* sB = (kMode == kTF32x3) ? sAlo + kMaxChunks * kABytes : sAlo;
-  uint8_t* sBlo = sB + p.chunks * bBytes;
+  uint8_t* sW = base;                                      // [chunks][n x 128 B]
+  uint8_t* sWlo = sW + p.chunks * bBytes;                  // tf32x3 only
+  uint8_t* sA = sWlo + (kSplit ? p.chunks * bBytes : 0);   // [stages][16 KB]
+  uint8_t* sAlo = sA + kStages * kAChunk;                  // tf32x3 only
 
-  __shared__ __align__(8) uint64_t bar_full;    // all TMA bytes landed
-  __shared__ __align__(8) uint64_t bar_split;   // hi/lo split done (tf32x3)
-  __shared__ __align__(8) uint64_t bar_mma;     // accumulator ready
+  __shared__ __align__(8) uint64_t bar_w;
+  __shared__ __align__(8) uint64_t bar_full[kStages], bar_split[kStages], bar_empty[kStages];
+  __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
   __shared__ uint32_t tmem_slot;
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int tile_m = blockIdx.x;
-  const int tile_n = blockIdx.y;
-  const int ks = blockIdx.z;  // split-K plane
-  const uint32_t tcols = p.n <= 32 ? 32u : (p.n <= 64 ? 64u : (p.n <= 128 ? 128u : 256u));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntile = blockIdx.y, ks = blockIdx.z;
+  const int kc0 = ks * p.chunks;  // first K chunk of this split
+  const uint32_t tcols = 2 * p.n <= 32 ? 32u : (2 * p.n <= 64 ? 64u : (2 * p.n <= 128 ? 128u : 256u));
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar_full, 1);
-    mbar_init(&bar_split, 128);
-    mbar_init(&bar_mma, 1);
+    mbar_init(&bar_w, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_split[i], 128);
+      mbar_init(&bar_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_acc_full[i], 1);
+      mbar_init(&bar_acc_empty[i], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -196,109 +211,149 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const int kc_base = p.kc0 * ks;
+  const int elems = kMode == kBF16 ? 64 : 32;  // elements per 128 B chunk
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes =
-          p.chunks * (kABytes + bBytes * (kMode == kTF32x3 ? 2u : 1u));
-      mbar_expect_tx(&bar_full, bytes);
+      // resident weights for this CTA's (N tile, K split)
+      mbar_expect_tx(&bar_w, p.chunks * bBytes * (kSplit ? 2u : 1u));
       for (int c = 0; c < p.chunks; ++c) {
-        const int kc = kc_base + c;
-        const int kx = kc * (kMode == kBF16 ? 64 : 32);  // element offset along K
-        if (p.a3d)
-          tma_load_3d(sA + c * kABytes, &tmA, &bar_full, kx, 0, tile_m * p.a_samples_box);
-        else
-          tma_load_2d(sA + c * kABytes, &tmA, &bar_full, kx, tile_m * kBM);
-        tma_load_2d(sB + c * bBytes, &tmB, &bar_full, kx, tile_n * p.n);
-        if (kMode == kTF32x3) tma_load_2d(sBlo + c * bBytes, &tmBlo, &bar_full, kx, tile_n * p.n);
+        tma_load_2d(sW + c * bBytes, &tmB, &bar_w, (kc0 + c) * elems, ntile * p.n);
+        if (kSplit) tma_load_2d(sWlo + c * bBytes, &tmBlo, &bar_w, (kc0 + c) * elems, ntile * p.n);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
+        for (int c = 0; c < p.chunks; ++c) {
+          mbar_wait(&bar_empty[stage], phase ^ 1);
+          mbar_expect_tx(&bar_full[stage], kAChunk);
+          const int kx = (kc0 + c) * elems;
+          if (p.a3d)
+            tma_load_3d(sA + stage * kAChunk, &tmA, &bar_full[stage], kx, 0, t * p.a_samples_box);
+          else
+            tma_load_2d(sA + stage * kAChunk, &tmA, &bar_full[stage], kx, t * kBM);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      mbar_wait(&bar_full, 0);
-      if (kMode == kTF32x3) mbar_wait(&bar_split, 0);
-      tc_fence_after();
+      mbar_wait(&bar_w, 0);
       const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, p.n);
-      uint32_t acc = 0;
-      for (int s = 0; s < p.ksteps; ++s) {
-        const int c = s >> 2, j = s & 3;  // 4 k-steps of 32 B per 128 B chunk
-        const uint32_t aoff = c * kABytes + j * 32, boff = c * bBytes + j * 32;
-        const uint64_t ad = smem_desc_sw128(su32(sA) + aoff);
-        const uint64_t bd = smem_desc_sw128(su32(sB) + boff);
-        if (kMode == kTF32x3) {
-          const uint64_t adl = smem_desc_sw128(su32(sAlo) + aoff);
-          const uint64_t bdl = smem_desc_sw128(su32(sBlo) + boff);
-          mma<kMode>(tmem, adl, bd, idesc, acc);  // small terms first
-          mma<kMode>(tmem, ad, bdl, idesc, 1);
-          mma<kMode>(tmem, ad, bd, idesc, 1);
-        } else {
-          mma<kMode>(tmem, ad, bd, idesc, acc);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&bar_acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * p.n;
+        for (int c = 0; c < p.chunks; ++c) {
+          mbar_wait(kSplit ? &bar_split[stage] : &bar_full[stage], phase);
+          tc_fence_after();
+          const int steps = c == p.chunks - 1 ? p.ksteps_last : 4;
+          for (int j = 0; j < steps; ++j) {
+            const uint32_t aoff = stage * kAChunk + j * 32, boff = c * bBytes + j * 32;
+            const uint64_t ad = smem_desc_sw128(su32(sA) + aoff);
+            const uint64_t bd = smem_desc_sw128(su32(sW) + boff);
+            const uint32_t first = (c == 0 && j == 0) ? 0u : 1u;
+            if (kSplit) {
+              mma<kMode>(d, smem_desc_sw128(su32(sAlo) + aoff), bd, idesc, first);  // small terms first
+              mma<kMode>(d, ad, smem_desc_sw128(su32(sWlo) + boff), idesc, 1);
+              mma<kMode>(d, ad, bd, idesc, 1);
+            } else {
+              mma<kMode>(d, ad, bd, idesc, first);
+            }
+          }
+          mma_commit(&bar_empty[stage]);  // the stage is free once these MMAs retire
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        acc = 1;
+        mma_commit(&bar_acc_full[acc]);
       }
-      mma_commit(&bar_mma);
     }
     __syncwarp();
-  } else {
-    // warps 2..5
-    const int t = threadIdx.x - 64;  // 0..127
-    if (kMode == kTF32x3) {
-      mbar_wait(&bar_full, 0);
-      const int nflt = p.chunks * (kABytes / 4);
-      float* a = reinterpret_cast<float*>(sA);
-      float* alo = reinterpret_cast<float*>(sAlo);
-      for (int i = t * 4; i < nflt; i += 128 * 4) {
-        float4 v = *reinterpret_cast<float4*>(a + i);
-        float4 h, l;
-        h.x = __uint_as_float(tf32_rna(v.x));
-        h.y = __uint_as_float(tf32_rna(v.y));
-        h.z = __uint_as_float(tf32_rna(v.z));
-        h.w = __uint_as_float(tf32_rna(v.w));
-        l.x = __uint_as_float(tf32_rna(v.x - h.x));
-        l.y = __uint_as_float(tf32_rna(v.y - h.y));
-        l.z = __uint_as_float(tf32_rna(v.z - h.z));
-        l.w = __uint_as_float(tf32_rna(v.w - h.w));
-        *reinterpret_cast<float4*>(a + i) = h;
-        *reinterpret_cast<float4*>(alo + i) = l;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&bar_split);
-    }
-    // epilogue: TMEM lane quadrant = warp % 4
-    mbar_wait(&bar_mma, 0);
-    tc_fence_after();
-    const int quad = warp & 3;
-    const int row = tile_m * kBM + quad * 32 + lane;
-    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    for (int c0 = 0; c0 < p.n; c0 += 16) {
-      float v[16];
-      tmem_ld16(tl + c0, v);
-      if (row < p.m) {
-        const int col = p.col0 + tile_n * p.n + c0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (p.bias) v[i] += p.bias[col + i];
-          if (p.relu) v[i] = fmaxf(v[i], 0.0f);
-        }
-        if (p.out_bf16) {
-          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<uint64_t>(row) * p.ldo + col;
-          uint4 pk[2];
-          uint32_t* w = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            w[i] = *reinterpret_cast<uint32_t*>(&b2);
+  } else if (warp < 6) {
+    if (kSplit) {  // hi/lo split of each landed A chunk
+      const int t128 = threadIdx.x - 64;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
+        for (int c = 0; c < p.chunks; ++c) {
+          mbar_wait(&bar_full[stage], phase);
+          float4* a = reinterpret_cast<float4*>(sA + stage * kAChunk);
+          float4* alo = reinterpret_cast<float4*>(sAlo + stage * kAChunk);
+#pragma unroll 4
+          for (int i = t128; i < static_cast<int>(kAChunk / 16); i += 128) {
+            const float4 v = a[i];
+            float4 h, l;
+            h.x = __uint_as_float(tf32_rna(v.x));
+            h.y = __uint_as_float(tf32_rna(v.y));
+            h.z = __uint_as_float(tf32_rna(v.z));
+            h.w = __uint_as_float(tf32_rna(v.w));
+            l.x = __uint_as_float(tf32_rna(v.x - h.x));
+            l.y = __uint_as_float(tf32_rna(v.y - h.y));
+            l.z = __uint_as_float(tf32_rna(v.z - h.z));
+            l.w = __uint_as_float(tf32_rna(v.w - h.w));
+            a[i] = h;
+            alo[i] = l;
           }
-          reinterpret_cast<uint4*>(o)[0] = pk[0];
-          reinterpret_cast<uint4*>(o)[1] = pk[1];
-        } else {
-          float* o = static_cast<float*>(p.out) + ks * p.out_split_stride + static_cast<uint64_t>(row) * p.ldo + col;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&bar_split[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
+    }
+  } else {
+    // epilogue warps 6..9: TMEM lane quadrant = warp % 4
+    const int quad = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = t * kBM + quad * 32 + lane;
+      const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * p.n;
+      for (int c0 = 0; c0 < p.n; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + c0, v);
+        if (row < p.m) {
+          const int col = ntile * p.n + c0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (p.bias) v[i] += p.bias[col + i];
+            if (p.relu) v[i] = fmaxf(v[i], 0.0f);
+          }
+          if (p.out_bf16) {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<uint64_t>(row) * p.ldo + col;
+            uint4 pk[2];
+            uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            reinterpret_cast<uint4*>(o)[0] = pk[0];
+            reinterpret_cast<uint4*>(o)[1] = pk[1];
+          } else {
+            float* o = static_cast<float*>(p.out) + ks * p.out_split_stride + static_cast<uint64_t>(row) * p.ldo + col;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_acc_empty[acc]);
     }
   }
   tc_fence_before();
@@ -309,30 +364,34 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
-// FC tail: h = ReLU(sum of split-K partials + b1) (fixed order), then
-// y = W2 h + b2 in fp32 (k-ascending, cnn.cpp:117-124).
-__global__ void __launch_bounds__(256) fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride,
-                                                      int hidden, const float* b1, const float* w2,
-                                                      const float* b2, int od, float* y, int samples) {
-  extern __shared__ float h[];
-  const int s = blockIdx.x;
+// FC tail, one warp per sample: h = ReLU(sum of split-K partials + b1) in a
+// fixed order, then y = W2 h + b2 with lanes striding k and a fixed shuffle
+// tree (deterministic, independent of the batch).
+constexpr int kTailWarps = 8;
+__global__ void __launch_bounds__(kTailWarps * 32)
+fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride, int hidden, const float* b1,
+               const float* w2t, const float* b2, int od, float* y, int samples) {
+  extern __shared__ float h_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kTailWarps + warp;
   if (s >= samples) return;
-  for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
+  float* h = h_all + warp * hidden;
+  for (int j = lane; j < hidden; j += 32) {
     float acc = 0.0f;
     for (int q = 0; q < nsplit; ++q) acc += part[q * split_stride + static_cast<uint64_t>(s) * hidden + j];
     h[j] = fmaxf(acc + b1[j], 0.0f);
   }
-  __syncthreads();
-  for (int o = threadIdx.x; o < od; o += blockDim.x) {
+  __syncwarp();
+  for (int o = 0; o < od; ++o) {
+    const float* w = w2t + static_cast<uint64_t>(o) * hidden;
     float acc = 0.0f;
-    for (int k = 0; k < hidden; ++k) acc = fmaf(w2[o + static_cast<uint64_t>(k) * od], h[k], acc);
-    y[static_cast<uint64_t>(s) * od + o] = acc + b2[o];
+    for (int k = lane; k < hidden; k += 32) acc = fmaf(w[k], h[k], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) y[static_cast<uint64_t>(s) * od + o] = acc + b2[o];
   }
 }
 
-// --------------------------------------------------------------------------
-// Host side
-// --------------------------------------------------------------------------
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -404,6 +463,7 @@ struct TcModel {
   int mode = kTF32x3;
   std::deque<TcWeights> conv;
   TcWeights fc1;
+  DevBuf w2t;   // fc2 weights transposed to [out_dim][hidden] (k contiguous)
   DevBuf part;  // split-K partials
 };
 
@@ -447,26 +507,27 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
 }
 
 size_t smem_bytes(int mode, int n, int chunks) {
-  size_t a = static_cast<size_t>(chunks) * kBM * 128;
-  size_t b = static_cast<size_t>(chunks) * n * 128;
-  size_t tot = a + b;
-  if (mode == kTF32x3) tot = 2 * (kMaxChunks * kBM * 128) + 2 * b;
-  else tot = kMaxChunks * kBM * 128 + b;
-  return tot + 1024;
+  const size_t w = static_cast<size_t>(chunks) * n * 128 * (mode == kTF32x3 ? 2 : 1);
+  const size_t a = static_cast<size_t>(kStages) * kAChunk * (mode == kTF32x3 ? 2 : 1);
+  return w + a + 1024;
 }
 
-template <int kMode>
-void launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const TcGemmParams& p,
-               dim3 grid, cudaStream_t s) {
-  const size_t sm = smem_bytes(kMode, p.n, p.chunks);
-  tc_gemm_kernel<kMode><<<grid, kThreads, sm, s>>>(a, b, blo, p);
-}
+int g_num_sms = 0;
 
 void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
-                 const TcGemmParams& p, dim3 grid, cudaStream_t s) {
-  if (mode == kBF16) launch_tc<kBF16>(a, b, blo, p, grid, s);
-  else if (mode == kTF32) launch_tc<kTF32>(a, b, blo, p, grid, s);
-  else launch_tc<kTF32x3>(a, b, blo, p, grid, s);
+                 const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int groups = ny * nz;
+  const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
+  const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
+  const size_t sm = smem_bytes(mode, p.n, p.chunks);
+  if (mode == kBF16) tc_layer_kernel<kBF16><<<grid, kLayerThreads, sm, s>>>(a, b, blo, p);
+  else if (mode == kTF32) tc_layer_kernel<kTF32><<<grid, kLayerThreads, sm, s>>>(a, b, blo, p);
+  else tc_layer_kernel<kTF32x3><<<grid, kLayerThreads, sm, s>>>(a, b, blo, p);
 }
 
 }  // namespace
@@ -479,28 +540,38 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   int cin = c.input_channels;
   for (int l = 0; l < c.n_conv; ++l) {
     const int k = 2 * cin;
-    if (c.conv[l] % 16 != 0 || c.conv[l] > 256) throw ApiError("tensor-core path: conv channels must be multiples of 16 <= 256");
+    if (c.conv[l] % 16 != 0 || (c.conv[l] > 128 && c.conv[l] % 128 != 0))
+      throw ApiError("tensor-core path: conv channels must be multiples of 16 (and of 128 above 128)");
     if ((k * esz + 127) / 128 > kMaxChunks) throw ApiError("tensor-core path: conv input width too large");
     if (c.residual) throw ApiError("tensor-core path: residual blocks not supported yet");
     cin = c.conv[l];
   }
   if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
   if (c.fc_hidden % 16 != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 16");
-  CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  CUDA_OK(cudaFuncSetAttribute(tc_gemm_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   auto* t = new TcModel();
   t->mode = mode;
   try {
     cin = c.input_channels;
     for (int l = 0; l < c.n_conv; ++l) t->conv.emplace_back();
     for (int l = 0; l < c.n_conv; ++l) {
-      upload_weights(t->conv[l], host_params + m.L.w[l], c.conv[l], 2 * cin, mode, c.conv[l], s);
+      upload_weights(t->conv[l], host_params + m.L.w[l], c.conv[l], 2 * cin, mode, std::min(c.conv[l], 128), s);
       cin = c.conv[l];
     }
     const int fc_tile = c.fc_hidden >= 64 ? 64 : c.fc_hidden;
     if (c.fc_hidden % fc_tile != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 64 (or <= 64)");
     upload_weights(t->fc1, host_params + m.L.fc1_w, c.fc_hidden, m.L.flat, mode, fc_tile, s);
+    // fc2 (reference column-major [od x hidden]) -> [od][hidden]
+    const int od = m.L.out_dim;
+    std::vector<float> w2t(static_cast<size_t>(od) * c.fc_hidden);
+    for (int o = 0; o < od; ++o)
+      for (int k = 0; k < c.fc_hidden; ++k)
+        w2t[static_cast<size_t>(o) * c.fc_hidden + k] = host_params[m.L.fc2_w + o + static_cast<size_t>(k) * od];
+    t->w2t.need(w2t.size() * 4);
+    CUDA_OK(cudaMemcpyAsync(t->w2t.p, w2t.data(), w2t.size() * 4, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
   } catch (...) {
     delete t;
     throw;
@@ -549,27 +620,25 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
                                static_cast<uint32_t>(kBM / olen)};
       amap = make_map(in, bf, 3, dims, strides, box);
       p.a3d = 1;
-      p.a_rows_per_box = olen;
-      p.a_samples_box = kBM / olen;
+        p.a_samples_box = kBM / olen;
     } else {
       const uint64_t dims[2] = {static_cast<uint64_t>(k), m_rows};
       const uint64_t strides[1] = {static_cast<uint64_t>(k) * esz};
       const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
       amap = make_map(in, bf, 2, dims, strides, box);
     }
+    const int bn = std::min(cout, 128);
     p.m = static_cast<int>(m_rows);
-    p.n = cout;
+    p.m_tiles = static_cast<int>((m_rows + kBM - 1) / kBM);
+    p.n = bn;
     p.chunks = (k * esz + 127) / 128;
-    p.ksteps = (k * esz + 31) / 32;
-    p.kc0 = 0;
+    p.ksteps_last = ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
     p.bias = P + m.L.b[l];
     p.relu = 1;
     p.out = fb.act[l];
     p.ldo = cout;
     p.out_bf16 = bf;
-    p.col0 = 0;
-    const dim3 grid(static_cast<unsigned>((m_rows + kBM - 1) / kBM), 1, 1);
-    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, p, grid, s);
+    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, p, cout / bn, 1, s);
     ++launches;
     in = fb.act[l];
     cin = cout;
@@ -591,26 +660,24 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     float* part = t.part.as<float>();
     TcGemmParams p{};
     p.m = static_cast<int>(samples);
+    p.m_tiles = static_cast<int>((samples + kBM - 1) / kBM);
     p.n = fc_tile;
     p.chunks = per;
-    p.ksteps = per * 4;
-    p.kc0 = per;
+    p.ksteps_last = 4;
     p.bias = nullptr;
     p.relu = 0;
     p.out = part;
     p.ldo = c.fc_hidden;
     p.out_bf16 = 0;
-    p.col0 = 0;
     p.out_split_stride = plane;
     if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
-    const dim3 grid(static_cast<unsigned>((samples + kBM - 1) / kBM), static_cast<unsigned>(t.fc1.npad / fc_tile),
-                    static_cast<unsigned>(nsplit));
-    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, grid, s);
+    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
     const int od = m.L.out_dim;
-    fc_tail_kernel<<<static_cast<unsigned>(samples), 256, c.fc_hidden * sizeof(float), s>>>(
-        part, nsplit, plane, c.fc_hidden, P + m.L.fc1_b, P + m.L.fc2_w, P + m.L.fc2_b, od, fb.y,
-        static_cast<int>(samples));
+    fc_tail_kernel<<<static_cast<unsigned>((samples + kTailWarps - 1) / kTailWarps), kTailWarps * 32,
+                     kTailWarps * c.fc_hidden * sizeof(float), s>>>(part, nsplit, plane, c.fc_hidden, P + m.L.fc1_b,
+                                                                     t.w2t.as<float>(), P + m.L.fc2_b, od, fb.y,
+                                                                     static_cast<int>(samples));
     ++launches;
   }
   return launches;
