@@ -253,6 +253,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     cp.x_stride = x_stride;
     cp.x_floats = x_floats;
     cp.x_bf16 = xprec == ILSIM_PREC_BF16;
+    cp.x_full = K > chunk;
     cp.max_context = mc;
     cp.bw = cfg.retire_bandwidth;
     cp.line = cfg.line_size;

@@ -43,7 +43,7 @@ struct __align__(16) SubState {
   uint32_t ph, pt, wh, wt;           // proc / write ring head, tail (monotonic counters)
   uint32_t status;
   uint32_t count_drain;
-  uint32_t pad_;
+  uint32_t xcols;                    // gathered-input columns written last round (zeroing bound)
   uint64_t err_tick;
 };
 static_assert(sizeof(SubState) == 128, "SubState layout");

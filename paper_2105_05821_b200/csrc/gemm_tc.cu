@@ -23,6 +23,7 @@
 #include <deque>
 #include <vector>
 
+#include "launch.cuh"
 #include "model.cuh"
 
 namespace simnet {
@@ -212,6 +213,10 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const int elems = kMode == kBF16 ? 64 : 32;  // elements per 128 B chunk
+  // PDL: let the next kernel start its prologue; everything above overlapped
+  // the previous kernel.  Weights are constants and may be fetched before the
+  // dependency wait; activations only after it.
+  asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -221,6 +226,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tma_load_2d(sW + c * bBytes, &tmB, &bar_w, (kc0 + c) * elems, ntile * p.n);
         if (kSplit) tma_load_2d(sWlo + c * bBytes, &tmBlo, &bar_w, (kc0 + c) * elems, ntile * p.n);
       }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
@@ -291,17 +297,20 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           float4* alo = reinterpret_cast<float4*>(sAlo + stage * kAChunk);
 #pragma unroll 4
           for (int i = t128; i < static_cast<int>(kAChunk / 16); i += 128) {
-            const float4 v = a[i];
-            float4 h, l;
-            h.x = __uint_as_float(tf32_rna(v.x));
-            h.y = __uint_as_float(tf32_rna(v.y));
-            h.z = __uint_as_float(tf32_rna(v.z));
-            h.w = __uint_as_float(tf32_rna(v.w));
-            l.x = __uint_as_float(tf32_rna(v.x - h.x));
-            l.y = __uint_as_float(tf32_rna(v.y - h.y));
-            l.z = __uint_as_float(tf32_rna(v.z - h.z));
-            l.w = __uint_as_float(tf32_rna(v.w - h.w));
-            a[i] = h;
+            const uint4 u = reinterpret_cast<const uint4*>(a)[i];
+            // hi = x rounded to tf32 (round half away, cvt.rna); lo = x - hi is
+            // exact in fp32 and is read by the MMA at tf32 precision
+            uint4 h;
+            h.x = (u.x + 0x1000u) & 0xffffe000u;
+            h.y = (u.y + 0x1000u) & 0xffffe000u;
+            h.z = (u.z + 0x1000u) & 0xffffe000u;
+            h.w = (u.w + 0x1000u) & 0xffffe000u;
+            float4 l;
+            l.x = __uint_as_float(u.x) - __uint_as_float(h.x);
+            l.y = __uint_as_float(u.y) - __uint_as_float(h.y);
+            l.z = __uint_as_float(u.z) - __uint_as_float(h.z);
+            l.w = __uint_as_float(u.w) - __uint_as_float(h.w);
+            reinterpret_cast<uint4*>(a)[i] = h;
             alo[i] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -315,6 +324,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   } else {
     // epilogue warps 6..9: TMEM lane quadrant = warp % 4
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int quad = warp & 3;
     int it = 0;
     for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x, ++it) {
@@ -364,31 +374,41 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
 }
 
-// FC tail, one warp per sample: h = ReLU(sum of split-K partials + b1) in a
-// fixed order, then y = W2 h + b2 with lanes striding k and a fixed shuffle
-// tree (deterministic, independent of the batch).
-constexpr int kTailWarps = 8;
-__global__ void __launch_bounds__(kTailWarps * 32)
+// FC tail: h = ReLU(sum of split-K partials + b1) summed in a fixed order,
+// then y = W2 h + b2 with W2 staged in shared memory; each (sample, output)
+// dot product is one warp with lanes striding k and a fixed shuffle tree
+// (deterministic and independent of the batch).
+constexpr int kTailSamples = 16;
+constexpr int kTailThreads = 256;
+__global__ void __launch_bounds__(kTailThreads)
 fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride, int hidden, const float* b1,
                const float* w2t, const float* b2, int od, float* y, int samples) {
-  extern __shared__ float h_all[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kTailWarps + warp;
-  if (s >= samples) return;
-  float* h = h_all + warp * hidden;
-  for (int j = lane; j < hidden; j += 32) {
+  extern __shared__ float sm_tail[];
+  float* w2s = sm_tail;                  // [od][hidden]
+  float* hs = sm_tail + od * hidden;     // [kTailSamples][hidden]
+  asm volatile("griddepcontrol.launch_dependents;");
+  for (int i = threadIdx.x; i < od * hidden; i += kTailThreads) w2s[i] = w2t[i];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int s0 = blockIdx.x * kTailSamples;
+  const int ns = min(kTailSamples, samples - s0);
+  for (int i = threadIdx.x; i < ns * hidden; i += kTailThreads) {
+    const int ls = i / hidden, j = i - ls * hidden;
+    const uint64_t off = static_cast<uint64_t>(s0 + ls) * hidden + j;
     float acc = 0.0f;
-    for (int q = 0; q < nsplit; ++q) acc += part[q * split_stride + static_cast<uint64_t>(s) * hidden + j];
-    h[j] = fmaxf(acc + b1[j], 0.0f);
+    for (int q = 0; q < nsplit; ++q) acc += part[q * split_stride + off];
+    hs[i] = fmaxf(acc + b1[j], 0.0f);
   }
-  __syncwarp();
-  for (int o = 0; o < od; ++o) {
-    const float* w = w2t + static_cast<uint64_t>(o) * hidden;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int task = warp; task < ns * od; task += kTailThreads / 32) {
+    const int ls = task / od, o = task - ls * od;
+    const float* w = w2s + o * hidden;
+    const float* h = hs + ls * hidden;
     float acc = 0.0f;
     for (int k = lane; k < hidden; k += 32) acc = fmaf(w[k], h[k], acc);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) y[static_cast<uint64_t>(s) * od + o] = acc + b2[o];
+    if (lane == 0) y[static_cast<uint64_t>(s0 + ls) * od + o] = acc + b2[o];
   }
 }
 
@@ -525,9 +545,9 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
   const size_t sm = smem_bytes(mode, p.n, p.chunks);
-  if (mode == kBF16) tc_layer_kernel<kBF16><<<grid, kLayerThreads, sm, s>>>(a, b, blo, p);
-  else if (mode == kTF32) tc_layer_kernel<kTF32><<<grid, kLayerThreads, sm, s>>>(a, b, blo, p);
-  else tc_layer_kernel<kTF32x3><<<grid, kLayerThreads, sm, s>>>(a, b, blo, p);
+  if (mode == kBF16) launch_pdl(tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
+  else if (mode == kTF32) launch_pdl(tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
+  else launch_pdl(tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
 }
 
 }  // namespace
@@ -551,6 +571,7 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(fc_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   auto* t = new TcModel();
   t->mode = mode;
   try {
@@ -674,10 +695,11 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
     const int od = m.L.out_dim;
-    fc_tail_kernel<<<static_cast<unsigned>((samples + kTailWarps - 1) / kTailWarps), kTailWarps * 32,
-                     kTailWarps * c.fc_hidden * sizeof(float), s>>>(part, nsplit, plane, c.fc_hidden, P + m.L.fc1_b,
-                                                                     t.w2t.as<float>(), P + m.L.fc2_b, od, fb.y,
-                                                                     static_cast<int>(samples));
+    const size_t tail_smem = static_cast<size_t>(od + kTailSamples) * c.fc_hidden * sizeof(float);
+    launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
+               dim3(kTailThreads), tail_smem, s, static_cast<const float*>(part), nsplit, plane, c.fc_hidden,
+               P + m.L.fc1_b, static_cast<const float*>(t.w2t.as<float>()), P + m.L.fc2_b, od, fb.y,
+               static_cast<int>(samples));
     ++launches;
   }
   return launches;

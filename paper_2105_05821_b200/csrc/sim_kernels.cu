@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "launch.cuh"
 #include "sim_kernels.cuh"
 
 namespace simnet {
@@ -99,6 +100,8 @@ ctx_kernel(CtxParams p) {
   __shared__ float s_sto[kCtxWarps][kMaxCols];
   __shared__ uint8_t s_flg[kCtxWarps][kMaxCols];
 
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t lane = lane_id();
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kCtxWarps + warp + p.first;
@@ -195,79 +198,112 @@ ctx_kernel(CtxParams p) {
   const uint64_t tpc = p.pc[tgt];
   const uint64_t taddr = p.addr[tgt];
   const bool tmem = (p.iflags[tgt] & kFlagMem) != 0;
-  for (uint32_t c = lane; c <= ncols; c += 32) {
-    if (c == 0) {
-      s_inst[warp][0] = static_cast<uint32_t>(tgt);
-      s_res[warp][0] = nc.zero[kSlotResidence];
-      s_exe[warp][0] = nc.zero[kSlotExecution];
-      s_sto[warp][0] = nc.zero[kSlotStore];
-      s_flg[warp][0] = 0;
-      continue;
+  // Column descriptors, 4 columns per lane in flight: ring entry, then the
+  // context instruction's pc/address/flags (newest first: proc, then write queue).
+  for (uint32_t c0 = 0; c0 <= ncols; c0 += 128) {
+    RingEntry e[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + u * 32 + lane;
+      ok[u] = c >= 1 && c <= ncols;
+      if (ok[u]) {
+        const uint32_t j = c - 1;
+        e[u] = j < nproc ? r.proc[(st.pt - 1 - j) & r.pmask] : r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
+      }
     }
-    const uint32_t j = c - 1;  // newest first: proc queue, then write queue
-    const RingEntry e = j < nproc ? r.proc[(st.pt - 1 - j) & r.pmask]
-                                  : r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
-    const uint64_t inst = st.begin + e.idx;
-    const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e.push));
-    s_inst[warp][c] = static_cast<uint32_t>(inst);
-    s_res[warp][c] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
-    s_exe[warp][c] = e.nexec;
-    s_sto[warp][c] = e.nstore;
-    // memory_dependency_flags (dataset.cpp:47-60)
-    const uint64_t cpc = p.pc[inst];
-    uint32_t f = (tpc / p.line) == (cpc / p.line) ? 1u : 0u;
-    if (tmem && (p.iflags[inst] & kFlagMem)) {
-      const uint64_t ca = p.addr[inst];
-      f |= (taddr == ca) ? 2u : 0u;
-      f |= (taddr / p.line) == (ca / p.line) ? 4u : 0u;
-      f |= (taddr / p.page) == (ca / p.page) ? 8u : 0u;
+    uint64_t cpc[4], ca[4];
+    uint8_t cf[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (ok[u]) {
+        const uint64_t inst = st.begin + e[u].idx;
+        cpc[u] = p.pc[inst];
+        ca[u] = p.addr[inst];
+        cf[u] = p.iflags[inst];
+      }
     }
-    f |= (tpc / p.page) == (cpc / p.page) ? 16u : 0u;
-    s_flg[warp][c] = static_cast<uint8_t>(f);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + u * 32 + lane;
+      if (c == 0) {
+        s_inst[warp][0] = static_cast<uint32_t>(tgt);
+        s_res[warp][0] = nc.zero[kSlotResidence];
+        s_exe[warp][0] = nc.zero[kSlotExecution];
+        s_sto[warp][0] = nc.zero[kSlotStore];
+        s_flg[warp][0] = 0;
+      } else if (ok[u]) {
+        const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e[u].push));
+        s_inst[warp][c] = static_cast<uint32_t>(st.begin + e[u].idx);
+        s_res[warp][c] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
+        s_exe[warp][c] = e[u].nexec;
+        s_sto[warp][c] = e[u].nstore;
+        // memory_dependency_flags (dataset.cpp:47-60)
+        uint32_t f = (tpc / p.line) == (cpc[u] / p.line) ? 1u : 0u;
+        if (tmem && (cf[u] & kFlagMem)) {
+          f |= (taddr == ca[u]) ? 2u : 0u;
+          f |= (taddr / p.line) == (ca[u] / p.line) ? 4u : 0u;
+          f |= (taddr / p.page) == (ca[u] / p.page) ? 8u : 0u;
+        }
+        f |= (tpc / p.page) == (cpc[u] / p.page) ? 16u : 0u;
+        s_flg[warp][c] = static_cast<uint8_t>(f);
+      }
+    }
   }
   __syncwarp();
 
-  // Coalesced write of the whole sample row: columns > ncols are exactly 0.
-  const uint32_t n4 = p.x_floats / 4;
+  // Row write: live columns, then zeros only where the previous round of this
+  // sub-trace left non-zero columns (the rest of the row is already 0).
   const uint32_t live = (ncols + 1) * kSlots;
+  const uint32_t prev = p.x_full ? p.x_floats : st.xcols * kSlots;
+  const uint32_t n4 = ((live > prev ? live : prev) + 3) / 4;
   float4* out4 = reinterpret_cast<float4*>(static_cast<float*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride));
   __nv_bfloat16* outb = static_cast<__nv_bfloat16*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride);
-  for (uint32_t q = lane; q < n4; q += 32) {
-    float v[4];
+  for (uint32_t q0 = 0; q0 < n4; q0 += 128) {
+    float v[4][4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t jf = 4 * q + t;
-      float val = 0.0f;
-      if (jf < live) {
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t jf = 4 * (q0 + u * 32 + lane) + t;
         const uint32_t col = jf / kSlots;
         const uint32_t slot = jf - col * kSlots;
-        if (slot < kStatic) {
-          val = __ldg(p.stat + static_cast<uint64_t>(s_inst[warp][col]) * kStatStride + slot);
-        } else if (slot == kSlotResidence) {
-          val = s_res[warp][col];
-        } else if (slot == kSlotExecution) {
-          val = s_exe[warp][col];
-        } else if (slot == kSlotStore) {
-          val = s_sto[warp][col];
-        } else if (slot < kSlotReserved) {
-          val = (s_flg[warp][col] >> (slot - kSlotFlag0)) & 1u ? nc.one[slot] : nc.zero[slot];
-        } else {
-          val = nc.zero[kSlotReserved];
+        float val = 0.0f;
+        if (jf < live) {
+          if (slot < kStatic) {
+            val = __ldg(p.stat + static_cast<uint64_t>(s_inst[warp][col]) * kStatStride + slot);
+          } else if (slot == kSlotResidence) {
+            val = s_res[warp][col];
+          } else if (slot == kSlotExecution) {
+            val = s_exe[warp][col];
+          } else if (slot == kSlotStore) {
+            val = s_sto[warp][col];
+          } else if (slot < kSlotReserved) {
+            val = (s_flg[warp][col] >> (slot - kSlotFlag0)) & 1u ? nc.one[slot] : nc.zero[slot];
+          } else {
+            val = nc.zero[kSlotReserved];
+          }
         }
+        v[u][t] = val;
       }
-      v[t] = val;
     }
-    if (p.x_bf16) {
-      const uint32_t row = (4 * q) / 100, within = 4 * q - 100 * row;
-      __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&a);
-      w.y = *reinterpret_cast<uint32_t*>(&b);
-      *reinterpret_cast<uint2*>(outb + row * 104 + within) = w;
-    } else {
-      out4[q] = make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = q0 + u * 32 + lane;
+      if (q >= n4) continue;
+      if (p.x_bf16) {
+        const uint32_t row = (4 * q) / 100, within = 4 * q - 100 * row;
+        __nv_bfloat162 a = __floats2bfloat162_rn(v[u][0], v[u][1]), b = __floats2bfloat162_rn(v[u][2], v[u][3]);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&a);
+        w.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(outb + row * 104 + within) = w;
+      } else {
+        out4[q] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+      }
     }
   }
+  if (lane == 0) sp->xcols = ncols + 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -302,6 +338,8 @@ __device__ void decode_triple(const float* y, const NormConsts& nc, int cf, int 
 }
 
 __global__ void decode_kernel(DecodeParams p) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x + p.first;
   if (s >= p.last) return;
   SubState* sp = p.state + s;
@@ -384,13 +422,13 @@ void launch_ctx(const CtxParams& p, cudaStream_t stream) {
   const uint64_t n = p.last - p.first;
   if (n == 0) return;
   const unsigned blocks = static_cast<unsigned>((n + kCtxWarps - 1) / kCtxWarps);
-  ctx_kernel<<<blocks, kCtxWarps * 32, 0, stream>>>(p);
+  launch_pdl(ctx_kernel, dim3(blocks), dim3(kCtxWarps * 32), 0, stream, p);
 }
 
 void launch_decode(const DecodeParams& p, cudaStream_t stream) {
   const uint64_t n = p.last - p.first;
   if (n == 0) return;
-  decode_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(p);
+  launch_pdl(decode_kernel, dim3(static_cast<unsigned>((n + 127) / 128)), dim3(128), 0, stream, p);
 }
 
 void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,

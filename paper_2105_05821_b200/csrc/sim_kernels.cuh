@@ -24,6 +24,7 @@ struct CtxParams {
   uint32_t x_stride;         // elements per sample in x
   uint32_t x_floats;         // logical floats per sample (100 per conv0 row, multiple of 4)
   int32_t x_bf16;            // 1: rows of 104 bf16 (100 + zero pad, TMA-aligned)
+  int32_t x_full;            // 1: rewrite whole rows (x rows shared between chunks)
   int32_t max_context;
   uint32_t bw, line, page;
   int32_t per_cycle;
