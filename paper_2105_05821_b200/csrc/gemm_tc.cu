@@ -375,40 +375,54 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 }
 
 // FC tail: h = ReLU(sum of split-K partials + b1) summed in a fixed order,
-// then y = W2 h + b2 with W2 staged in shared memory; each (sample, output)
-// dot product is one warp with lanes striding k and a fixed shuffle tree
-// (deterministic and independent of the batch).
+// then y = W2 h + b2 with W2 staged in shared memory (rows padded by one
+// float: conflict-free), one thread per (sample, output) with four
+// interleaved accumulators combined in a fixed order (deterministic and
+// independent of the batch).
 constexpr int kTailSamples = 16;
+constexpr int kMaxSplit = 8;  // split-K planes of FC1 (flat 1024 f32 = 32 chunks / 4)
 constexpr int kTailThreads = 256;
 __global__ void __launch_bounds__(kTailThreads)
 fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride, int hidden, const float* b1,
                const float* w2t, const float* b2, int od, float* y, int samples) {
   extern __shared__ float sm_tail[];
-  float* w2s = sm_tail;                  // [od][hidden]
-  float* hs = sm_tail + od * hidden;     // [kTailSamples][hidden]
+  const int ws = hidden + 1;
+  float* w2s = sm_tail;                  // [od][hidden + 1]
+  float* hs = sm_tail + od * ws;         // [kTailSamples][hidden]
   asm volatile("griddepcontrol.launch_dependents;");
-  for (int i = threadIdx.x; i < od * hidden; i += kTailThreads) w2s[i] = w2t[i];
+  for (int i = threadIdx.x; i < od * hidden; i += kTailThreads) {
+    const int o = i / hidden;
+    w2s[o * ws + (i - o * hidden)] = w2t[i];
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int s0 = blockIdx.x * kTailSamples;
   const int ns = min(kTailSamples, samples - s0);
   for (int i = threadIdx.x; i < ns * hidden; i += kTailThreads) {
     const int ls = i / hidden, j = i - ls * hidden;
     const uint64_t off = static_cast<uint64_t>(s0 + ls) * hidden + j;
+    float pv[kMaxSplit];
+#pragma unroll
+    for (int q = 0; q < kMaxSplit; ++q) pv[q] = q < nsplit ? part[q * split_stride + off] : 0.0f;  // all in flight
     float acc = 0.0f;
-    for (int q = 0; q < nsplit; ++q) acc += part[q * split_stride + off];
+#pragma unroll
+    for (int q = 0; q < kMaxSplit; ++q) acc += pv[q];  // fixed order (zeros past nsplit are exact)
     hs[i] = fmaxf(acc + b1[j], 0.0f);
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int task = warp; task < ns * od; task += kTailThreads / 32) {
+  for (int task = threadIdx.x; task < ns * od; task += kTailThreads) {
     const int ls = task / od, o = task - ls * od;
-    const float* w = w2s + o * hidden;
+    const float* w = w2s + o * ws;
     const float* h = hs + ls * hidden;
-    float acc = 0.0f;
-    for (int k = lane; k < hidden; k += 32) acc = fmaf(w[k], h[k], acc);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) y[static_cast<uint64_t>(s0 + ls) * od + o] = acc + b2[o];
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    int k = 0;
+    for (; k + 4 <= hidden; k += 4) {
+      a0 = fmaf(w[k], h[k], a0);
+      a1 = fmaf(w[k + 1], h[k + 1], a1);
+      a2 = fmaf(w[k + 2], h[k + 2], a2);
+      a3 = fmaf(w[k + 3], h[k + 3], a3);
+    }
+    for (; k < hidden; ++k) a0 = fmaf(w[k], h[k], a0);
+    y[static_cast<uint64_t>(s0 + ls) * od + o] = ((a0 + a1) + (a2 + a3)) + b2[o];
   }
 }
 
@@ -692,10 +706,11 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     p.out_bf16 = 0;
     p.out_split_stride = plane;
     if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
+    if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
     launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
     const int od = m.L.out_dim;
-    const size_t tail_smem = static_cast<size_t>(od + kTailSamples) * c.fc_hidden * sizeof(float);
+    const size_t tail_smem = (static_cast<size_t>(od) * (c.fc_hidden + 1) + kTailSamples * c.fc_hidden) * sizeof(float);
     launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
                dim3(kTailThreads), tail_smem, s, static_cast<const float*>(part), nsplit, plane, c.fc_hidden,
                P + m.L.fc1_b, static_cast<const float*>(t.w2t.as<float>()), P + m.L.fc2_b, od, fb.y,

@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "host_util.cuh"
 
 namespace simnet {
@@ -20,8 +22,11 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // Opt-in: measured slower on B200 for this round loop (early dependents
+  // launch and then contend with the running kernel), so off by default.
+  static const bool disabled = std::getenv("SIMNET_PDL") == nullptr;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = disabled ? 0 : 1;
   CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
