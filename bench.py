@@ -44,7 +44,8 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--precision", default=os.environ.get("SIMNET_PRECISION", "fp32"))
+    p.add_argument("--precision", default=os.environ.get("SIMNET_PRECISION", "tf32x3"),
+                   choices=["fp32", "tf32x3", "tf32", "bf16"])
     p.add_argument("--n", type=int, default=N_INSTR)
     p.add_argument("--k", type=int, default=K_SUB)
     p.add_argument("--regime", default="default", choices=["default", "memory"])
@@ -245,16 +246,12 @@ def main():
         barrier()
         wall = time.perf_counter() - t0
     step_ms = sum(dev_ms) / len(dev_ms)
-    # max over ranks of the device time, and the one collective: totals
-    totals = torch.tensor([r.total_cycles, r.instructions, sum(s.sum_fetch for s in r.sub_results),
-                           sum(s.delta for s in r.sub_results), sum(s.drain_cycles for s in r.sub_results),
-                           sum(s.overflow_stall_cycles for s in r.sub_results)], dtype=torch.int64, device="cuda")
-    tmax = torch.tensor([step_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(totals)
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-    step_ms_max = float(tmax.item())
-    n_all = int(totals[1].item())
+    # max over ranks of the device time, and the one collective: the totals
+    from paper_2105_05821_b200.dist import Totals, all_reduce_totals, max_over_ranks
+
+    tot = all_reduce_totals(Totals.of(r.sub_results), device="cuda")
+    step_ms_max = max_over_ranks(step_ms, device="cuda")
+    n_all = tot.instructions
     value = n_all / (step_ms_max / 1e3) / 1e6
 
     # kernel breakdown + roofline of the dominant kernel (instrumented pass)
@@ -286,12 +283,10 @@ def main():
             t1 = time.perf_counter()
             g.simulate_parallel(ptrace, pc)
             e2e_s.append(time.perf_counter() - t1)
-        e2e_t = torch.tensor([statistics.median(e2e_s)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = max_over_ranks(statistics.median(e2e_s), device="cuda")
         h2d = trace_h2d_bytes(trace)
         d2h = args.k * 56 + trace.n * 4
-        e2e_line = {"value": n_all / e2e_t.item() / 1e6, "unit": "MIPS", "h2d_bytes_per_step": h2d,
+        e2e_line = {"value": n_all / e2e_t / 1e6, "unit": "MIPS", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "scope": "ilsim_gpu_simulate_parallel: H2D trace + pack + rounds + "
                                                         "D2H sub-results and predicted fetch series (wall clock)"}
 
@@ -315,7 +310,7 @@ def main():
                    "precision": args.precision, "regime": args.regime, "sub_traces": args.k * world,
                    "instructions": n_all, "rounds": r0.rounds,
                    "l2": "trace+state > 126 MB L2 per step (no flush needed)"},
-        "cpi": int(totals[0].item()) / max(n_all, 1),
+        "cpi": tot.cpi,
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "kernels_ms_per_step": k_ms,
         "roofline": roofline,

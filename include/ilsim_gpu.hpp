@@ -1,0 +1,160 @@
+// ilsim_gpu.hpp — header-only C++ adapter from the reference's types
+// (ilsim::AnnotatedInstruction, ModelWeights, ParallelConfig, ParallelResult;
+// /root/reference/proj/include/ilsim) onto the C-ABI in ilsim_gpu.h.
+//
+// A reference maintainer adds this next to parallel.hpp and calls
+//   ilsim::gpu::simulate_parallel_gpu(trace, weights, config)
+// wherever simulate_parallel(trace, cnn_predictor, config) is called today
+// (tools/ilsim_main.cpp:148-169, bindings/module.cpp:131-155).  Errors are
+// rethrown as ilsim::Error with the library's message.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "ilsim/cnn.hpp"
+#include "ilsim/parallel.hpp"
+#include "ilsim_gpu.h"
+
+namespace ilsim::gpu {
+
+class Context {
+public:
+  explicit Context(int device = 0, int precision = ILSIM_PREC_TF32X3) {
+    ilsim_gpu_options o{};
+    o.device = device;
+    o.precision = precision;
+    char err[512] = {0};
+    if (ilsim_gpu_create(&o, &ctx_, err, sizeof err) != 0) throw Error(err);
+  }
+  ~Context() { ilsim_gpu_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  // load_model (cnn.cpp:662-697) output -> device (CnnPredictor ctor).
+  void load_model(const ModelWeights& w) {
+    ilsim_cnn_config c{};
+    c.input_channels = w.config.input_channels;
+    c.max_context = w.config.max_context;
+    c.sequence_length = w.config.sequence_length;
+    c.n_conv = static_cast<int32_t>(w.config.conv_channels.size());
+    for (int i = 0; i < c.n_conv && i < 8; ++i) c.conv[i] = w.config.conv_channels[i];
+    c.fc_hidden = w.config.fc_hidden;
+    c.class_fetch = w.config.class_fetch;
+    c.class_exec = w.config.class_exec;
+    c.class_store = w.config.class_store;
+    c.residual = w.config.residual_blocks ? 1 : 0;
+    double norm[106];
+    for (int k = 0; k < 50; ++k) {
+      norm[k] = w.norm.mean[k];
+      norm[50 + k] = w.norm.stdev[k];
+    }
+    for (int k = 0; k < 3; ++k) {
+      norm[100 + k] = w.norm.label_mean[k];
+      norm[103 + k] = w.norm.label_stdev[k];
+    }
+    check(ilsim_gpu_load_model(ctx_, &c, norm, w.params.data(), w.params.size()));
+    max_context_ = w.config.max_context;
+  }
+
+  // simulate_parallel (parallel.cpp:26-93) on the GPU.
+  ParallelResult simulate_parallel(std::span<const AnnotatedInstruction> trace, const ParallelConfig& pc,
+                                   bool oracle = false) {
+    Soa soa(trace);
+    ilsim_sim_config c{};
+    c.k = pc.k;
+    c.subtrace_size = pc.subtrace_size;
+    c.batch_max = pc.batch_max;
+    c.max_context = pc.sim.max_context;
+    c.retire_bandwidth = pc.sim.retire_bandwidth;
+    c.per_cycle_advance = pc.sim.per_cycle_advance ? 1 : 0;
+    c.record_fetch = pc.sim.record_fetch ? 1 : 0;
+    c.oracle = oracle ? 1 : 0;
+    c.line_size = pc.sim.line_size;
+    c.page_size = pc.sim.page_size;
+    uint64_t k = pc.k;
+    if (pc.subtrace_size > 0 && k == 0) k = trace.empty() ? 1 : (trace.size() + pc.subtrace_size - 1) / pc.subtrace_size;
+    if (k == 0) k = 1;
+    std::vector<ilsim_sub_result> subs(k);
+    std::vector<uint32_t> fetch(pc.sim.record_fetch ? trace.size() : 0);
+    ilsim_totals tot{};
+    check(ilsim_gpu_simulate_parallel(ctx_, &soa.view, &c, subs.data(), subs.size(),
+                                      fetch.empty() ? nullptr : fetch.data(), &tot));
+    ParallelResult out;
+    out.instructions = trace.size();
+    size_t off = 0;
+    for (uint64_t i = 0; i < tot.sub_traces; ++i) {
+      SimResult r;
+      r.instructions = subs[i].instructions;
+      r.total_cycles = subs[i].total_cycles;
+      r.sum_fetch = subs[i].sum_fetch;
+      r.delta = subs[i].delta;
+      r.drain_cycles = subs[i].drain_cycles;
+      r.overflow_stall_cycles = subs[i].overflow_stall_cycles;
+      r.empty = subs[i].empty != 0;
+      r.cpi = r.instructions ? static_cast<double>(r.total_cycles) / r.instructions : 0.0;
+      if (!fetch.empty()) r.predicted_fetch.assign(fetch.begin() + off, fetch.begin() + off + r.instructions);
+      off += r.instructions;
+      out.total_cycles += r.total_cycles;
+      out.sub_results.push_back(std::move(r));
+    }
+    out.cpi = trace.empty() ? 0.0 : static_cast<double>(out.total_cycles) / trace.size();
+    out.predicted_fetch = std::move(fetch);
+    return out;
+  }
+
+private:
+  struct Soa {  // AnnotatedInstruction (trace.hpp:98-109) -> structure of arrays
+    std::vector<uint64_t> pc, addr;
+    std::vector<uint8_t> op, has;
+    std::vector<uint16_t> src, dst, hist;
+    std::vector<uint32_t> truth;
+    ilsim_trace_view view{};
+    explicit Soa(std::span<const AnnotatedInstruction> t) {
+      const size_t n = t.size();
+      pc.resize(n);
+      addr.resize(n);
+      has.resize(n);
+      op.resize(n * 13);
+      src.resize(n * 8);
+      dst.resize(n * 6);
+      hist.resize(n * 14);
+      truth.resize(n * 3);
+      for (size_t i = 0; i < n; ++i) {
+        const auto& a = t[i];
+        pc[i] = a.stat.pc;
+        addr[i] = a.stat.has_data ? a.stat.data_addr : 0;
+        has[i] = a.stat.has_data ? 1 : 0;
+        for (int j = 0; j < 13; ++j) op[i * 13 + j] = a.stat.op[j];
+        for (int j = 0; j < 8; ++j) src[i * 8 + j] = a.stat.src[j];
+        for (int j = 0; j < 6; ++j) dst[i * 6 + j] = a.stat.dst[j];
+        for (int j = 0; j < 14; ++j) hist[i * 14 + j] = a.hist.v[j];
+        truth[i * 3 + 0] = a.truth.fetch;
+        truth[i * 3 + 1] = a.truth.execution;
+        truth[i * 3 + 2] = a.truth.store;
+      }
+      view = ilsim_trace_view{n, pc.data(), op.data(), src.data(), dst.data(), has.data(), addr.data(), hist.data(),
+                              truth.data()};
+    }
+  };
+
+  void check(int rc) {
+    if (rc != 0) throw Error(ilsim_gpu_last_error(ctx_));
+  }
+
+  ilsim_gpu_ctx* ctx_ = nullptr;
+  int max_context_ = 110;
+};
+
+// Drop-in for `simulate_parallel(trace, CnnPredictor(weights), config)`.
+inline ParallelResult simulate_parallel_gpu(std::span<const AnnotatedInstruction> trace, const ModelWeights& w,
+                                            const ParallelConfig& config, int device = 0,
+                                            int precision = ILSIM_PREC_TF32X3) {
+  Context ctx(device, precision);
+  ctx.load_model(w);
+  return ctx.simulate_parallel(trace, config);
+}
+
+}  // namespace ilsim::gpu

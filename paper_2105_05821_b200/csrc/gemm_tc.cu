@@ -390,9 +390,23 @@ fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride, int hidden,
   float* w2s = sm_tail;                  // [od][hidden + 1]
   float* hs = sm_tail + od * ws;         // [kTailSamples][hidden]
   asm volatile("griddepcontrol.launch_dependents;");
-  for (int i = threadIdx.x; i < od * hidden; i += kTailThreads) {
-    const int o = i / hidden;
-    w2s[o * ws + (i - o * hidden)] = w2t[i];
+  {
+    // each thread stages a contiguous run of W2 rows: 8 loads in flight, no division
+    const int total = od * hidden;
+    for (int base = threadIdx.x * 8; base < total; base += kTailThreads * 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = base + u < total ? __ldg(w2t + base + u) : 0.0f;
+      int o = base / hidden, k = base - o * hidden;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (base + u < total) w2s[o * ws + k] = v[u];
+        if (++k == hidden) {
+          k = 0;
+          ++o;
+        }
+      }
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int s0 = blockIdx.x * kTailSamples;

@@ -1,0 +1,81 @@
+"""Multi-GPU plumbing: one process per GPU, sub-traces sharded contiguously.
+
+Sub-traces are independent (parallel.cpp:51-58; "no inter-GPU communication
+is required during the simulation process"), so rank r
+simulates sub-traces [shard_begin, shard_end) of the reference's global
+partition (parallel.cpp:9-24) and owns one contiguous instruction range.  The
+only collective is one all-reduce of the per-shard totals after the last
+round (NCCL over NVLink on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+TOTAL_FIELDS = ("total_cycles", "instructions", "sum_fetch", "delta", "drain_cycles", "overflow_stall_cycles")
+
+
+def shard_range(k: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of sub-traces for `rank` (first ranks take the remainder)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, rem = divmod(k, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+@dataclass
+class Totals:
+    total_cycles: int = 0
+    instructions: int = 0
+    sum_fetch: int = 0
+    delta: int = 0
+    drain_cycles: int = 0
+    overflow_stall_cycles: int = 0
+
+    @staticmethod
+    def of(subs) -> "Totals":
+        t = Totals()
+        for s in subs:
+            for f in TOTAL_FIELDS:
+                setattr(t, f, getattr(t, f) + int(getattr(s, f) if not isinstance(s, dict) else s[f]))
+        return t
+
+    def as_list(self) -> list[int]:
+        return [getattr(self, f) for f in TOTAL_FIELDS]
+
+    @property
+    def cpi(self) -> float:
+        return self.total_cycles / self.instructions if self.instructions else 0.0
+
+
+def all_reduce_totals(t: Totals, device=None) -> Totals:
+    """Sum the shard totals over all ranks (exact: integer sums)."""
+    import torch
+    import torch.distributed as dist
+
+    v = torch.tensor(t.as_list(), dtype=torch.int64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+    return Totals(*[int(x) for x in v.tolist()])
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank timing (multi-GPU times are the slowest rank's)."""
+    import torch
+    import torch.distributed as dist
+
+    v = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    return float(v.item())
+
+
+def simulate_sharded(sim, trace, pc, rank: int, world: int, *, oracle: bool = False):
+    """Run this rank's shard of the global partition on its GPU and return
+    (shard ParallelResult, global Totals)."""
+    from .api import GpuSimulator
+
+    k = GpuSimulator._num_sub(pc, trace.n, False)
+    shard = shard_range(k, rank, world)
+    res = sim.simulate_parallel(trace, pc, oracle=oracle, shard=shard)
+    return res, all_reduce_totals(Totals.of(res.sub_results), device="cuda")

@@ -111,3 +111,42 @@ def test_format_errors(tmp_path):
     p.write_bytes(raw[:-5])
     with pytest.raises(IlsimError, match="trace truncated"):
         read_trace(p)
+
+
+def test_cpp_adapter_compiles_against_reference_headers(tmp_path, L):
+    """include/ilsim_gpu.hpp adapts the reference's own C++ types onto the
+    C-ABI; build a caller against /root/reference headers and run it (no GPU
+    here: the adapter must surface the library error as ilsim::Error)."""
+    import shutil
+    import subprocess
+
+    ref_inc = Path("/root/reference/proj/include")
+    if not ref_inc.exists() or not shutil.which("g++"):
+        pytest.skip("reference headers or g++ unavailable")
+    src = tmp_path / "adapter.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "ilsim_gpu.hpp"
+int main() {
+  std::vector<ilsim::AnnotatedInstruction> trace(10);
+  ilsim::ModelWeights w;
+  w.params.assign(293857, 0.0f);  // default CnnConfig == preset_c3(110)
+  ilsim::ParallelConfig pc;
+  pc.k = 2;
+  try {
+    auto r = ilsim::gpu::simulate_parallel_gpu(trace, w, pc);
+    std::printf("ok %llu\n", (unsigned long long)r.total_cycles);
+  } catch (const ilsim::Error& e) {
+    std::printf("error: %s\n", e.what());
+  }
+  return 0;
+}
+''')
+    exe = tmp_path / "adapter"
+    lib_dir = ROOT / "paper_2105_05821_b200"
+    subprocess.run(["g++", "-std=c++20", "-I", str(ROOT / "include"), "-I", str(ref_inc), str(src), "-o", str(exe),
+                    "-L", str(lib_dir), "-l:libilsim_gpu.so", f"-Wl,-rpath,{lib_dir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout
+    import torch
+
+    assert out.startswith("ok" if torch.cuda.is_available() else "error:"), out
