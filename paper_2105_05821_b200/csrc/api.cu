@@ -263,11 +263,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     launch_ctx(cp, c->stream);
     return uint64_t{1};
   };
-  auto do_forward = [&](uint64_t f, uint64_t l) -> uint64_t {
-    if (oracle) return 0;
-    return forward_launch(c->model, c->precision, d_x, x_stride, l - f, fb, c->stream);
-  };
-  auto do_decode = [&](uint64_t f, uint64_t l) {
+  auto decode_params = [&](uint64_t f, uint64_t l) {
     DecodeParams dp{};
     dp.state = d_state;
     dp.first = f;
@@ -282,8 +278,18 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     dp.class_exec = c->cfg.class_exec;
     dp.class_store = c->cfg.class_store;
     dp.per_cycle = cfg.per_cycle_advance;
-    launch_decode(dp, c->stream);
-    return uint64_t{1};
+    return dp;
+  };
+  bool k3_fused = false;  // tensor-core tails run K3 themselves
+  auto do_forward = [&](uint64_t f, uint64_t l) -> uint64_t {
+    if (oracle) return 0;
+    const DecodeParams dp = decode_params(f, l);
+    return forward_launch(c->model, c->precision, d_x, x_stride, l - f, fb, c->stream, &dp, &k3_fused);
+  };
+  auto do_decode = [&](uint64_t f, uint64_t l) -> uint64_t {
+    if (k3_fused) return 0;
+    launch_decode(decode_params(f, l), c->stream);
+    return 1;
   };
   auto launch_round = [&]() -> uint64_t {
     uint64_t launches = 0;

@@ -23,8 +23,10 @@
 #include <deque>
 #include <vector>
 
+#include "decode.cuh"
 #include "launch.cuh"
 #include "model.cuh"
+#include "sim_kernels.cuh"
 
 namespace simnet {
 
@@ -374,69 +376,78 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
 }
 
-// FC tail: h = ReLU(sum of split-K partials + b1) summed in a fixed order,
-// then y = W2 h + b2 with W2 staged in shared memory (rows padded by one
-// float: conflict-free), one thread per (sample, output) with four
-// interleaved accumulators combined in a fixed order (deterministic and
-// independent of the batch).
-constexpr int kTailSamples = 16;
+// FC tail (+ fused K3): h = ReLU(sum of split-K partials + b1), summed in a
+// fixed order; y = W2 h + b2 in fp32 with four interleaved accumulators
+// combined in a fixed order (deterministic, batch-independent); then, when
+// simulating, the hybrid decode and clock advance of K3 for each sample.
+constexpr int kTailSamples = 4;
 constexpr int kMaxSplit = 8;  // split-K planes of FC1 (flat 1024 f32 = 32 chunks / 4)
-constexpr int kTailThreads = 256;
-__global__ void __launch_bounds__(kTailThreads)
-fc_tail_kernel(const float* part, int nsplit, uint64_t split_stride, int hidden, const float* b1,
-               const float* w2t, const float* b2, int od, float* y, int samples) {
-  extern __shared__ float sm_tail[];
-  const int ws = hidden + 1;
-  float* w2s = sm_tail;                  // [od][hidden + 1]
-  float* hs = sm_tail + od * ws;         // [kTailSamples][hidden]
+constexpr int kTailThreads = 128;
+constexpr int kMaxHidden = 1024;
+constexpr int kMaxOut = 64;
+
+struct TailParams {
+  const float* part;
+  int nsplit;
+  uint64_t split_stride;
+  int hidden;
+  const float* b1;
+  const float* w2t;  // [od][hidden]
+  const float* b2;
+  int od;
+  float* y;
+  int samples;
+  DecodeParams dec;  // dec.state == nullptr: outputs only
+};
+
+__global__ void __launch_bounds__(kTailThreads) fc_tail_kernel(TailParams p) {
+  __shared__ float hs[kTailSamples][kMaxHidden];
+  __shared__ float ys[kTailSamples][kMaxOut];
   asm volatile("griddepcontrol.launch_dependents;");
-  {
-    // each thread stages a contiguous run of W2 rows: 8 loads in flight, no division
-    const int total = od * hidden;
-    for (int base = threadIdx.x * 8; base < total; base += kTailThreads * 8) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = base + u < total ? __ldg(w2t + base + u) : 0.0f;
-      int o = base / hidden, k = base - o * hidden;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (base + u < total) w2s[o * ws + k] = v[u];
-        if (++k == hidden) {
-          k = 0;
-          ++o;
-        }
-      }
-    }
-  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int s0 = blockIdx.x * kTailSamples;
-  const int ns = min(kTailSamples, samples - s0);
-  for (int i = threadIdx.x; i < ns * hidden; i += kTailThreads) {
-    const int ls = i / hidden, j = i - ls * hidden;
-    const uint64_t off = static_cast<uint64_t>(s0 + ls) * hidden + j;
+  const int ns = min(kTailSamples, p.samples - s0);
+  const int hid = p.hidden;
+  for (int i = threadIdx.x; i < ns * hid; i += kTailThreads) {
+    const int ls = i / hid, j = i - ls * hid;
+    const uint64_t off = static_cast<uint64_t>(s0 + ls) * hid + j;
     float pv[kMaxSplit];
 #pragma unroll
-    for (int q = 0; q < kMaxSplit; ++q) pv[q] = q < nsplit ? part[q * split_stride + off] : 0.0f;  // all in flight
+    for (int q = 0; q < kMaxSplit; ++q) pv[q] = q < p.nsplit ? __ldg(p.part + q * p.split_stride + off) : 0.0f;
     float acc = 0.0f;
 #pragma unroll
     for (int q = 0; q < kMaxSplit; ++q) acc += pv[q];  // fixed order (zeros past nsplit are exact)
-    hs[i] = fmaxf(acc + b1[j], 0.0f);
+    hs[ls][j] = fmaxf(acc + __ldg(p.b1 + j), 0.0f);
   }
   __syncthreads();
-  for (int task = threadIdx.x; task < ns * od; task += kTailThreads) {
-    const int ls = task / od, o = task - ls * od;
-    const float* w = w2s + o * ws;
-    const float* h = hs + ls * hidden;
+  for (int task = threadIdx.x; task < ns * p.od; task += kTailThreads) {
+    const int ls = task / p.od, o = task - ls * p.od;
+    const float4* w = reinterpret_cast<const float4*>(p.w2t + static_cast<uint64_t>(o) * hid);
+    const float* h = hs[ls];
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-    int k = 0;
-    for (; k + 4 <= hidden; k += 4) {
-      a0 = fmaf(w[k], h[k], a0);
-      a1 = fmaf(w[k + 1], h[k + 1], a1);
-      a2 = fmaf(w[k + 2], h[k + 2], a2);
-      a3 = fmaf(w[k + 3], h[k + 3], a3);
+#pragma unroll 4
+    for (int k4 = 0; k4 < hid / 4; ++k4) {
+      const float4 wv = __ldg(w + k4);
+      a0 = fmaf(wv.x, h[4 * k4 + 0], a0);
+      a1 = fmaf(wv.y, h[4 * k4 + 1], a1);
+      a2 = fmaf(wv.z, h[4 * k4 + 2], a2);
+      a3 = fmaf(wv.w, h[4 * k4 + 3], a3);
     }
-    for (; k < hidden; ++k) a0 = fmaf(w[k], h[k], a0);
-    y[static_cast<uint64_t>(s0 + ls) * od + o] = ((a0 + a1) + (a2 + a3)) + b2[o];
+    const float v = ((a0 + a1) + (a2 + a3)) + __ldg(p.b2 + o);
+    ys[ls][o] = v;
+    p.y[static_cast<uint64_t>(s0 + ls) * p.od + o] = v;
+  }
+  if (p.dec.state == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x < ns) {  // K3: decode + clock for this sample's sub-trace
+    const DecodeParams& d = p.dec;
+    SubState* sp = d.state + d.first + s0 + threadIdx.x;
+    if (sp->status == kOk && sp->pos < sp->len) {
+      uint32_t t[3];
+      decode_triple(ys[threadIdx.x], *d.nc, d.class_fetch, d.class_exec, d.class_store,
+                    (d.iflags[sp->begin + sp->pos] & kFlagStore) != 0, t);
+      apply_decoded(sp, t, d.pred_fetch, d.per_cycle);
+    }
   }
 }
 
@@ -599,7 +610,6 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CUDA_OK(cudaFuncSetAttribute(fc_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   auto* t = new TcModel();
   t->mode = mode;
   try {
@@ -640,7 +650,7 @@ void tc_prepare(const DevModel& m, uint64_t samples) {
 }
 
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride, uint64_t samples,
-                    const ForwardBuffers& fb, cudaStream_t s) {
+                    const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse) {
   (void)precision;
   TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
@@ -724,11 +734,22 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
     const int od = m.L.out_dim;
-    const size_t tail_smem = (static_cast<size_t>(od) * (c.fc_hidden + 1) + kTailSamples * c.fc_hidden) * sizeof(float);
+    if (c.fc_hidden > kMaxHidden || od > kMaxOut || c.fc_hidden % 4 != 0)
+      throw ApiError("tensor-core path: FC tail supports fc_hidden <= 1024 (multiple of 4), <= 64 outputs");
+    TailParams tp{};
+    tp.part = part;
+    tp.nsplit = nsplit;
+    tp.split_stride = plane;
+    tp.hidden = c.fc_hidden;
+    tp.b1 = P + m.L.fc1_b;
+    tp.w2t = t.w2t.as<float>();
+    tp.b2 = P + m.L.fc2_b;
+    tp.od = od;
+    tp.y = fb.y;
+    tp.samples = static_cast<int>(samples);
+    if (fuse) tp.dec = *fuse;
     launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
-               dim3(kTailThreads), tail_smem, s, static_cast<const float*>(part), nsplit, plane, c.fc_hidden,
-               P + m.L.fc1_b, static_cast<const float*>(t.w2t.as<float>()), P + m.L.fc2_b, od, fb.y,
-               static_cast<int>(samples));
+               dim3(kTailThreads), 0, s, tp);
     ++launches;
   }
   return launches;

@@ -160,8 +160,13 @@ ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, D
 }
 
 uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32_t x_stride,
-                        uint64_t samples, const ForwardBuffers& fb, cudaStream_t s) {
-  if (precision != ILSIM_PREC_FP32) return tc_forward(m, precision, xv, x_stride, samples, fb, s);
+                        uint64_t samples, const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse,
+                        bool* fused) {
+  if (fused) *fused = false;
+  if (precision != ILSIM_PREC_FP32) {
+    if (fused) *fused = fuse != nullptr;
+    return tc_forward(m, precision, xv, x_stride, samples, fb, s, fuse);
+  }
   const float* x = static_cast<const float*>(xv);
   const ilsim_cnn_config& c = m.cfg;
   const float* P = m.params.as<float>();

@@ -7,6 +7,7 @@
 
 #include "../../include/ilsim_gpu.h"
 #include "host_util.cuh"
+#include "sim_kernels.cuh"
 
 namespace simnet {
 
@@ -59,14 +60,17 @@ void model_upload(DevModel& m, const ilsim_cnn_config& c, const float* params, i
                   cudaStream_t s);
 ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, DevBuf& y);
 // Runs the forward for `samples` gathered rows; returns kernels launched.
+// With `fuse`, the tensor-core path also performs K3 (decode + clock) in its
+// tail and returns true in *fused.
 uint64_t forward_launch(const DevModel& m, int precision, const void* x, uint32_t x_stride,
-                        uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
+                        uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
+                        const DecodeParams* fuse = nullptr, bool* fused = nullptr);
 
 // tensor-core path (gemm_tc.cu)
 TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s);
 void tc_model_destroy(TcModel* t);
 void tc_prepare(const DevModel& m, uint64_t samples);
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride,
-                    uint64_t samples, const ForwardBuffers& fb, cudaStream_t s);
+                    uint64_t samples, const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse);
 
 }  // namespace simnet

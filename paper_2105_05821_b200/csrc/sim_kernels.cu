@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "decode.cuh"
 #include "launch.cuh"
 #include "sim_kernels.cuh"
 
@@ -309,34 +310,6 @@ ctx_kernel(CtxParams p) {
 // ---------------------------------------------------------------------------
 // K3: hybrid decode (or truth in oracle mode) and the fetch-clock advance.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t decode_head(const float* y, int base, int n, float r,
-                                                double mu, double sigma) {
-  int best = 0;
-  float bv = y[base];
-  for (int i = 1; i < n; ++i) {
-    const float v = y[base + i];
-    if (v > bv) {  // strict: first maximum wins, NaN never wins (cnn.cpp:388-393)
-      bv = v;
-      best = i;
-    }
-  }
-  if (best < n - 1) return static_cast<uint32_t>(best);
-  // overflow class: de-normalise out of log1p space (cnn.cpp:399-401); the
-  // reference's -march=native build contracts r*sigma+mu into one fp64 FMA.
-  const double z = fmin(fma(static_cast<double>(r), sigma, mu), 22.0);
-  const double raw = fmax(0.0, expm1(z));
-  const long long v = llround(fmin(raw, 4.0e9));
-  return static_cast<uint32_t>(v > 0xffffffffLL ? 0xffffffffLL : v);
-}
-
-__device__ void decode_triple(const float* y, const NormConsts& nc, int cf, int ce, int cs,
-                              bool is_store, uint32_t* out) {
-  out[0] = decode_head(y, 3, cf, y[0], nc.label_mean[0], nc.label_sd[0]);
-  const uint32_t e = decode_head(y, 3 + cf, ce, y[1], nc.label_mean[1], nc.label_sd[1]);
-  out[1] = e < 1u ? 1u : e;
-  out[2] = is_store ? decode_head(y, 3 + cf + ce, cs, y[2], nc.label_mean[2], nc.label_sd[2]) : 0u;
-}
-
 __global__ void decode_kernel(DecodeParams p) {
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -357,15 +330,7 @@ __global__ void decode_kernel(DecodeParams p) {
     decode_triple(y, *p.nc, p.class_fetch, p.class_exec, p.class_store,
                   (p.iflags[idx] & kFlagStore) != 0, t);
   }
-  sp->pend_f = t[0];
-  sp->pend_e = t[1];
-  sp->pend_s = t[2];
-  sp->has_pend = 1;
-  if (!p.per_cycle && t[0] > 0) sp->cur += t[0];  // advance_cycles(F, ...): cur += F
-  if (pos >= sp->warm) {
-    sp->sum_fetch += t[0];
-    if (p.pred_fetch) p.pred_fetch[sp->fetch_off + (pos - sp->warm)] = t[0];
-  }
+  apply_decoded(sp, t, p.pred_fetch, p.per_cycle);
 }
 
 // Teacher-forced decode of caller logits (ilsim_gpu_predict).
