@@ -1,0 +1,375 @@
+// K2, fused conv chain: conv0 -> conv1 -> conv2 of the C3 latency predictor
+// (cnn.cpp:90-110 for each conv layer) for 8 samples per work item, entirely
+// on chip.  Accumulators live in TMEM; between layers the epilogue warps read
+// them (tcgen05.ld), apply bias + ReLU, and restage them in shared memory as
+// the next layer's K-major SWIZZLE_128B A operand (row pairs concatenated: a
+// kernel-2/stride-2 window is two adjacent rows).  Only the final conv2
+// activations ("flat", 4 KB per sample) leave the SM.
+//
+//   TMEM (f32 columns): conv0 4 tiles x 64 [0,256) | conv1 2 x 64 [256,384) |
+//                       conv2 64 [384,448)
+//   SMEM: R1 128 KB  = conv0 input ring (4 stages of 16 KB chunk (+16 KB lo))
+//                      or the restaged A tile of conv1 / conv2
+//         R2  64 KB  = the current layer's weights (hi + lo), TMA-loaded
+//
+//   warp 0      TMA producer (weights per layer, gathered-input chunks)
+//   warp 1      TMEM allocator + tcgen05.mma issuer
+//   warps 2-5   3xTF32 hi/lo split of input chunks
+//   warps 6-9   epilogue: TMEM -> bias/ReLU -> restage (or -> global)
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "conv_chain.cuh"
+#include "tc_common.cuh"
+
+namespace simnet {
+
+namespace {
+
+constexpr int kItem = 8;            // samples per work item
+constexpr int kC = 64;              // channels of every conv layer (C3)
+constexpr uint32_t kR1 = 128 * 1024;
+constexpr uint32_t kR2 = 64 * 1024;
+constexpr int kRing = 4;
+constexpr int kThreadsCC = 320;
+
+// byte offset of element (row r, float k) in a K-major SW128 tile of 128 rows
+// whose K extent is split into 128-byte chunks of 32 floats (chunk-major).
+__device__ __forceinline__ uint32_t sw128_f32(int r, int k) {
+  const int chunk = k >> 5, kk = k & 31;
+  return chunk * (128 * 128) + r * 128 + ((((kk >> 2) ^ (r & 7)) << 4) | ((kk & 3) << 2));
+}
+// same for bf16 (64 elements per chunk), offset of the 16-byte unit holding k..k+7
+__device__ __forceinline__ uint32_t sw128_bf16_unit(int r, int k) {
+  const int chunk = k >> 6, kk = k & 63;
+  return chunk * (128 * 128) + r * 128 + (((kk >> 3) ^ (r & 7)) << 4);
+}
+
+template <int kMode>
+struct ChainShape {
+  static constexpr bool kSplit = kMode == kTF32x3;
+  static constexpr int kElems = kMode == kBF16 ? 64 : 32;      // elements per 128 B chunk
+  static constexpr int kK0Chunks = kMode == kBF16 ? 2 : 4;     // conv0 K = 100 (+pad)
+  static constexpr int kK0Steps = kMode == kBF16 ? 7 : 13;     // 32 B MMA k-steps covering K = 100
+  static constexpr int kKChunks = kMode == kBF16 ? 2 : 4;      // conv1/2 K = 128
+  static constexpr uint32_t kWBytes = kC * 128 * kKChunks;     // one weight copy (hi or lo)
+  static constexpr uint32_t kStage = 128 * 128;                // one A chunk
+  static constexpr uint32_t kALo = kKChunks * kStage;          // offset of the lo copy of a restaged A
+};
+
+// Restage 64 accumulator columns of TMEM lane-row `tl` (one conv output row)
+// into the A operand at row `ar`, K offset `k0`, with bias + ReLU.
+template <int kMode>
+__device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, int ar, int k0, const float* bias) {
+  using S = ChainShape<kMode>;
+  for (int c0 = 0; c0 < kC; c0 += 16) {
+    float v[16];
+    tmem_ld16(tl + c0, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + bias[c0 + i], 0.0f);
+    if constexpr (kMode == kBF16) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint4 pk;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * h + 2 * i], v[8 * h + 2 * i + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(a + sw128_bf16_unit(ar, k0 + c0 + 8 * h)) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + c0 + 4 * q;
+        float4 hi;
+        if constexpr (S::kSplit) {
+          uint32_t u[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) u[i] = (__float_as_uint(v[4 * q + i]) + 0x1000u) & 0xffffe000u;
+          hi = make_float4(__uint_as_float(u[0]), __uint_as_float(u[1]), __uint_as_float(u[2]), __uint_as_float(u[3]));
+          const float4 lo = make_float4(v[4 * q] - hi.x, v[4 * q + 1] - hi.y, v[4 * q + 2] - hi.z, v[4 * q + 3] - hi.w);
+          *reinterpret_cast<float4*>(a + S::kALo + sw128_f32(ar, k)) = lo;
+        } else {
+          hi = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        *reinterpret_cast<float4*>(a + sw128_f32(ar, k)) = hi;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+template <int kMode>
+__global__ void __launch_bounds__(kThreadsCC, 1)
+conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW0,
+                  const __grid_constant__ CUtensorMap tmW0lo, const __grid_constant__ CUtensorMap tmW1,
+                  const __grid_constant__ CUtensorMap tmW1lo, const __grid_constant__ CUtensorMap tmW2,
+                  const __grid_constant__ CUtensorMap tmW2lo, ChainParams p) {
+  using S = ChainShape<kMode>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* R1 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* R2 = R1 + kR1;
+  uint8_t* ringA = R1;                                   // stage s: hi at s*kStage, lo at (kRing + s)*kStage
+  __shared__ __align__(8) uint64_t full[kRing], split[kRing], empty[kRing];
+  __shared__ __align__(8) uint64_t bar_w, bar_c0, bar_a, bar_mdone, bar_out;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = (p.samples + kItem - 1) / kItem;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&split[i], 128);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&bar_w, 1);
+    mbar_init(&bar_c0, 1);
+    mbar_init(&bar_a, 128);
+    mbar_init(&bar_mdone, 1);
+    mbar_init(&bar_out, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  auto load_w = [&](const CUtensorMap* hi, const CUtensorMap* lo, int chunks) {
+    mbar_expect_tx(&bar_w, S::kWBytes * (S::kSplit ? 2u : 1u) / S::kKChunks * chunks);
+    for (int c = 0; c < chunks; ++c) {
+      tma_load_2d(R2 + c * (kC * 128), hi, &bar_w, c * S::kElems, 0);
+      if (S::kSplit) tma_load_2d(R2 + S::kWBytes + c * (kC * 128), lo, &bar_w, c * S::kElems, 0);
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(&bar_mdone, (3 * (it - 1) + 2) & 1);  // previous conv2 done: R1, R2 free
+        load_w(&tmW0, &tmW0lo, S::kK0Chunks);
+        for (int c = 0; c < 4 * S::kK0Chunks; ++c) {
+          const int tile = c / S::kK0Chunks, kc = c % S::kK0Chunks;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], S::kStage);
+          tma_load_3d(ringA + stage * S::kStage, &tmX, &full[stage], kc * S::kElems, 0, item * kItem + 2 * tile);
+          if (++stage == kRing) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
+        load_w(&tmW1, &tmW1lo, S::kKChunks);
+        mbar_wait(&bar_mdone, (3 * it + 1) & 1);  // conv1 done: W1 no longer read
+        load_w(&tmW2, &tmW2lo, S::kKChunks);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, kC);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      const uint32_t r1 = su32(R1), r2 = su32(R2);
+      auto gemm_resident_a = [&](uint32_t d, int ksteps) {  // A restaged in R1, W in R2
+        for (int s = 0; s < ksteps; ++s) {
+          const int c = s >> 2, j = s & 3;
+          const uint32_t ao = c * S::kStage + j * 32, wo = c * (kC * 128) + j * 32;
+          const uint64_t ad = smem_desc_sw128(r1 + ao), bd = smem_desc_sw128(r2 + wo);
+          if (S::kSplit) {
+            mma<kMode>(d, smem_desc_sw128(r1 + S::kALo + ao), bd, idesc, s > 0);
+            mma<kMode>(d, ad, smem_desc_sw128(r2 + S::kWBytes + wo), idesc, 1);
+            mma<kMode>(d, ad, bd, idesc, 1);
+          } else {
+            mma<kMode>(d, ad, bd, idesc, s > 0);
+          }
+        }
+      };
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        // conv0: 4 tiles of 128 rows (2 samples each) streamed through the ring
+        mbar_wait(&bar_w, (3 * it) & 1);
+        tc_fence_after();
+        for (int tile = 0; tile < 4; ++tile) {
+          const uint32_t d = tmem + tile * kC;
+          for (int kc = 0; kc < S::kK0Chunks; ++kc) {
+            mbar_wait(S::kSplit ? &split[stage] : &full[stage], phase);
+            tc_fence_after();
+            const int steps = kc == S::kK0Chunks - 1 ? S::kK0Steps - 4 * (S::kK0Chunks - 1) : 4;
+            for (int j = 0; j < steps; ++j) {
+              const uint32_t ao = su32(ringA) + stage * S::kStage + j * 32;
+              const uint32_t wo = r2 + kc * (kC * 128) + j * 32;
+              const uint32_t acc = (kc == 0 && j == 0) ? 0u : 1u;
+              if (S::kSplit) {
+                mma<kMode>(d, smem_desc_sw128(ao + kRing * S::kStage), smem_desc_sw128(wo), idesc, acc);
+                mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo + S::kWBytes), idesc, 1);
+                mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo), idesc, 1);
+              } else {
+                mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo), idesc, acc);
+              }
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == kRing) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+        mma_commit(&bar_c0);
+        // conv1: two tiles of 128 rows (4 samples each), A restaged by the epilogue
+        mbar_wait(&bar_a, (3 * it) & 1);
+        mbar_wait(&bar_w, (3 * it + 1) & 1);
+        tc_fence_after();
+        gemm_resident_a(tmem + 256, 4 * S::kKChunks);
+        mma_commit(&bar_mdone);
+        mbar_wait(&bar_a, (3 * it + 1) & 1);
+        tc_fence_after();
+        gemm_resident_a(tmem + 256 + kC, 4 * S::kKChunks);
+        mma_commit(&bar_mdone);
+        // conv2: one tile of 128 rows (8 samples)
+        mbar_wait(&bar_a, (3 * it + 2) & 1);
+        mbar_wait(&bar_w, (3 * it + 2) & 1);
+        if (it > 0) mbar_wait(&bar_out, (it - 1) & 1);  // previous conv2 accumulator drained
+        tc_fence_after();
+        gemm_resident_a(tmem + 384, 4 * S::kKChunks);
+        mma_commit(&bar_mdone);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    if (S::kSplit) {  // 3xTF32 split of every landed input chunk
+      const int t128 = threadIdx.x - 64;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        for (int c = 0; c < 4 * S::kK0Chunks; ++c) {
+          mbar_wait(&full[stage], phase);
+          uint4* a = reinterpret_cast<uint4*>(ringA + stage * S::kStage);
+          float4* alo = reinterpret_cast<float4*>(ringA + (kRing + stage) * S::kStage);
+#pragma unroll 4
+          for (int i = t128; i < static_cast<int>(S::kStage / 16); i += 128) {
+            const uint4 u = a[i];
+            uint4 h;
+            h.x = (u.x + 0x1000u) & 0xffffe000u;
+            h.y = (u.y + 0x1000u) & 0xffffe000u;
+            h.z = (u.z + 0x1000u) & 0xffffe000u;
+            h.w = (u.w + 0x1000u) & 0xffffe000u;
+            alo[i] = make_float4(__uint_as_float(u.x) - __uint_as_float(h.x), __uint_as_float(u.y) - __uint_as_float(h.y),
+                                 __uint_as_float(u.z) - __uint_as_float(h.z), __uint_as_float(u.w) - __uint_as_float(h.w));
+            a[i] = h;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&split[stage]);
+          if (++stage == kRing) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // epilogue warps 6..9: thread owns TMEM lane m = 32*(warp%4) + lane
+    const int quad = warp & 3;
+    const int m = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    int it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      // A1 passes: conv0 tiles (2*pass, 2*pass+1) -> conv1 A rows
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 0)
+          mbar_wait(&bar_c0, it & 1);
+        else
+          mbar_wait(&bar_mdone, (3 * it) & 1);  // conv1 tile 0 has consumed R1
+        tc_fence_after();
+        for (int t2 = 0; t2 < 2; ++t2) {
+          // conv0 row m of tile (2*pass + t2) = (sample, pos) -> A1 row t2*64 + m/2, K half m%2
+          restage_row<kMode>(R1, tmem + lane_off + (2 * pass + t2) * kC, t2 * 64 + (m >> 1), (m & 1) * kC, p.b0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&bar_a);
+      }
+      // A2: conv1 tiles 0,1 -> conv2 A rows
+      mbar_wait(&bar_mdone, (3 * it + 1) & 1);
+      tc_fence_after();
+      for (int t2 = 0; t2 < 2; ++t2)
+        restage_row<kMode>(R1, tmem + lane_off + 256 + t2 * kC, t2 * 64 + (m >> 1), (m & 1) * kC, p.b1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&bar_a);
+      // conv2 -> flat[sample][pos*64 + c]: row m of the tile is flat row item*128 + m
+      mbar_wait(&bar_mdone, (3 * it + 2) & 1);
+      tc_fence_after();
+      const int sample = item * kItem + (m >> 4);
+      for (int c0 = 0; c0 < kC; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + lane_off + 384 + c0, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + p.b2[c0 + i], 0.0f);
+        if (sample < p.samples) {
+          const uint64_t off = static_cast<uint64_t>(item) * (kItem * 16 * kC) + m * kC + c0;
+          if (kMode == kBF16) {
+            uint4 pk[2];
+            uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+            o[0] = pk[0];
+            o[1] = pk[1];
+          } else {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_out);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+size_t chain_smem_bytes() { return kR1 + kR2 + 1024; }
+
+void launch_conv_chain(int mode, const CUtensorMap& x, const CUtensorMap* w, const ChainParams& p, int num_sms,
+                       cudaStream_t s) {
+  const int items = (p.samples + kItem - 1) / kItem;
+  const dim3 grid(static_cast<unsigned>(items < num_sms ? items : num_sms));
+  const size_t sm = chain_smem_bytes();
+  if (mode == kBF16)
+    conv_chain_kernel<kBF16><<<grid, kThreadsCC, sm, s>>>(x, w[0], w[1], w[2], w[3], w[4], w[5], p);
+  else if (mode == kTF32)
+    conv_chain_kernel<kTF32><<<grid, kThreadsCC, sm, s>>>(x, w[0], w[1], w[2], w[3], w[4], w[5], p);
+  else
+    conv_chain_kernel<kTF32x3><<<grid, kThreadsCC, sm, s>>>(x, w[0], w[1], w[2], w[3], w[4], w[5], p);
+}
+
+void conv_chain_set_attributes() {
+  const int sm = static_cast<int>(chain_smem_bytes());
+  CUDA_OK(cudaFuncSetAttribute(conv_chain_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(conv_chain_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(conv_chain_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+}
+
+}  // namespace simnet

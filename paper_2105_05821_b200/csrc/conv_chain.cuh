@@ -1,0 +1,24 @@
+// Fused conv0 -> conv1 -> conv2 kernel (tensor cores) for the C3 preset.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "host_util.cuh"
+
+namespace simnet {
+
+struct ChainParams {
+  int samples;
+  const float* b0;
+  const float* b1;
+  const float* b2;
+  void* out;  // flat [samples][1024] (f32, or bf16 for the bf16 path)
+};
+
+// w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
+void launch_conv_chain(int mode, const CUtensorMap& x, const CUtensorMap* w, const ChainParams& p, int num_sms,
+                       cudaStream_t s);
+void conv_chain_set_attributes();
+size_t chain_smem_bytes();
+
+}  // namespace simnet

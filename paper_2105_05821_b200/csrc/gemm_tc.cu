@@ -18,124 +18,21 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <deque>
 #include <vector>
 
+#include "conv_chain.cuh"
 #include "decode.cuh"
+#include "tc_common.cuh"
 #include "launch.cuh"
 #include "model.cuh"
 #include "sim_kernels.cuh"
 
 namespace simnet {
 
-enum TcMode : int { kBF16 = 0, kTF32 = 1, kTF32x3 = 2 };
-
-constexpr int kMaxChunks = 4;    // K chunks (128 B each) resident per CTA
-constexpr int kBM = 128;
-constexpr int kThreads = 192;    // 6 warps
-
-// --------------------------------------------------------------------------
-// PTX helpers
-// --------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  const uint32_t a = su32(b);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
-          "r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row x 128 B atoms,
-// SBO = 1024 B between 8-row groups, version 1 (sm_100), layout type 2.
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>(1) << 16;                  // LBO (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;          // SBO
-  d |= static_cast<uint64_t>(1) << 46;                  // descriptor version
-  d |= static_cast<uint64_t>(2) << 61;                  // SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor: D f32, A/B K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t instr_desc(int fmt, int n) {
-  return (1u << 4) | (static_cast<uint32_t>(fmt) << 7) | (static_cast<uint32_t>(fmt) << 10) |
-         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
-}
-
-template <int kMode>
-__device__ __forceinline__ void mma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  if constexpr (kMode == kBF16) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-  }
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
-// --------------------------------------------------------------------------
 // --------------------------------------------------------------------------
 // Persistent, warp-specialised layer GEMM
 // --------------------------------------------------------------------------
@@ -382,8 +279,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // simulating, the hybrid decode and clock advance of K3 for each sample.
 constexpr int kTailSamples = 4;
 constexpr int kMaxSplit = 8;  // split-K planes of FC1 (flat 1024 f32 = 32 chunks / 4)
-constexpr int kTailThreads = 128;
-constexpr int kMaxHidden = 1024;
+constexpr int kTailThreads = 256;
 constexpr int kMaxOut = 64;
 
 struct TailParams {
@@ -400,41 +296,73 @@ struct TailParams {
   DecodeParams dec;  // dec.state == nullptr: outputs only
 };
 
+// dynamic smem: W2 [od][hidden + 4] | h [kTailSamples][hidden] | y [kTailSamples][kMaxOut]
 __global__ void __launch_bounds__(kTailThreads) fc_tail_kernel(TailParams p) {
-  __shared__ float hs[kTailSamples][kMaxHidden];
-  __shared__ float ys[kTailSamples][kMaxOut];
+  extern __shared__ __align__(16) float tail_sm[];
+  const int hid = p.hidden, ws = hid + 4;  // +4: conflict-free float4 row reads
+  float* w2s = tail_sm;
+  float* hs = w2s + p.od * ws;
+  float* ys = hs + kTailSamples * hid;
   asm volatile("griddepcontrol.launch_dependents;");
+  // W2 (a constant) is staged before the dependency wait: all float4 loads in flight
+  {
+    const int per_row = hid / 4, total = p.od * per_row;
+    const float4* src = reinterpret_cast<const float4*>(p.w2t);
+    for (int base = threadIdx.x; base < total; base += kTailThreads * 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * kTailThreads;
+        if (i < total) v[u] = __ldg(src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * kTailThreads;
+        if (i < total) {
+          const int o = i / per_row, k4 = i - o * per_row;
+          *reinterpret_cast<float4*>(w2s + o * ws + 4 * k4) = v[u];
+        }
+      }
+    }
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int s0 = blockIdx.x * kTailSamples;
   const int ns = min(kTailSamples, p.samples - s0);
-  const int hid = p.hidden;
-  for (int i = threadIdx.x; i < ns * hid; i += kTailThreads) {
-    const int ls = i / hid, j = i - ls * hid;
-    const uint64_t off = static_cast<uint64_t>(s0 + ls) * hid + j;
-    float pv[kMaxSplit];
+  // hidden unit j of every sample in the block: kTailSamples x kMaxSplit loads in flight
+  for (int j = threadIdx.x; j < hid; j += kTailThreads) {
+    float pv[kTailSamples][kMaxSplit];
 #pragma unroll
-    for (int q = 0; q < kMaxSplit; ++q) pv[q] = q < p.nsplit ? __ldg(p.part + q * p.split_stride + off) : 0.0f;
-    float acc = 0.0f;
+    for (int ls = 0; ls < kTailSamples; ++ls)
 #pragma unroll
-    for (int q = 0; q < kMaxSplit; ++q) acc += pv[q];  // fixed order (zeros past nsplit are exact)
-    hs[ls][j] = fmaxf(acc + __ldg(p.b1 + j), 0.0f);
+      for (int q = 0; q < kMaxSplit; ++q)
+        pv[ls][q] = (ls < ns && q < p.nsplit)
+                        ? __ldg(p.part + q * p.split_stride + static_cast<uint64_t>(s0 + ls) * hid + j)
+                        : 0.0f;
+    const float bj = __ldg(p.b1 + j);
+#pragma unroll
+    for (int ls = 0; ls < kTailSamples; ++ls) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < kMaxSplit; ++q) acc += pv[ls][q];  // fixed order (zeros past nsplit are exact)
+      hs[ls * hid + j] = fmaxf(acc + bj, 0.0f);
+    }
   }
   __syncthreads();
   for (int task = threadIdx.x; task < ns * p.od; task += kTailThreads) {
     const int ls = task / p.od, o = task - ls * p.od;
-    const float4* w = reinterpret_cast<const float4*>(p.w2t + static_cast<uint64_t>(o) * hid);
-    const float* h = hs[ls];
+    const float4* w = reinterpret_cast<const float4*>(w2s + o * ws);
+    const float4* h = reinterpret_cast<const float4*>(hs + ls * hid);
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-#pragma unroll 4
+#pragma unroll 8
     for (int k4 = 0; k4 < hid / 4; ++k4) {
-      const float4 wv = __ldg(w + k4);
-      a0 = fmaf(wv.x, h[4 * k4 + 0], a0);
-      a1 = fmaf(wv.y, h[4 * k4 + 1], a1);
-      a2 = fmaf(wv.z, h[4 * k4 + 2], a2);
-      a3 = fmaf(wv.w, h[4 * k4 + 3], a3);
+      const float4 wv = w[k4], hv = h[k4];
+      a0 = fmaf(wv.x, hv.x, a0);
+      a1 = fmaf(wv.y, hv.y, a1);
+      a2 = fmaf(wv.z, hv.z, a2);
+      a3 = fmaf(wv.w, hv.w, a3);
     }
     const float v = ((a0 + a1) + (a2 + a3)) + __ldg(p.b2 + o);
-    ys[ls][o] = v;
+    ys[ls * kMaxOut + o] = v;
     p.y[static_cast<uint64_t>(s0 + ls) * p.od + o] = v;
   }
   if (p.dec.state == nullptr) return;
@@ -444,7 +372,7 @@ __global__ void __launch_bounds__(kTailThreads) fc_tail_kernel(TailParams p) {
     SubState* sp = d.state + d.first + s0 + threadIdx.x;
     if (sp->status == kOk && sp->pos < sp->len) {
       uint32_t t[3];
-      decode_triple(ys[threadIdx.x], *d.nc, d.class_fetch, d.class_exec, d.class_store,
+      decode_triple(ys + threadIdx.x * kMaxOut, *d.nc, d.class_fetch, d.class_exec, d.class_store,
                     (d.iflags[sp->begin + sp->pos] & kFlagStore) != 0, t);
       apply_decoded(sp, t, d.pred_fetch, d.per_cycle);
     }
@@ -520,6 +448,7 @@ int mode_of(int precision) {
 
 struct TcModel {
   int mode = kTF32x3;
+  bool chain = false;  // C3 shape: fused conv chain kernel
   std::deque<TcWeights> conv;
   TcWeights fc1;
   DevBuf w2t;   // fc2 weights transposed to [out_dim][hidden] (k contiguous)
@@ -572,14 +501,18 @@ size_t smem_bytes(int mode, int n, int chunks) {
 }
 
 int g_num_sms = 0;
-
-void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
-                 const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
+int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
     CUDA_OK(cudaGetDevice(&dev));
     CUDA_OK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  return g_num_sms;
+}
+
+void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
+                 const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
+  num_sms();
   const int groups = ny * nz;
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
@@ -610,8 +543,12 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(fc_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  conv_chain_set_attributes();
   auto* t = new TcModel();
   t->mode = mode;
+  t->chain = c.n_conv == 3 && c.conv[0] == 64 && c.conv[1] == 64 && c.conv[2] == 64 && c.input_channels == 50 &&
+             c.sequence_length == 128 && !c.residual && std::getenv("SIMNET_NO_CHAIN") == nullptr;
   try {
     cin = c.input_channels;
     for (int l = 0; l < c.n_conv; ++l) t->conv.emplace_back();
@@ -664,7 +601,22 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
   int len = c.sequence_length;
   int cin = c.input_channels;
   const void* in = x;
-  for (int l = 0; l < c.n_conv; ++l) {
+  if (t.chain) {  // conv0 -> conv1 -> conv2 fused, activations stay on chip
+    const uint64_t row_elems = bf ? 104 : 100;
+    const uint64_t rows = x_stride / row_elems;
+    const uint64_t dims[3] = {100, rows, samples};
+    const uint64_t strides[2] = {row_elems * esz, static_cast<uint64_t>(x_stride) * esz};
+    const uint32_t box[3] = {static_cast<uint32_t>(chunk_elems), 64, 2};
+    const CUtensorMap xmap = make_map(x, bf, 3, dims, strides, box);
+    const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
+                              t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
+    ChainParams cp{static_cast<int>(samples), P + m.L.b[0], P + m.L.b[1], P + m.L.b[2], fb.act[2]};
+    launch_conv_chain(mode, xmap, w, cp, num_sms(), s);
+    ++launches;
+    in = fb.act[2];
+    len = 0;
+  }
+  for (int l = 0; l < c.n_conv && !t.chain; ++l) {
     const int olen = len / 2, cout = c.conv[l], k = 2 * cin;
     const uint64_t m_rows = samples * olen;
     CUtensorMap amap;
@@ -734,8 +686,10 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
     const int od = m.L.out_dim;
-    if (c.fc_hidden > kMaxHidden || od > kMaxOut || c.fc_hidden % 4 != 0)
-      throw ApiError("tensor-core path: FC tail supports fc_hidden <= 1024 (multiple of 4), <= 64 outputs");
+    if (od > kMaxOut || c.fc_hidden % 4 != 0)
+      throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
+    const size_t tail_smem =
+        (static_cast<size_t>(od) * (c.fc_hidden + 4) + kTailSamples * c.fc_hidden + kTailSamples * kMaxOut) * 4;
     TailParams tp{};
     tp.part = part;
     tp.nsplit = nsplit;
@@ -749,7 +703,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     tp.samples = static_cast<int>(samples);
     if (fuse) tp.dec = *fuse;
     launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
-               dim3(kTailThreads), 0, s, tp);
+               dim3(kTailThreads), tail_smem, s, tp);
     ++launches;
   }
   return launches;
