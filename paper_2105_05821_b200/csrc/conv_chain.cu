@@ -114,7 +114,12 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   uint8_t* R2 = R1 + kR1;
   uint8_t* ringA = R1;                                   // stage s: hi at s*kStage, lo at (kRing + s)*kStage
   __shared__ __align__(8) uint64_t full[kRing], split[kRing], empty[kRing];
-  __shared__ __align__(8) uint64_t bar_w, bar_c0, bar_a, bar_mdone, bar_out;
+  // One barrier per event, each completing exactly once per work item, so a
+  // parity wait on (item & 1) is unambiguous (no waiter can fall two phases behind).
+  __shared__ __align__(8) uint64_t bar_w[3];              // weights of layer l landed (TMA tx)
+  __shared__ __align__(8) uint64_t bar_c0, bar_m1a, bar_m1b, bar_m2;  // MMAs done (tcgen05.commit)
+  __shared__ __align__(8) uint64_t bar_a[3];              // A operand restaged for conv1 t0 / t1 / conv2
+  __shared__ __align__(8) uint64_t bar_out;               // conv2 accumulator drained
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -126,10 +131,14 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       mbar_init(&split[i], 128);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(&bar_w, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&bar_w[i], 1);
+      mbar_init(&bar_a[i], 128);
+    }
     mbar_init(&bar_c0, 1);
-    mbar_init(&bar_a, 128);
-    mbar_init(&bar_mdone, 1);
+    mbar_init(&bar_m1a, 1);
+    mbar_init(&bar_m1b, 1);
+    mbar_init(&bar_m2, 1);
     mbar_init(&bar_out, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -145,11 +154,12 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
-  auto load_w = [&](const CUtensorMap* hi, const CUtensorMap* lo, int chunks) {
-    mbar_expect_tx(&bar_w, S::kWBytes * (S::kSplit ? 2u : 1u) / S::kKChunks * chunks);
+  auto load_w = [&](int layer, const CUtensorMap* hi, const CUtensorMap* lo, int chunks) {
+    uint64_t* b = &bar_w[layer];
+    mbar_expect_tx(b, S::kWBytes * (S::kSplit ? 2u : 1u) / S::kKChunks * chunks);
     for (int c = 0; c < chunks; ++c) {
-      tma_load_2d(R2 + c * (kC * 128), hi, &bar_w, c * S::kElems, 0);
-      if (S::kSplit) tma_load_2d(R2 + S::kWBytes + c * (kC * 128), lo, &bar_w, c * S::kElems, 0);
+      tma_load_2d(R2 + c * (kC * 128), hi, b, c * S::kElems, 0);
+      if (S::kSplit) tma_load_2d(R2 + S::kWBytes + c * (kC * 128), lo, b, c * S::kElems, 0);
     }
   };
 
@@ -159,8 +169,8 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       uint32_t phase = 0;
       int it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        if (it > 0) mbar_wait(&bar_mdone, (3 * (it - 1) + 2) & 1);  // previous conv2 done: R1, R2 free
-        load_w(&tmW0, &tmW0lo, S::kK0Chunks);
+        if (it > 0) mbar_wait(&bar_m2, (it - 1) & 1);  // previous conv2 done: R1, R2 free
+        load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
         for (int c = 0; c < 4 * S::kK0Chunks; ++c) {
           const int tile = c / S::kK0Chunks, kc = c % S::kK0Chunks;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -172,9 +182,9 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           }
         }
         mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
-        load_w(&tmW1, &tmW1lo, S::kKChunks);
-        mbar_wait(&bar_mdone, (3 * it + 1) & 1);  // conv1 done: W1 no longer read
-        load_w(&tmW2, &tmW2lo, S::kKChunks);
+        load_w(1, &tmW1, &tmW1lo, S::kKChunks);
+        mbar_wait(&bar_m1b, it & 1);  // conv1 done: W1 no longer read
+        load_w(2, &tmW2, &tmW2lo, S::kKChunks);
       }
     }
   } else if (warp == 1) {
@@ -200,7 +210,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       };
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         // conv0: 4 tiles of 128 rows (2 samples each) streamed through the ring
-        mbar_wait(&bar_w, (3 * it) & 1);
+        mbar_wait(&bar_w[0], it & 1);
         tc_fence_after();
         for (int tile = 0; tile < 4; ++tile) {
           const uint32_t d = tmem + tile * kC;
@@ -229,22 +239,22 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         }
         mma_commit(&bar_c0);
         // conv1: two tiles of 128 rows (4 samples each), A restaged by the epilogue
-        mbar_wait(&bar_a, (3 * it) & 1);
-        mbar_wait(&bar_w, (3 * it + 1) & 1);
+        mbar_wait(&bar_a[0], it & 1);
+        mbar_wait(&bar_w[1], it & 1);
         tc_fence_after();
         gemm_resident_a(tmem + 256, 4 * S::kKChunks);
-        mma_commit(&bar_mdone);
-        mbar_wait(&bar_a, (3 * it + 1) & 1);
+        mma_commit(&bar_m1a);
+        mbar_wait(&bar_a[1], it & 1);
         tc_fence_after();
         gemm_resident_a(tmem + 256 + kC, 4 * S::kKChunks);
-        mma_commit(&bar_mdone);
+        mma_commit(&bar_m1b);
         // conv2: one tile of 128 rows (8 samples)
-        mbar_wait(&bar_a, (3 * it + 2) & 1);
-        mbar_wait(&bar_w, (3 * it + 2) & 1);
+        mbar_wait(&bar_a[2], it & 1);
+        mbar_wait(&bar_w[2], it & 1);
         if (it > 0) mbar_wait(&bar_out, (it - 1) & 1);  // previous conv2 accumulator drained
         tc_fence_after();
         gemm_resident_a(tmem + 384, 4 * S::kKChunks);
-        mma_commit(&bar_mdone);
+        mma_commit(&bar_m2);
       }
     }
     __syncwarp();
@@ -291,7 +301,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         if (pass == 0)
           mbar_wait(&bar_c0, it & 1);
         else
-          mbar_wait(&bar_mdone, (3 * it) & 1);  // conv1 tile 0 has consumed R1
+          mbar_wait(&bar_m1a, it & 1);  // conv1 tile 0 has consumed R1
         tc_fence_after();
         for (int t2 = 0; t2 < 2; ++t2) {
           // conv0 row m of tile (2*pass + t2) = (sample, pos) -> A1 row t2*64 + m/2, K half m%2
@@ -299,18 +309,18 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(&bar_a);
+        mbar_arrive(&bar_a[pass]);
       }
       // A2: conv1 tiles 0,1 -> conv2 A rows
-      mbar_wait(&bar_mdone, (3 * it + 1) & 1);
+      mbar_wait(&bar_m1b, it & 1);
       tc_fence_after();
       for (int t2 = 0; t2 < 2; ++t2)
         restage_row<kMode>(R1, tmem + lane_off + 256 + t2 * kC, t2 * 64 + (m >> 1), (m & 1) * kC, p.b1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(&bar_a);
+      mbar_arrive(&bar_a[2]);
       // conv2 -> flat[sample][pos*64 + c]: row m of the tile is flat row item*128 + m
-      mbar_wait(&bar_mdone, (3 * it + 2) & 1);
+      mbar_wait(&bar_m2, it & 1);
       tc_fence_after();
       const int sample = item * kItem + (m >> 4);
       for (int c0 = 0; c0 < kC; c0 += 16) {
