@@ -110,7 +110,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                   const __grid_constant__ CUtensorMap tmW2lo, ChainParams p) {
   using S = ChainShape<kMode>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* R1 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* R1 = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
   uint8_t* R2 = R1 + kR1;
   uint8_t* ringA = R1;                                   // stage s: hi at s*kStage, lo at (kRing + s)*kStage
   __shared__ __align__(8) uint64_t full[kRing], split[kRing], empty[kRing];
@@ -121,9 +121,14 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   __shared__ __align__(8) uint64_t bar_a[3];              // A operand restaged for conv1 t0 / t1 / conv2
   __shared__ __align__(8) uint64_t bar_out;               // conv2 accumulator drained
   __shared__ uint32_t tmem_slot;
+  __shared__ float sbias[3][kC];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = (p.samples + kItem - 1) / kItem;
+  if (threadIdx.x < 3 * kC) {
+    const int l = threadIdx.x / kC, c = threadIdx.x % kC;
+    sbias[l][c] = (l == 0 ? p.b0 : (l == 1 ? p.b1 : p.b2))[c];
+  }
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
@@ -305,7 +310,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         tc_fence_after();
         for (int t2 = 0; t2 < 2; ++t2) {
           // conv0 row m of tile (2*pass + t2) = (sample, pos) -> A1 row t2*64 + m/2, K half m%2
-          restage_row<kMode>(R1, tmem + lane_off + (2 * pass + t2) * kC, t2 * 64 + (m >> 1), (m & 1) * kC, p.b0);
+          restage_row<kMode>(R1, tmem + lane_off + (2 * pass + t2) * kC, t2 * 64 + (m >> 1), (m & 1) * kC, sbias[0]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
@@ -315,7 +320,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       mbar_wait(&bar_m1b, it & 1);
       tc_fence_after();
       for (int t2 = 0; t2 < 2; ++t2)
-        restage_row<kMode>(R1, tmem + lane_off + 256 + t2 * kC, t2 * 64 + (m >> 1), (m & 1) * kC, p.b1);
+        restage_row<kMode>(R1, tmem + lane_off + 256 + t2 * kC, t2 * 64 + (m >> 1), (m & 1) * kC, sbias[1]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&bar_a[2]);
@@ -327,7 +332,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         float v[16];
         tmem_ld16(tmem + lane_off + 384 + c0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + p.b2[c0 + i], 0.0f);
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
         if (sample < p.samples) {
           const uint64_t off = static_cast<uint64_t>(item) * (kItem * 16 * kC) + m * kC + c0;
           if (kMode == kBF16) {

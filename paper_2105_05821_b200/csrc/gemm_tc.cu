@@ -70,7 +70,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmBlo, TcGemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr bool kSplit = kMode == kTF32x3;
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
   const uint32_t bBytes = static_cast<uint32_t>(p.n) * 128;
   uint8_t* sW = base;                                      // [chunks][n x 128 B]
   uint8_t* sWlo = sW + p.chunks * bBytes;                  // tf32x3 only
