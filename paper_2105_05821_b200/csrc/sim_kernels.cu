@@ -95,11 +95,9 @@ __device__ __forceinline__ uint64_t head_gap(uint64_t cur, uint64_t push, uint32
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kCtxWarps * 32)
 ctx_kernel(CtxParams p) {
+  // per column: instruction index and the 9 dynamic slots (41..49), normalised
   __shared__ uint32_t s_inst[kCtxWarps][kMaxCols];
-  __shared__ float s_res[kCtxWarps][kMaxCols];
-  __shared__ float s_exe[kCtxWarps][kMaxCols];
-  __shared__ float s_sto[kCtxWarps][kMaxCols];
-  __shared__ uint8_t s_flg[kCtxWarps][kMaxCols];
+  __shared__ float s_dyn[kCtxWarps][kMaxCols][kSlots - kStatic];
 
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -200,7 +198,9 @@ ctx_kernel(CtxParams p) {
   const uint64_t taddr = p.addr[tgt];
   const bool tmem = (p.iflags[tgt] & kFlagMem) != 0;
   // Column descriptors, 4 columns per lane in flight: ring entry, then the
-  // context instruction's pc/address/flags (newest first: proc, then write queue).
+  // context instruction's pc/address/flags (newest first: proc, then write
+  // queue).  Loads are unconditional from clamped, always-valid addresses so
+  // they issue back to back; predicates only select the results.
   for (uint32_t c0 = 0; c0 <= ncols; c0 += 128) {
     RingEntry e[4];
     bool ok[4];
@@ -208,37 +208,29 @@ ctx_kernel(CtxParams p) {
     for (int u = 0; u < 4; ++u) {
       const uint32_t c = c0 + u * 32 + lane;
       ok[u] = c >= 1 && c <= ncols;
-      if (ok[u]) {
-        const uint32_t j = c - 1;
-        e[u] = j < nproc ? r.proc[(st.pt - 1 - j) & r.pmask] : r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
-      }
+      const uint32_t j = ok[u] ? c - 1 : 0;
+      const RingEntry* src = j < nproc ? &r.proc[(st.pt - 1 - j) & r.pmask]
+                                       : &r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
+      e[u] = (nproc + nwq) > 0 ? *src : RingEntry{};
     }
     uint64_t cpc[4], ca[4];
     uint8_t cf[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (ok[u]) {
-        const uint64_t inst = st.begin + e[u].idx;
-        cpc[u] = p.pc[inst];
-        ca[u] = p.addr[inst];
-        cf[u] = p.iflags[inst];
-      }
+      const uint64_t inst = ok[u] ? st.begin + e[u].idx : tgt;
+      cpc[u] = p.pc[inst];
+      ca[u] = p.addr[inst];
+      cf[u] = p.iflags[inst];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t c = c0 + u * 32 + lane;
       if (c == 0) {
         s_inst[warp][0] = static_cast<uint32_t>(tgt);
-        s_res[warp][0] = nc.zero[kSlotResidence];
-        s_exe[warp][0] = nc.zero[kSlotExecution];
-        s_sto[warp][0] = nc.zero[kSlotStore];
-        s_flg[warp][0] = 0;
+#pragma unroll
+        for (int k = kStatic; k < kSlots; ++k) s_dyn[warp][0][k - kStatic] = nc.zero[k];
       } else if (ok[u]) {
         const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e[u].push));
-        s_inst[warp][c] = static_cast<uint32_t>(st.begin + e[u].idx);
-        s_res[warp][c] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
-        s_exe[warp][c] = e[u].nexec;
-        s_sto[warp][c] = e[u].nstore;
         // memory_dependency_flags (dataset.cpp:47-60)
         uint32_t f = (tpc / p.line) == (cpc[u] / p.line) ? 1u : 0u;
         if (tmem && (cf[u] & kFlagMem)) {
@@ -247,60 +239,62 @@ ctx_kernel(CtxParams p) {
           f |= (taddr / p.page) == (ca[u] / p.page) ? 8u : 0u;
         }
         f |= (tpc / p.page) == (cpc[u] / p.page) ? 16u : 0u;
-        s_flg[warp][c] = static_cast<uint8_t>(f);
+        float* d = s_dyn[warp][c];
+        s_inst[warp][c] = static_cast<uint32_t>(st.begin + e[u].idx);
+        d[0] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
+        d[1] = e[u].nexec;
+        d[2] = e[u].nstore;
+#pragma unroll
+        for (int b = 0; b < 5; ++b) d[3 + b] = ((f >> b) & 1u) ? nc.one[kSlotFlag0 + b] : nc.zero[kSlotFlag0 + b];
+        d[8] = nc.zero[kSlotReserved];
       }
     }
   }
   __syncwarp();
 
   // Row write: live columns, then zeros only where the previous round of this
-  // sub-trace left non-zero columns (the rest of the row is already 0).
+  // sub-trace left non-zero columns (the rest of the row is already 0).  The
+  // 16 static-slot loads of an iteration are unconditional (clamped index).
   const uint32_t live = (ncols + 1) * kSlots;
   const uint32_t prev = p.x_full ? p.x_floats : st.xcols * kSlots;
   const uint32_t n4 = ((live > prev ? live : prev) + 3) / 4;
   float4* out4 = reinterpret_cast<float4*>(static_cast<float*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride));
   __nv_bfloat16* outb = static_cast<__nv_bfloat16*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride);
   for (uint32_t q0 = 0; q0 < n4; q0 += 128) {
-    float v[4][4];
+    float stv[4][4], dyv[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const uint32_t jf = 4 * (q0 + u * 32 + lane) + t;
-        const uint32_t col = jf / kSlots;
-        const uint32_t slot = jf - col * kSlots;
-        float val = 0.0f;
-        if (jf < live) {
-          if (slot < kStatic) {
-            val = __ldg(p.stat + static_cast<uint64_t>(s_inst[warp][col]) * kStatStride + slot);
-          } else if (slot == kSlotResidence) {
-            val = s_res[warp][col];
-          } else if (slot == kSlotExecution) {
-            val = s_exe[warp][col];
-          } else if (slot == kSlotStore) {
-            val = s_sto[warp][col];
-          } else if (slot < kSlotReserved) {
-            val = (s_flg[warp][col] >> (slot - kSlotFlag0)) & 1u ? nc.one[slot] : nc.zero[slot];
-          } else {
-            val = nc.zero[kSlotReserved];
-          }
-        }
-        v[u][t] = val;
+        const uint32_t col = jf / kSlots, slot = jf - col * kSlots;
+        const uint32_t colc = jf < live ? col : 0u;
+        const bool st_slot = slot < kStatic;
+        stv[u][t] = __ldg(p.stat + static_cast<uint64_t>(s_inst[warp][colc]) * kStatStride + (st_slot ? slot : 0u));
+        dyv[u][t] = s_dyn[warp][colc][st_slot ? 0u : slot - kStatic];
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t q = q0 + u * 32 + lane;
+      float v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t jf = 4 * q + t;
+        const uint32_t slot = jf - (jf / kSlots) * kSlots;
+        const float val = slot < kStatic ? stv[u][t] : dyv[u][t];
+        v[t] = jf < live ? val : 0.0f;
+      }
       if (q >= n4) continue;
       if (p.x_bf16) {
         const uint32_t row = (4 * q) / 100, within = 4 * q - 100 * row;
-        __nv_bfloat162 a = __floats2bfloat162_rn(v[u][0], v[u][1]), b = __floats2bfloat162_rn(v[u][2], v[u][3]);
+        __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
         uint2 w;
         w.x = *reinterpret_cast<uint32_t*>(&a);
         w.y = *reinterpret_cast<uint32_t*>(&b);
         *reinterpret_cast<uint2*>(outb + row * 104 + within) = w;
       } else {
-        out4[q] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+        out4[q] = make_float4(v[0], v[1], v[2], v[3]);
       }
     }
   }

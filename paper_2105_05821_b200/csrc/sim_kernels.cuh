@@ -7,7 +7,7 @@
 namespace simnet {
 
 constexpr int kCtxWarps = 8;    // sub-traces per K1 block (one warp each)
-constexpr int kMaxCols = 256;   // max_context + 1 supported by the gather
+constexpr int kMaxCols = 128;   // max_context + 1 supported by the gather (C3: 111)
 
 struct CtxParams {
   SubState* state;
