@@ -20,16 +20,21 @@ enum : uint32_t { kOk = 0, kErrStall = 1, kErrDrain = 2, kErrWriteRing = 3 };
 // One in-flight instruction (SimCore::InFlight, simcore.hpp:61-68) in the
 // push-tick formulation: residence == cur - push (simcore.hpp:55-57), so no
 // per-entry counter is stored and "advance" is O(1).  Normalised
-// execution/store slots are computed once at push.  32 B: one sector.
+// execution/store slots are computed once at push, and the instruction's pc /
+// data address / flags ride along so the gather needs no extra load level
+// for the dependency flags.  48 B.
 struct __align__(16) RingEntry {
   uint64_t push;      // cur_tick when pushed
+  uint64_t pc;        // StaticInstruction::pc
+  uint64_t addr;      // StaticInstruction::data_addr
   uint32_t idx;       // position within the sub-trace (local_index)
   uint32_t exec;      // predicted execution latency
   uint32_t store;     // predicted store latency
   float nexec;        // normalised slot 42
   float nstore;       // normalised slot 43
-  uint32_t is_store;
+  uint32_t flags;     // kFlagMem | kFlagStore
 };
+static_assert(sizeof(RingEntry) == 48, "RingEntry layout");
 
 // Per-sub-trace machine state (SimCore members, simcore.hpp:79-90, plus the
 // round-loop bookkeeping of parallel.cpp:63-81).  128 B.
@@ -45,8 +50,11 @@ struct __align__(16) SubState {
   uint32_t count_drain;
   uint32_t xcols;                    // gathered-input columns written last round (zeroing bound)
   uint64_t err_tick;
+  uint64_t t_pc, t_addr;             // pc / data address of instruction `pos` (set by the gather)
+  uint32_t t_flags;                  // its flags, copied into the ring entry at push
+  uint32_t pad_[3];
 };
-static_assert(sizeof(SubState) == 128, "SubState layout");
+static_assert(sizeof(SubState) == 160, "SubState layout");
 
 // Normalisation constants derived from NormStats (dataset.hpp:54-65).
 struct NormConsts {

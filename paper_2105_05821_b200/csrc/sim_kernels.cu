@@ -52,7 +52,7 @@ __device__ uint32_t warp_retire(uint64_t cur, uint64_t budget, const Rings& r, u
     }
     const uint32_t run = leading_run(__ballot_sync(kFull, ready));
     const uint32_t take = static_cast<uint32_t>(min(static_cast<uint64_t>(run), budget));
-    const bool mv = lane < take && e.is_store;
+    const bool mv = lane < take && (e.flags & kFlagStore);
     const uint32_t sm = __ballot_sync(kFull, mv);
     const uint32_t nmv = __popc(sm);
     if (wt + nmv - wh > r.wcap) {
@@ -148,7 +148,9 @@ ctx_kernel(CtxParams p) {
         e.store = st.pend_s;
         e.nexec = norm_slot(static_cast<int32_t>(st.pend_e), nc.mean[kSlotExecution], nc.sd[kSlotExecution]);
         e.nstore = norm_slot(static_cast<int32_t>(st.pend_s), nc.mean[kSlotStore], nc.sd[kSlotStore]);
-        e.is_store = (p.iflags[st.begin + st.pos] & kFlagStore) ? 1u : 0u;
+        e.pc = st.t_pc;  // stashed by this sub-trace's previous gather (0 when none ran)
+        e.addr = st.t_addr;
+        e.flags = p.gather ? st.t_flags : p.iflags[st.begin + st.pos];
         r.proc[st.pt & r.pmask] = e;
       }
       st.pt += 1;
@@ -214,13 +216,12 @@ ctx_kernel(CtxParams p) {
       e[u] = (nproc + nwq) > 0 ? *src : RingEntry{};
     }
     uint64_t cpc[4], ca[4];
-    uint8_t cf[4];
+    uint32_t cf[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint64_t inst = ok[u] ? st.begin + e[u].idx : tgt;
-      cpc[u] = p.pc[inst];
-      ca[u] = p.addr[inst];
-      cf[u] = p.iflags[inst];
+      cpc[u] = e[u].pc;
+      ca[u] = e[u].addr;
+      cf[u] = e[u].flags;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -298,7 +299,12 @@ ctx_kernel(CtxParams p) {
       }
     }
   }
-  if (lane == 0) sp->xcols = ncols + 1;
+  if (lane == 0) {
+    sp->xcols = ncols + 1;
+    sp->t_pc = tpc;  // the next round's push carries these into the ring entry
+    sp->t_addr = taddr;
+    sp->t_flags = p.iflags[tgt];
+  }
 }
 
 // ---------------------------------------------------------------------------
