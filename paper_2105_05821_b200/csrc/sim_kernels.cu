@@ -92,103 +92,112 @@ __device__ __forceinline__ uint64_t head_gap(uint64_t cur, uint64_t push, uint32
 
 // ---------------------------------------------------------------------------
 // K1: apply the pending step, drain finished sub-traces, gather the next input.
+// One 128-thread block per sub-trace: warp 0 runs the (inherently serial)
+// queue update with warp ballots; then all 128 threads gather, one column
+// descriptor per thread and one coalesced pass over the row, so the gather is
+// two dependent memory levels (ring entries, static slots) instead of a
+// per-warp loop of them.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCtxWarps * 32)
+__global__ void __launch_bounds__(kCtxThreads)
 ctx_kernel(CtxParams p) {
-  // per column: instruction index and the 9 dynamic slots (41..49), normalised
-  __shared__ uint32_t s_inst[kCtxWarps][kMaxCols];
-  __shared__ float s_dyn[kCtxWarps][kMaxCols][kSlots - kStatic];
+  __shared__ uint32_t s_inst[kMaxCols];                // instruction of each column
+  __shared__ float s_dyn[kMaxCols][kSlots - kStatic];  // its 9 dynamic slots, normalised
+  __shared__ SubState s_st;                            // state after the apply step
 
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t lane = lane_id();
-  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kCtxWarps + warp + p.first;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  const uint64_t s = blockIdx.x + p.first;
   if (s >= p.last) return;
 
   SubState* sp = p.state + s;
-  SubState st = *sp;  // every lane holds a copy; lane 0 writes back
-  if (st.status != kOk) return;
   const NormConsts& nc = *p.nc;
   Rings r{p.proc + s * (p.pmask + 1ull), p.wq + s * (p.wmask + 1ull), p.pmask, p.wmask, p.wmask + 1u};
-  uint32_t err = kOk;
-
-  if (st.has_pend) {
-    const uint32_t F = st.pend_f;
-    // fetch advance: K3 already moved cur by F (lumped); retire with budget bw*F
-    if (F > 0) {
-      if (p.per_cycle) {
-        for (uint32_t c = 0; c < F && err == kOk; ++c) {
-          st.cur += 1;
-          warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+  if (warp == 0) {
+    SubState st = *sp;  // every lane holds a copy; lane 0 writes back
+    uint32_t err = kOk;
+    if (st.status == kOk) {
+      if (st.has_pend) {
+        const uint32_t F = st.pend_f;
+        // fetch advance: K3 already moved cur by F (lumped); retire with budget bw*F
+        if (F > 0) {
+          if (p.per_cycle) {
+            for (uint32_t c = 0; c < F && err == kOk; ++c) {
+              st.cur += 1;
+              warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+            }
+          } else {
+            warp_retire(st.cur, static_cast<uint64_t>(p.bw) * F, r, st.ph, st.pt, st.wh, st.wt, &err);
+          }
         }
-      } else {
-        warp_retire(st.cur, static_cast<uint64_t>(p.bw) * F, r, st.ph, st.pt, st.wh, st.wt, &err);
-      }
-    }
-    // forced stall (simcore.cpp:127-136): budget bw, not bw*gap
-    while (err == kOk && st.pt - st.ph >= static_cast<uint32_t>(p.max_context)) {
-      const uint32_t before = st.pt - st.ph;
-      const RingEntry& h = r.proc[st.ph & r.pmask];
-      const uint64_t gap = head_gap(st.cur, h.push, h.exec);
-      st.cur += gap;
-      st.overflow += gap;
-      warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
-      if (err == kOk && st.pt - st.ph >= before) {
-        err = kErrStall;
-        st.err_tick = st.cur;
-      }
-    }
-    if (err == kOk) {  // push (simcore.cpp:138-145)
-      if (lane == 0) {
-        RingEntry e;
-        e.push = st.cur;
-        e.idx = st.pos;
-        e.exec = st.pend_e;
-        e.store = st.pend_s;
-        e.nexec = norm_slot(static_cast<int32_t>(st.pend_e), nc.mean[kSlotExecution], nc.sd[kSlotExecution]);
-        e.nstore = norm_slot(static_cast<int32_t>(st.pend_s), nc.mean[kSlotStore], nc.sd[kSlotStore]);
-        e.pc = st.t_pc;  // stashed by this sub-trace's previous gather (0 when none ran)
-        e.addr = st.t_addr;
-        e.flags = p.gather ? st.t_flags : p.iflags[st.begin + st.pos];
-        r.proc[st.pt & r.pmask] = e;
-      }
-      st.pt += 1;
-      st.pos += 1;
-      st.has_pend = 0;
-      if (st.pos == st.warm) {  // warm-up extension: counting starts after this step
-        st.base_cur = st.cur;
-        st.base_overflow = st.overflow;
-      }
-      // drain right after the last step (parallel.cpp:79, simcore.cpp:152-159)
-      if (st.pos == st.len && st.count_drain) {
-        while (err == kOk && (st.ph != st.pt || st.wh != st.wt)) {
-          uint64_t gap = ~uint64_t{0};
-          if (st.ph != st.pt) {
-            const RingEntry& h = r.proc[st.ph & r.pmask];
-            { const uint64_t g = head_gap(st.cur, h.push, h.exec); gap = g < gap ? g : gap; }
-          }
-          if (st.wh != st.wt) {
-            const RingEntry& h = r.wq[st.wh & r.wmask];
-            { const uint64_t g = head_gap(st.cur, h.push, h.store); gap = g < gap ? g : gap; }
-          }
-          if (gap < 1) gap = 1;
+        // forced stall (simcore.cpp:127-136): budget bw, not bw*gap
+        while (err == kOk && st.pt - st.ph >= static_cast<uint32_t>(p.max_context)) {
+          const uint32_t before = st.pt - st.ph;
+          const RingEntry& h = r.proc[st.ph & r.pmask];
+          const uint64_t gap = head_gap(st.cur, h.push, h.exec);
           st.cur += gap;
-          st.drain += gap;
-          const uint32_t ev = warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
-          if (err == kOk && ev == 0) {
-            err = kErrDrain;
+          st.overflow += gap;
+          warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+          if (err == kOk && st.pt - st.ph >= before) {
+            err = kErrStall;
             st.err_tick = st.cur;
           }
         }
+        if (err == kOk) {  // push (simcore.cpp:138-145)
+          if (lane == 0) {
+            RingEntry e;
+            e.push = st.cur;
+            e.idx = st.pos;
+            e.exec = st.pend_e;
+            e.store = st.pend_s;
+            e.nexec = norm_slot(static_cast<int32_t>(st.pend_e), nc.mean[kSlotExecution], nc.sd[kSlotExecution]);
+            e.nstore = norm_slot(static_cast<int32_t>(st.pend_s), nc.mean[kSlotStore], nc.sd[kSlotStore]);
+            e.pc = st.t_pc;  // stashed by this sub-trace's previous gather (0 when none ran)
+            e.addr = st.t_addr;
+            e.flags = p.gather ? st.t_flags : p.iflags[st.begin + st.pos];
+            r.proc[st.pt & r.pmask] = e;
+          }
+          st.pt += 1;
+          st.pos += 1;
+          st.has_pend = 0;
+          if (st.pos == st.warm) {  // warm-up extension: counting starts after this step
+            st.base_cur = st.cur;
+            st.base_overflow = st.overflow;
+          }
+          // drain right after the last step (parallel.cpp:79, simcore.cpp:152-159)
+          if (st.pos == st.len && st.count_drain) {
+            while (err == kOk && (st.ph != st.pt || st.wh != st.wt)) {
+              uint64_t gap = ~uint64_t{0};
+              if (st.ph != st.pt) {
+                const RingEntry& h = r.proc[st.ph & r.pmask];
+                { const uint64_t g = head_gap(st.cur, h.push, h.exec); gap = g < gap ? g : gap; }
+              }
+              if (st.wh != st.wt) {
+                const RingEntry& h = r.wq[st.wh & r.wmask];
+                { const uint64_t g = head_gap(st.cur, h.push, h.store); gap = g < gap ? g : gap; }
+              }
+              if (gap < 1) gap = 1;
+              st.cur += gap;
+              st.drain += gap;
+              const uint32_t ev = warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
+              if (err == kOk && ev == 0) {
+                err = kErrDrain;
+                st.err_tick = st.cur;
+              }
+            }
+          }
+        }
+        if (err != kOk) st.status = err;
+        __syncwarp();
+        if (lane == 0) *sp = st;
+        __syncwarp();
       }
     }
-    if (err != kOk) st.status = err;
-    __syncwarp();
-    if (lane == 0) *sp = st;
-    __syncwarp();
+    (void)err;
+    if (lane == 0) s_st = st;
   }
-
+  __syncthreads();
+  const SubState st = s_st;
   if (!p.gather || st.status != kOk || st.pos >= st.len) return;
 
   // ---- gather (simcore.cpp:25-66) --------------------------------------
@@ -203,55 +212,34 @@ ctx_kernel(CtxParams p) {
   // context instruction's pc/address/flags (newest first: proc, then write
   // queue).  Loads are unconditional from clamped, always-valid addresses so
   // they issue back to back; predicates only select the results.
-  for (uint32_t c0 = 0; c0 <= ncols; c0 += 128) {
-    RingEntry e[4];
-    bool ok[4];
+  for (uint32_t c = tid; c <= ncols; c += kCtxThreads) {
+    if (c == 0) {
+      s_inst[0] = static_cast<uint32_t>(tgt);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t c = c0 + u * 32 + lane;
-      ok[u] = c >= 1 && c <= ncols;
-      const uint32_t j = ok[u] ? c - 1 : 0;
-      const RingEntry* src = j < nproc ? &r.proc[(st.pt - 1 - j) & r.pmask]
-                                       : &r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
-      e[u] = (nproc + nwq) > 0 ? *src : RingEntry{};
+      for (int k = kStatic; k < kSlots; ++k) s_dyn[0][k - kStatic] = nc.zero[k];
+      continue;
     }
-    uint64_t cpc[4], ca[4];
-    uint32_t cf[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      cpc[u] = e[u].pc;
-      ca[u] = e[u].addr;
-      cf[u] = e[u].flags;
+    const uint32_t j = c - 1;
+    const RingEntry e = j < nproc ? r.proc[(st.pt - 1 - j) & r.pmask] : r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
+    const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e.push));
+    // memory_dependency_flags (dataset.cpp:47-60)
+    uint32_t f = (tpc / p.line) == (e.pc / p.line) ? 1u : 0u;
+    if (tmem && (e.flags & kFlagMem)) {
+      f |= (taddr == e.addr) ? 2u : 0u;
+      f |= (taddr / p.line) == (e.addr / p.line) ? 4u : 0u;
+      f |= (taddr / p.page) == (e.addr / p.page) ? 8u : 0u;
     }
+    f |= (tpc / p.page) == (e.pc / p.page) ? 16u : 0u;
+    float* d = s_dyn[c];
+    s_inst[c] = static_cast<uint32_t>(st.begin + e.idx);
+    d[0] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
+    d[1] = e.nexec;
+    d[2] = e.nstore;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t c = c0 + u * 32 + lane;
-      if (c == 0) {
-        s_inst[warp][0] = static_cast<uint32_t>(tgt);
-#pragma unroll
-        for (int k = kStatic; k < kSlots; ++k) s_dyn[warp][0][k - kStatic] = nc.zero[k];
-      } else if (ok[u]) {
-        const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e[u].push));
-        // memory_dependency_flags (dataset.cpp:47-60)
-        uint32_t f = (tpc / p.line) == (cpc[u] / p.line) ? 1u : 0u;
-        if (tmem && (cf[u] & kFlagMem)) {
-          f |= (taddr == ca[u]) ? 2u : 0u;
-          f |= (taddr / p.line) == (ca[u] / p.line) ? 4u : 0u;
-          f |= (taddr / p.page) == (ca[u] / p.page) ? 8u : 0u;
-        }
-        f |= (tpc / p.page) == (cpc[u] / p.page) ? 16u : 0u;
-        float* d = s_dyn[warp][c];
-        s_inst[warp][c] = static_cast<uint32_t>(st.begin + e[u].idx);
-        d[0] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);
-        d[1] = e[u].nexec;
-        d[2] = e[u].nstore;
-#pragma unroll
-        for (int b = 0; b < 5; ++b) d[3 + b] = ((f >> b) & 1u) ? nc.one[kSlotFlag0 + b] : nc.zero[kSlotFlag0 + b];
-        d[8] = nc.zero[kSlotReserved];
-      }
-    }
+    for (int b = 0; b < 5; ++b) d[3 + b] = ((f >> b) & 1u) ? nc.one[kSlotFlag0 + b] : nc.zero[kSlotFlag0 + b];
+    d[8] = nc.zero[kSlotReserved];
   }
-  __syncwarp();
+  __syncthreads();
 
   // Row write: live columns, then zeros only where the previous round of this
   // sub-trace left non-zero columns (the rest of the row is already 0).  The
@@ -261,23 +249,23 @@ ctx_kernel(CtxParams p) {
   const uint32_t n4 = ((live > prev ? live : prev) + 3) / 4;
   float4* out4 = reinterpret_cast<float4*>(static_cast<float*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride));
   __nv_bfloat16* outb = static_cast<__nv_bfloat16*>(p.x) + (s - p.first) * static_cast<uint64_t>(p.x_stride);
-  for (uint32_t q0 = 0; q0 < n4; q0 += 128) {
+  for (uint32_t q0 = 0; q0 < n4; q0 += 4 * kCtxThreads) {
     float stv[4][4], dyv[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const uint32_t jf = 4 * (q0 + u * 32 + lane) + t;
+        const uint32_t jf = 4 * (q0 + u * kCtxThreads + tid) + t;
         const uint32_t col = jf / kSlots, slot = jf - col * kSlots;
         const uint32_t colc = jf < live ? col : 0u;
         const bool st_slot = slot < kStatic;
-        stv[u][t] = __ldg(p.stat + static_cast<uint64_t>(s_inst[warp][colc]) * kStatStride + (st_slot ? slot : 0u));
-        dyv[u][t] = s_dyn[warp][colc][st_slot ? 0u : slot - kStatic];
+        stv[u][t] = __ldg(p.stat + static_cast<uint64_t>(s_inst[colc]) * kStatStride + (st_slot ? slot : 0u));
+        dyv[u][t] = s_dyn[colc][st_slot ? 0u : slot - kStatic];
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint32_t q = q0 + u * 32 + lane;
+      const uint32_t q = q0 + u * kCtxThreads + tid;
       float v[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -299,7 +287,7 @@ ctx_kernel(CtxParams p) {
       }
     }
   }
-  if (lane == 0) {
+  if (tid == 0) {
     sp->xcols = ncols + 1;
     sp->t_pc = tpc;  // the next round's push carries these into the ring entry
     sp->t_addr = taddr;
@@ -386,8 +374,7 @@ void launch_pack_inputs(const float* in, uint64_t n, uint32_t width, void* x, ui
 void launch_ctx(const CtxParams& p, cudaStream_t stream) {
   const uint64_t n = p.last - p.first;
   if (n == 0) return;
-  const unsigned blocks = static_cast<unsigned>((n + kCtxWarps - 1) / kCtxWarps);
-  launch_pdl(ctx_kernel, dim3(blocks), dim3(kCtxWarps * 32), 0, stream, p);
+  launch_pdl(ctx_kernel, dim3(static_cast<unsigned>(n)), dim3(kCtxThreads), 0, stream, p);
 }
 
 void launch_decode(const DecodeParams& p, cudaStream_t stream) {

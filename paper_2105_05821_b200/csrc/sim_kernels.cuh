@@ -6,7 +6,7 @@
 
 namespace simnet {
 
-constexpr int kCtxWarps = 8;    // sub-traces per K1 block (one warp each)
+constexpr int kCtxThreads = 128;  // K1 block: one sub-trace per block (warp 0 applies, all gather)
 constexpr int kMaxCols = 128;   // max_context + 1 supported by the gather (C3: 111)
 
 struct CtxParams {
