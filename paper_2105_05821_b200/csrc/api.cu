@@ -13,6 +13,7 @@
 
 #include "../../include/ilsim_gpu.h"
 #include "common.cuh"
+#include "conv_chain.cuh"
 #include "gemm.cuh"
 #include "host_util.cuh"
 #include "model.cuh"
@@ -229,7 +230,9 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   const int xprec = oracle ? ILSIM_PREC_FP32 : c->precision;
   const uint32_t x_stride = needs_input ? input_stride(mc, xprec) : 0;
   const uint32_t x_floats = needs_input ? input_row_floats(mc) : 0;
-  const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(xprec);
+  const bool x_split = !oracle && split_input(c->model);  // 3xTF32 hi/lo planes
+  const uint64_t x_lo_off = x_split ? chunk * x_stride : 0;
+  const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(xprec) * (x_split ? 2 : 1);
   void* d_x = needs_input ? c->x.need(x_bytes) : nullptr;
   if (needs_input) CUDA_OK(cudaMemsetAsync(d_x, 0, x_bytes, c->stream));  // bf16 row padding stays 0
   ForwardBuffers fb{};
@@ -254,6 +257,8 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     cp.x_floats = x_floats;
     cp.x_bf16 = xprec == ILSIM_PREC_BF16;
     cp.x_full = K > chunk;
+    cp.x_split = x_split;
+    cp.x_lo_off = x_lo_off;
     cp.max_context = mc;
     cp.bw = cfg.retire_bandwidth;
     cp.line = cfg.line_size;
@@ -284,7 +289,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   auto do_forward = [&](uint64_t f, uint64_t l) -> uint64_t {
     if (oracle) return 0;
     const DecodeParams dp = decode_params(f, l);
-    return forward_launch(c->model, c->precision, d_x, x_stride, l - f, fb, c->stream, &dp, &k3_fused);
+    return forward_launch(c->model, c->precision, d_x, x_stride, l - f, fb, c->stream, &dp, &k3_fused, x_lo_off);
   };
   auto do_decode = [&](uint64_t f, uint64_t l) -> uint64_t {
     if (k3_fused) return 0;
@@ -449,6 +454,14 @@ int guard(ilsim_gpu_ctx* c, F&& f) {
 
 extern "C" {
 
+// Diagnostics only (not in ilsim_gpu.h): copy the conv-chain event clocks of
+// the last traced launch (SIMNET_CHAIN_TRACE=1) into out[148*32].
+int simnet_debug_chain_trace(long long* out) {
+  long long* p = chain_trace_ptr();
+  if (!p) return 1;
+  return cudaMemcpy(out, p, 148 * 32 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
+
 int ilsim_gpu_abi_version(void) { return ILSIM_GPU_ABI_VERSION; }
 
 int ilsim_gpu_create(const ilsim_gpu_options* o, ilsim_gpu_ctx** out, char* err, int errlen) {
@@ -563,7 +576,8 @@ int ilsim_gpu_predict(ilsim_gpu_ctx* c, const float* inputs, uint64_t n, const u
     const uint32_t width = static_cast<uint32_t>(kSlots * (mc + 1));
     const uint32_t x_stride = input_stride(mc, c->precision);
     const uint64_t chunk = std::min<uint64_t>(n, 65536);
-    const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(c->precision);
+    const uint64_t x_lo_off = split_input(c->model) ? chunk * x_stride : 0;
+    const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(c->precision) * (x_lo_off ? 2 : 1);
     void* d_x = c->x.need(x_bytes);
     ForwardBuffers fb = forward_buffers(c->model, chunk, c->act, c->y);
     DevBuf d_store, d_trip, d_in;
@@ -575,9 +589,9 @@ int ilsim_gpu_predict(ilsim_gpu_ctx* c, const float* inputs, uint64_t n, const u
       CUDA_OK(cudaMemsetAsync(d_x, 0, x_bytes, c->stream));
       CUDA_OK(cudaMemcpyAsync(din, inputs + f * width, m * width * sizeof(float), cudaMemcpyHostToDevice,
                               c->stream));
-      launch_pack_inputs(din, m, width, d_x, x_stride, c->precision == ILSIM_PREC_BF16, c->stream);
+      launch_pack_inputs(din, m, width, d_x, x_stride, c->precision == ILSIM_PREC_BF16, x_lo_off, c->stream);
       CUDA_OK(cudaMemcpyAsync(ds, is_store + f, m, cudaMemcpyHostToDevice, c->stream));
-      forward_launch(c->model, c->precision, d_x, x_stride, m, fb, c->stream);
+      forward_launch(c->model, c->precision, d_x, x_stride, m, fb, c->stream, nullptr, nullptr, x_lo_off);
       launch_decode_only(fb.y, fb.y_stride, m, ds, c->nc_dev.as<NormConsts>(), c->cfg.class_fetch,
                          c->cfg.class_exec, c->cfg.class_store, dt, c->stream);
       CUDA_OK(cudaGetLastError());

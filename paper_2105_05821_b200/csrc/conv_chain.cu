@@ -14,7 +14,7 @@
 //
 //   warp 0      TMA producer (weights per layer, gathered-input chunks)
 //   warp 1      TMEM allocator + tcgen05.mma issuer
-//   warps 2-5   3xTF32 hi/lo split of input chunks
+//   warps 2-5   spare (K1 writes the 3xTF32 hi/lo input planes)
 //   warps 6-9   epilogue: TMEM -> bias/ReLU -> restage (or -> global)
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -104,7 +104,8 @@ __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, int ar, int
 
 template <int kMode>
 __global__ void __launch_bounds__(kThreadsCC, 1)
-conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW0,
+conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmXlo,
+                  const __grid_constant__ CUtensorMap tmW0,
                   const __grid_constant__ CUtensorMap tmW0lo, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW1lo, const __grid_constant__ CUtensorMap tmW2,
                   const __grid_constant__ CUtensorMap tmW2lo, ChainParams p) {
@@ -158,6 +159,12 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  // diagnostics: clock64 per event for the first work item of each CTA
+  long long* tr = p.trace ? p.trace + blockIdx.x * 32 : nullptr;
+  auto mark = [&](int i) {
+    if (tr) tr[i] = clock64();
+  };
+  if (threadIdx.x == 0) mark(0);
 
   auto load_w = [&](int layer, const CUtensorMap* hi, const CUtensorMap* lo, int chunks) {
     uint64_t* b = &bar_w[layer];
@@ -176,19 +183,25 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         if (it > 0) mbar_wait(&bar_m2, (it - 1) & 1);  // previous conv2 done: R1, R2 free
         load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
+        if (it == 0) mark(1);
         for (int c = 0; c < 4 * S::kK0Chunks; ++c) {
           const int tile = c / S::kK0Chunks, kc = c % S::kK0Chunks;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], S::kStage);
+          mbar_expect_tx(&full[stage], S::kStage * (S::kSplit ? 2u : 1u));
           tma_load_3d(ringA + stage * S::kStage, &tmX, &full[stage], kc * S::kElems, 0, item * kItem + 2 * tile);
+          if (S::kSplit)  // K1 wrote the 3xTF32 lo plane next to the hi plane
+            tma_load_3d(ringA + (kRing + stage) * S::kStage, &tmXlo, &full[stage], kc * S::kElems, 0,
+                        item * kItem + 2 * tile);
           if (++stage == kRing) {
             stage = 0;
             phase ^= 1;
           }
         }
         mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
+        if (it == 0) mark(2);
         load_w(1, &tmW1, &tmW1lo, S::kKChunks);
         mbar_wait(&bar_m1b, it & 1);  // conv1 done: W1 no longer read
+        if (it == 0) mark(3);
         load_w(2, &tmW2, &tmW2lo, S::kKChunks);
       }
     }
@@ -216,11 +229,12 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         // conv0: 4 tiles of 128 rows (2 samples each) streamed through the ring
         mbar_wait(&bar_w[0], it & 1);
+        if (it == 0) mark(4);
         tc_fence_after();
         for (int tile = 0; tile < 4; ++tile) {
           const uint32_t d = tmem + tile * kC;
           for (int kc = 0; kc < S::kK0Chunks; ++kc) {
-            mbar_wait(S::kSplit ? &split[stage] : &full[stage], phase);
+            mbar_wait(&full[stage], phase);
             tc_fence_after();
             const int steps = kc == S::kK0Chunks - 1 ? S::kK0Steps - 4 * (S::kK0Chunks - 1) : 4;
             for (int j = 0; j < steps; ++j) {
@@ -243,57 +257,35 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           }
         }
         mma_commit(&bar_c0);
+        if (it == 0) mark(5);
         // conv1: two tiles of 128 rows (4 samples each), A restaged by the epilogue
         mbar_wait(&bar_a[0], it & 1);
+        if (it == 0) mark(6);
         mbar_wait(&bar_w[1], it & 1);
+        if (it == 0) mark(7);
         tc_fence_after();
         gemm_resident_a(tmem + 256, 4 * S::kKChunks);
         mma_commit(&bar_m1a);
         mbar_wait(&bar_a[1], it & 1);
+        if (it == 0) mark(8);
         tc_fence_after();
         gemm_resident_a(tmem + 256 + kC, 4 * S::kKChunks);
         mma_commit(&bar_m1b);
         // conv2: one tile of 128 rows (8 samples)
         mbar_wait(&bar_a[2], it & 1);
+        if (it == 0) mark(9);
         mbar_wait(&bar_w[2], it & 1);
+        if (it == 0) mark(10);
         if (it > 0) mbar_wait(&bar_out, (it - 1) & 1);  // previous conv2 accumulator drained
         tc_fence_after();
         gemm_resident_a(tmem + 384, 4 * S::kKChunks);
         mma_commit(&bar_m2);
+        if (it == 0) mark(11);
       }
     }
     __syncwarp();
   } else if (warp < 6) {
-    if (S::kSplit) {  // 3xTF32 split of every landed input chunk
-      const int t128 = threadIdx.x - 64;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        for (int c = 0; c < 4 * S::kK0Chunks; ++c) {
-          mbar_wait(&full[stage], phase);
-          uint4* a = reinterpret_cast<uint4*>(ringA + stage * S::kStage);
-          float4* alo = reinterpret_cast<float4*>(ringA + (kRing + stage) * S::kStage);
-#pragma unroll 4
-          for (int i = t128; i < static_cast<int>(S::kStage / 16); i += 128) {
-            const uint4 u = a[i];
-            uint4 h;
-            h.x = (u.x + 0x1000u) & 0xffffe000u;
-            h.y = (u.y + 0x1000u) & 0xffffe000u;
-            h.z = (u.z + 0x1000u) & 0xffffe000u;
-            h.w = (u.w + 0x1000u) & 0xffffe000u;
-            alo[i] = make_float4(__uint_as_float(u.x) - __uint_as_float(h.x), __uint_as_float(u.y) - __uint_as_float(h.y),
-                                 __uint_as_float(u.z) - __uint_as_float(h.z), __uint_as_float(u.w) - __uint_as_float(h.w));
-            a[i] = h;
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&split[stage]);
-          if (++stage == kRing) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
+    // warps 2-5: spare (the 3xTF32 split of the input now happens in K1)
   } else {
     // epilogue warps 6..9: thread owns TMEM lane m = 32*(warp%4) + lane
     const int quad = warp & 3;
@@ -326,6 +318,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       mbar_arrive(&bar_a[2]);
       // conv2 -> flat[sample][pos*64 + c]: row m of the tile is flat row item*128 + m
       mbar_wait(&bar_m2, it & 1);
+      if (it == 0 && m == 0) mark(12);
       tc_fence_after();
       const int sample = item * kItem + (m >> 4);
       for (int c0 = 0; c0 < kC; c0 += 16) {
@@ -355,6 +348,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       }
       tc_fence_before();
       mbar_arrive(&bar_out);
+      if (it == 0 && m == 0) mark(13);
     }
   }
   tc_fence_before();
@@ -367,17 +361,17 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
 size_t chain_smem_bytes() { return kR1 + kR2 + 1024; }
 
-void launch_conv_chain(int mode, const CUtensorMap& x, const CUtensorMap* w, const ChainParams& p, int num_sms,
-                       cudaStream_t s) {
+void launch_conv_chain(int mode, const CUtensorMap& x, const CUtensorMap& xlo, const CUtensorMap* w,
+                       const ChainParams& p, int num_sms, cudaStream_t s) {
   const int items = (p.samples + kItem - 1) / kItem;
   const dim3 grid(static_cast<unsigned>(items < num_sms ? items : num_sms));
   const size_t sm = chain_smem_bytes();
   if (mode == kBF16)
-    conv_chain_kernel<kBF16><<<grid, kThreadsCC, sm, s>>>(x, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    conv_chain_kernel<kBF16><<<grid, kThreadsCC, sm, s>>>(x, xlo, w[0], w[1], w[2], w[3], w[4], w[5], p);
   else if (mode == kTF32)
-    conv_chain_kernel<kTF32><<<grid, kThreadsCC, sm, s>>>(x, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    conv_chain_kernel<kTF32><<<grid, kThreadsCC, sm, s>>>(x, xlo, w[0], w[1], w[2], w[3], w[4], w[5], p);
   else
-    conv_chain_kernel<kTF32x3><<<grid, kThreadsCC, sm, s>>>(x, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    conv_chain_kernel<kTF32x3><<<grid, kThreadsCC, sm, s>>>(x, xlo, w[0], w[1], w[2], w[3], w[4], w[5], p);
 }
 
 void conv_chain_set_attributes() {

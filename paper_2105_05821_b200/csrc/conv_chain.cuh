@@ -13,12 +13,18 @@ struct ChainParams {
   const float* b1;
   const float* b2;
   void* out;  // flat [samples][1024] (f32, or bf16 for the bf16 path)
+  long long* trace;  // optional: per-CTA event clocks (diagnostics, SIMNET_CHAIN_TRACE)
 };
 
 // w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
-void launch_conv_chain(int mode, const CUtensorMap& x, const CUtensorMap* w, const ChainParams& p, int num_sms,
-                       cudaStream_t s);
+// x / xlo: gathered input planes (xlo: 3xTF32 lo plane, ignored otherwise)
+void launch_conv_chain(int mode, const CUtensorMap& x, const CUtensorMap& xlo, const CUtensorMap* w,
+                       const ChainParams& p, int num_sms, cudaStream_t s);
 void conv_chain_set_attributes();
 size_t chain_smem_bytes();
+inline long long*& chain_trace_ptr() {
+  static long long* p = nullptr;
+  return p;
+}
 
 }  // namespace simnet

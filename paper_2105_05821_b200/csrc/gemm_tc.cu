@@ -586,8 +586,10 @@ void tc_prepare(const DevModel& m, uint64_t samples) {
   t.part.need(samples * static_cast<uint64_t>(m.cfg.fc_hidden) * nsplit * sizeof(float));
 }
 
+bool tc_split_input(const TcModel* t) { return t->chain && t->mode == kTF32x3; }
+
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride, uint64_t samples,
-                    const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse) {
+                    const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse, uint64_t x_lo_off) {
   (void)precision;
   TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
@@ -608,10 +610,20 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     const uint64_t strides[2] = {row_elems * esz, static_cast<uint64_t>(x_stride) * esz};
     const uint32_t box[3] = {static_cast<uint32_t>(chunk_elems), 64, 2};
     const CUtensorMap xmap = make_map(x, bf, 3, dims, strides, box);
+    if (mode == kTF32x3 && x_lo_off == 0) throw ApiError("internal: 3xTF32 chain needs split input planes");
+    const CUtensorMap xlo = mode == kTF32x3
+                                ? make_map(static_cast<const float*>(x) + x_lo_off, false, 3, dims, strides, box)
+                                : xmap;
     const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
                               t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
-    ChainParams cp{static_cast<int>(samples), P + m.L.b[0], P + m.L.b[1], P + m.L.b[2], fb.act[2]};
-    launch_conv_chain(mode, xmap, w, cp, num_sms(), s);
+    ChainParams cp{static_cast<int>(samples), P + m.L.b[0], P + m.L.b[1], P + m.L.b[2], fb.act[2], nullptr};
+    static long long* trace_buf = nullptr;  // SIMNET_CHAIN_TRACE: event clocks of the last launch
+    if (std::getenv("SIMNET_CHAIN_TRACE")) {
+      if (!trace_buf) CUDA_OK(cudaMalloc(&trace_buf, 148 * 32 * sizeof(long long)));
+      cp.trace = trace_buf;
+      chain_trace_ptr() = trace_buf;
+    }
+    launch_conv_chain(mode, xmap, xlo, w, cp, num_sms(), s);
     ++launches;
     in = fb.act[2];
     len = 0;

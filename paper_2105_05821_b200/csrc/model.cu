@@ -120,6 +120,8 @@ void init_weights_into(const ilsim_cnn_config& c, uint64_t seed, float* out) {
   fill(L.fc2_b, L.out_dim, 1);
 }
 
+bool split_input(const DevModel& m) { return m.tc != nullptr && tc_split_input(m.tc); }
+
 DevModel::~DevModel() {
   if (tc) tc_model_destroy(tc);
 }
@@ -161,11 +163,11 @@ ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, D
 
 uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32_t x_stride,
                         uint64_t samples, const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse,
-                        bool* fused) {
+                        bool* fused, uint64_t x_lo_off) {
   if (fused) *fused = false;
   if (precision != ILSIM_PREC_FP32) {
     if (fused) *fused = fuse != nullptr;
-    return tc_forward(m, precision, xv, x_stride, samples, fb, s, fuse);
+    return tc_forward(m, precision, xv, x_stride, samples, fb, s, fuse, x_lo_off);
   }
   const float* x = static_cast<const float*>(xv);
   const ilsim_cnn_config& c = m.cfg;

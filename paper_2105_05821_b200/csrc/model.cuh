@@ -64,13 +64,18 @@ ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, D
 // tail and returns true in *fused.
 uint64_t forward_launch(const DevModel& m, int precision, const void* x, uint32_t x_stride,
                         uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
-                        const DecodeParams* fuse = nullptr, bool* fused = nullptr);
+                        const DecodeParams* fuse = nullptr, bool* fused = nullptr, uint64_t x_lo_off = 0);
+// True when the model's inference wants the gathered input pre-split into
+// 3xTF32 hi / lo planes (tensor-core 3xTF32 with the fused conv chain).
+bool split_input(const DevModel& m);
 
 // tensor-core path (gemm_tc.cu)
 TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s);
 void tc_model_destroy(TcModel* t);
 void tc_prepare(const DevModel& m, uint64_t samples);
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride,
-                    uint64_t samples, const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse);
+                    uint64_t samples, const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse,
+                    uint64_t x_lo_off);
+bool tc_split_input(const TcModel* t);
 
 }  // namespace simnet

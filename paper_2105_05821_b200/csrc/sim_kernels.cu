@@ -282,6 +282,15 @@ ctx_kernel(CtxParams p) {
         w.x = *reinterpret_cast<uint32_t*>(&a);
         w.y = *reinterpret_cast<uint32_t*>(&b);
         *reinterpret_cast<uint2*>(outb + row * 104 + within) = w;
+      } else if (p.x_split) {  // 3xTF32: hi = tf32 round-half-away (cvt.rna), lo = v - hi (exact)
+        float h[4], l[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          h[t] = __uint_as_float((__float_as_uint(v[t]) + 0x1000u) & 0xffffe000u);
+          l[t] = v[t] - h[t];
+        }
+        out4[q] = make_float4(h[0], h[1], h[2], h[3]);
+        reinterpret_cast<float4*>(reinterpret_cast<float*>(out4) + p.x_lo_off)[q] = make_float4(l[0], l[1], l[2], l[3]);
       } else {
         out4[q] = make_float4(v[0], v[1], v[2], v[3]);
       }
@@ -350,7 +359,7 @@ __global__ void pack_kernel(PackParams p) {
 }
 
 __global__ void pack_inputs_kernel(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride,
-                                   int x_bf16) {
+                                   int x_bf16, uint64_t x_lo_off) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n * width) return;
   const uint64_t smp = i / width;
@@ -358,17 +367,22 @@ __global__ void pack_inputs_kernel(const float* in, uint64_t n, uint32_t width, 
   if (x_bf16) {
     const uint32_t row = j / 100, within = j - 100 * row;
     static_cast<__nv_bfloat16*>(x)[smp * x_stride + row * 104 + within] = __float2bfloat16_rn(in[i]);
+  } else if (x_lo_off) {
+    const float v = in[i];
+    const float h = __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u);
+    static_cast<float*>(x)[smp * x_stride + j] = h;
+    static_cast<float*>(x)[smp * x_stride + j + x_lo_off] = v - h;
   } else {
     static_cast<float*>(x)[smp * x_stride + j] = in[i];
   }
 }
 
 void launch_pack_inputs(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride, int x_bf16,
-                        cudaStream_t stream) {
+                        uint64_t x_lo_off, cudaStream_t stream) {
   const uint64_t tot = n * width;
   if (tot == 0) return;
   pack_inputs_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(in, n, width, x, x_stride,
-                                                                                    x_bf16);
+                                                                                    x_bf16, x_lo_off);
 }
 
 void launch_ctx(const CtxParams& p, cudaStream_t stream) {

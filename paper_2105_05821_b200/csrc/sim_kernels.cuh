@@ -25,6 +25,8 @@ struct CtxParams {
   uint32_t x_floats;         // logical floats per sample (100 per conv0 row, multiple of 4)
   int32_t x_bf16;            // 1: rows of 104 bf16 (100 + zero pad, TMA-aligned)
   int32_t x_full;            // 1: rewrite whole rows (x rows shared between chunks)
+  int32_t x_split;           // 1: 3xTF32 planes: x = tf32 hi, x + x_lo_off = lo (x - hi)
+  uint64_t x_lo_off;         // elements from the hi plane to the lo plane
   int32_t max_context;
   uint32_t bw, line, page;
   int32_t per_cycle;
@@ -63,6 +65,6 @@ void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t*
 void launch_pack(const PackParams& p, cudaStream_t stream);
 // Caller inputs [n][width] f32 -> gathered-input layout (ilsim_gpu_predict).
 void launch_pack_inputs(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride, int x_bf16,
-                        cudaStream_t stream);
+                        uint64_t x_lo_off, cudaStream_t stream);
 
 }  // namespace simnet
