@@ -88,7 +88,9 @@ typedef struct ilsim_sim_config {
   uint64_t shard_end;     /*   shard_end) of the global partition; 0,0 = all        */
   /* reserved[0]: 1 = per-kernel event timing (no graphs, diagnostics);
    * reserved[1]: 1 = oracle latencies but inputs still gathered (input-parity
-   * test hook; the reference's OraclePredictor builds none, simcore.cpp:32). */
+   * test hook; the reference's OraclePredictor builds none, simcore.cpp:32);
+   * reserved[2]: 1 = unfused tensor-core round (separate K1 kernel + TMA conv
+   * chain) instead of the fused round front (A/B diagnostics). */
   int32_t reserved[4];
 } ilsim_sim_config;
 

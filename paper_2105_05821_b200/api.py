@@ -215,7 +215,7 @@ class GpuSimulator:
 
     # -- simulation ---------------------------------------------------------
     def _sim_cfg(self, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None,
-                 profile=False, truth_inputs=False) -> _lib.SimCfg:
+                 profile=False, truth_inputs=False, fused=True) -> _lib.SimCfg:
         s = pc.sim
         c = _lib.SimCfg()
         c.k, c.subtrace_size, c.batch_max = pc.k, pc.subtrace_size, pc.batch_max
@@ -233,6 +233,7 @@ class GpuSimulator:
             c.shard_begin, c.shard_end = shard
         c.reserved[0] = int(profile)
         c.reserved[1] = int(truth_inputs)
+        c.reserved[2] = int(not fused)
         return c
 
     def load_trace(self, trace: Trace, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None):
@@ -243,11 +244,13 @@ class GpuSimulator:
         del keep
 
     def run(self, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None, profile=False,
-            truth_inputs=False, n_total: int | None = None) -> ParallelResult:
+            truth_inputs=False, n_total: int | None = None, fused=True) -> ParallelResult:
         """Round loop over the loaded trace.  ``truth_inputs``: test hook, truth
-        latencies with the input tensor still gathered (for input capture)."""
+        latencies with the input tensor still gathered (for input capture).
+        ``fused=False`` forces the unfused tensor-core round (separate K1
+        kernel + TMA conv chain) instead of the fused round front (A/B checks)."""
         cfg = self._sim_cfg(pc, sequential=sequential, oracle=oracle or truth_inputs, shard=shard,
-                            profile=profile, truth_inputs=truth_inputs)
+                            profile=profile, truth_inputs=truth_inputs, fused=fused)
         n = self._trace_n if n_total is None else n_total
         k = self._num_sub(pc, n, sequential)
         sb, se = shard if shard is not None else (0, k)

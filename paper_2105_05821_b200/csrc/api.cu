@@ -226,6 +226,12 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
 
   // chunking of the batch (bounds activation memory; results are batch-independent)
   const uint64_t chunk = std::min<uint64_t>(K, 65536);
+  // Fused round front (tensor-core C3): K1 apply + gather + conv chain in one
+  // kernel, the gathered input stays in shared memory.  reserved[2] = 1 forces
+  // the unfused path (ctx_kernel + TMA conv chain), e.g. for A/B checks.
+  const bool fused = !oracle && c->model.tc != nullptr && tc_fused_front(c->model.tc) && cfg.reserved[2] == 0;
+  const bool capture_mode = c->cap_round != UINT32_MAX;
+  const uint32_t dump_stride = input_stride(mc, ILSIM_PREC_FP32);  // fused capture: f32 rows of 100
   // gathered inputs: f32 rows of 100, or (bf16 inference) bf16 rows of 104
   const int xprec = oracle ? ILSIM_PREC_FP32 : c->precision;
   const uint32_t x_stride = needs_input ? input_stride(mc, xprec) : 0;
@@ -233,12 +239,22 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   const bool x_split = !oracle && split_input(c->model);  // 3xTF32 hi/lo planes
   const uint64_t x_lo_off = x_split ? chunk * x_stride : 0;
   const uint64_t x_bytes = chunk * x_stride * input_elem_bytes(xprec) * (x_split ? 2 : 1);
-  void* d_x = needs_input ? c->x.need(x_bytes) : nullptr;
-  if (needs_input) CUDA_OK(cudaMemsetAsync(d_x, 0, x_bytes, c->stream));  // bf16 row padding stays 0
+  void* d_x = nullptr;
+  if (fused) {
+    if (capture_mode) d_x = c->x.need(chunk * dump_stride * sizeof(float));
+  } else if (needs_input) {
+    d_x = c->x.need(x_bytes);
+    CUDA_OK(cudaMemsetAsync(d_x, 0, x_bytes, c->stream));  // bf16 row padding stays 0
+  }
   ForwardBuffers fb{};
   if (!oracle) fb = forward_buffers(c->model, chunk, c->act, c->y);
 
-  auto do_ctx = [&](uint64_t f, uint64_t l, bool gather) {
+  // A "span" is a contiguous range [f, l) of sub-traces whose buffers start at
+  // sample `off` of the chunk buffers, launched on stream `st`.
+  auto x_at = [&](uint64_t off) -> void* {
+    return d_x ? static_cast<void*>(static_cast<char*>(d_x) + off * x_stride * input_elem_bytes(xprec)) : nullptr;
+  };
+  auto do_ctx = [&](uint64_t f, uint64_t l, bool gather, uint64_t off, cudaStream_t st) {
     CtxParams cp{};
     cp.state = d_state;
     cp.proc = d_proc;
@@ -252,7 +268,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     cp.addr = c->addr.as<uint64_t>();
     cp.iflags = c->iflags.as<uint8_t>();
     cp.nc = c->nc_dev.as<NormConsts>();
-    cp.x = d_x;
+    cp.x = x_at(off);
     cp.x_stride = x_stride;
     cp.x_floats = x_floats;
     cp.x_bf16 = xprec == ILSIM_PREC_BF16;
@@ -265,16 +281,16 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     cp.page = cfg.page_size;
     cp.per_cycle = cfg.per_cycle_advance;
     cp.gather = gather && needs_input;
-    launch_ctx(cp, c->stream);
+    launch_ctx(cp, st);
     return uint64_t{1};
   };
-  auto decode_params = [&](uint64_t f, uint64_t l) {
+  auto decode_params = [&](uint64_t f, uint64_t l, const ForwardBuffers& fbs) {
     DecodeParams dp{};
     dp.state = d_state;
     dp.first = f;
     dp.last = l;
-    dp.y = fb.y;
-    dp.y_stride = fb.y_stride;
+    dp.y = fbs.y;
+    dp.y_stride = fbs.y_stride;
     dp.truth = oracle ? c->truth.as<uint32_t>() : nullptr;
     dp.iflags = c->iflags.as<uint8_t>();
     dp.nc = c->nc_dev.as<NormConsts>();
@@ -286,34 +302,67 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     return dp;
   };
   bool k3_fused = false;  // tensor-core tails run K3 themselves
-  auto do_forward = [&](uint64_t f, uint64_t l) -> uint64_t {
-    if (oracle) return 0;
-    const DecodeParams dp = decode_params(f, l);
-    return forward_launch(c->model, c->precision, d_x, x_stride, l - f, fb, c->stream, &dp, &k3_fused, x_lo_off);
+  auto do_front = [&](uint64_t f, uint64_t l, float* dump, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
+    FrontParams fp{};
+    fp.state = d_state;
+    fp.proc = d_proc;
+    fp.wq = d_wq;
+    fp.pmask = pcap - 1;
+    fp.wmask = wcap - 1;
+    fp.first = f;
+    fp.last = l;
+    fp.stat = c->stat.as<float>();
+    fp.pc = c->pc.as<uint64_t>();
+    fp.addr = c->addr.as<uint64_t>();
+    fp.iflags = c->iflags.as<uint8_t>();
+    fp.nc = c->nc_dev.as<NormConsts>();
+    fp.max_context = mc;
+    fp.bw = cfg.retire_bandwidth;
+    fp.line = cfg.line_size;
+    fp.page = cfg.page_size;
+    fp.per_cycle = cfg.per_cycle_advance;
+    fp.dump = dump;
+    fp.dump_stride = dump_stride;
+    return tc_front(c->model, fp, fbs, st);
   };
-  auto do_decode = [&](uint64_t f, uint64_t l) -> uint64_t {
+  auto do_fc = [&](uint64_t f, uint64_t l, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
+    const DecodeParams dp = decode_params(f, l, fbs);
+    k3_fused = true;
+    return tc_fc(c->model, fbs.act[2], l - f, fbs, st, &dp);
+  };
+  auto do_forward = [&](uint64_t f, uint64_t l, uint64_t off, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
+    if (oracle) return 0;
+    const DecodeParams dp = decode_params(f, l, fbs);
+    return forward_launch(c->model, c->precision, x_at(off), x_stride, l - f, fbs, st, &dp, &k3_fused, x_lo_off);
+  };
+  auto do_decode = [&](uint64_t f, uint64_t l, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
     if (k3_fused) return 0;
-    launch_decode(decode_params(f, l), c->stream);
+    launch_decode(decode_params(f, l, fbs), st);
     return 1;
   };
-  auto launch_round = [&]() -> uint64_t {
-    uint64_t launches = 0;
-    for (uint64_t f = 0; f < K; f += chunk) {
-      const uint64_t l = std::min(K, f + chunk);
-      launches += do_ctx(f, l, true);
-      launches += do_forward(f, l);
-      launches += do_decode(f, l);
+  // one round of one span: K1 -> K2 -> K3 (fused: front -> FC)
+  auto run_span = [&](uint64_t f, uint64_t l, uint64_t off, cudaStream_t st) -> uint64_t {
+    const ForwardBuffers fbs = oracle ? fb : fb_slice(c->model, fb, off);
+    if (fused) {
+      static const int ko = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
+      return ((ko & 8) ? 0 : do_front(f, l, nullptr, fbs, st)) + ((ko & 4) ? 0 : do_fc(f, l, fbs, st));
     }
+    return do_ctx(f, l, true, off, st) + do_forward(f, l, off, fbs, st) + do_decode(f, l, fbs, st);
+  };
+
+  auto launch_rounds = [&](uint32_t reps) -> uint64_t {
+    uint64_t launches = 0;
+    for (uint32_t r = 0; r < reps; ++r)
+      for (uint64_t f = 0; f < K; f += chunk) launches += run_span(f, std::min(K, f + chunk), 0, c->stream);
     return launches;
   };
 
-  const bool capture_mode = c->cap_round != UINT32_MAX;
   if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
-  if (capture_mode && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
+  if (capture_mode && !fused && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
   const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs
   constexpr uint32_t kGraphRounds = 16;
   cudaGraphExec_t g1 = nullptr, gN = nullptr;
-  uint64_t launches_per_round = 0;
+  uint64_t launches_1 = 0, launches_n = 0;
   if (!capture_mode && !profile) {
     for (int which = 0; which < 2; ++which) {
       const uint32_t reps = which == 0 ? 1 : kGraphRounds;
@@ -321,7 +370,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
       cudaGraph_t g = nullptr;
       CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       try {
-        for (uint32_t r = 0; r < reps; ++r) launches_per_round = launch_round();
+        (which == 0 ? launches_1 : launches_n) = launch_rounds(reps);
       } catch (...) {
         cudaStreamEndCapture(c->stream, &g);  // leave the stream usable
         if (g) cudaGraphDestroy(g);
@@ -342,18 +391,25 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     for (uint32_t r = 0; r < rounds; ++r) {
       for (uint64_t f = 0; f < K; f += chunk) {
         const uint64_t l = std::min(K, f + chunk);
+        const bool cap_now = capture_mode && r == c->cap_round && needs_input;
         if (profile) CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
-        launches += do_ctx(f, l, true);
+        if (fused) {
+          if (cap_now) CUDA_OK(cudaMemsetAsync(d_x, 0, chunk * dump_stride * sizeof(float), c->stream));
+          launches += do_front(f, l, cap_now ? static_cast<float*>(d_x) : nullptr, fb, c->stream);
+        } else {
+          launches += do_ctx(f, l, true, 0, c->stream);
+        }
         if (profile) CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
-        if (capture_mode && r == c->cap_round && needs_input) {
+        if (cap_now) {
           const uint32_t width = static_cast<uint32_t>(kSlots * (mc + 1));
           const uint64_t rows = std::min<uint64_t>(c->cap_rows, l - f);
-          CUDA_OK(cudaMemcpy2DAsync(c->cap_host, width * sizeof(float), d_x, x_stride * sizeof(float),
+          const uint32_t pitch = fused ? dump_stride : x_stride;
+          CUDA_OK(cudaMemcpy2DAsync(c->cap_host, width * sizeof(float), d_x, pitch * sizeof(float),
                                     width * sizeof(float), rows, cudaMemcpyDeviceToHost, c->stream));
         }
-        launches += do_forward(f, l);
+        launches += fused ? do_fc(f, l, fb, c->stream) : do_forward(f, l, 0, fb, c->stream);
         if (profile) CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
-        launches += do_decode(f, l);
+        launches += do_decode(f, l, fb, c->stream);
         if (profile) {
           CUDA_OK(cudaEventRecord(c->ev[5], c->stream));
           CUDA_OK(cudaEventSynchronize(c->ev[5]));
@@ -371,12 +427,15 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     uint32_t r = 0;
     while (gN && r + kGraphRounds <= rounds) {
       CUDA_OK(cudaGraphLaunch(gN, c->stream));
+      launches += launches_n;
       r += kGraphRounds;
     }
-    for (; r < rounds; ++r) CUDA_OK(cudaGraphLaunch(g1, c->stream));
-    launches += launches_per_round * rounds;
+    for (; r < rounds; ++r) {
+      CUDA_OK(cudaGraphLaunch(g1, c->stream));
+      launches += launches_1;
+    }
   }
-  for (uint64_t f = 0; f < K; f += chunk) launches += do_ctx(f, std::min(K, f + chunk), false);  // apply final step, drain
+  for (uint64_t f = 0; f < K; f += chunk) launches += do_ctx(f, std::min(K, f + chunk), false, 0, c->stream);  // apply final step, drain
   CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
   CUDA_OK(cudaGetLastError());
   CUDA_OK(cudaEventSynchronize(c->ev[1]));
@@ -401,7 +460,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     if (st.status == kErrWriteRing)
       throw ApiError("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
                      std::to_string(i) + "; raise write_ring");
-    if (st.pos != st.len) throw ApiError("internal: sub-trace did not finish");
+    if (st.pos != st.len && !std::getenv("SIMNET_KNOCKOUT")) throw ApiError("internal: sub-trace did not finish");
     ilsim_sub_result& r = subs[j];
     r.instructions = st.len - st.warm;
     r.total_cycles = st.cur - st.base_cur;

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "conv_chain.cuh"
+#include "round_front.cuh"
 #include "decode.cuh"
 #include "tc_common.cuh"
 #include "launch.cuh"
@@ -545,6 +546,9 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CUDA_OK(cudaFuncSetAttribute(fc_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   conv_chain_set_attributes();
+  round_front_set_attributes();
+  if (std::getenv("SIMNET_CHAIN_TRACE") && !chain_trace_ptr())  // diagnostics buffer, allocated outside capture
+    CUDA_OK(cudaMalloc(&chain_trace_ptr(), 148 * 32 * sizeof(long long)));
   auto* t = new TcModel();
   t->mode = mode;
   t->chain = c.n_conv == 3 && c.conv[0] == 64 && c.conv[1] == 64 && c.conv[2] == 64 && c.input_channels == 50 &&
@@ -587,6 +591,97 @@ void tc_prepare(const DevModel& m, uint64_t samples) {
 }
 
 bool tc_split_input(const TcModel* t) { return t->chain && t->mode == kTF32x3; }
+uint32_t tc_act_bytes(const TcModel* t) { return t->mode == kBF16 ? 2u : 4u; }
+
+// FC1 (split-K tcgen05 partials) and the FC tail (FC2 + fused K3) on the
+// flat conv output `in`.
+uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
+               const DecodeParams* fuse) {
+  if (!m.tc) throw ApiError("internal: tensor-core model missing");
+  TcModel& t = *m.tc;
+  const ilsim_cnn_config& c = m.cfg;
+  const int mode = t.mode;
+  const bool bf = mode == kBF16;
+  const int esz = bf ? 2 : 4;
+  const int chunk_elems = bf ? 64 : 32;
+  const float* P = m.params.as<float>();
+  uint64_t launches = 0;
+  // FC1 split-K partials
+  const int flat = m.L.flat;
+  const int total_chunks = (flat * esz + 127) / 128;
+  const int per = kMaxChunks;
+  const int nsplit = (total_chunks + per - 1) / per;
+  const int fc_tile = t.fc1.npad >= 64 ? 64 : t.fc1.npad;
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(flat), samples};
+    const uint64_t strides[1] = {static_cast<uint64_t>(flat) * esz};
+    const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
+    const CUtensorMap amap = make_map(in, bf, 2, dims, strides, box);
+    const uint64_t plane = samples * static_cast<uint64_t>(c.fc_hidden);
+    // this slice's own [nsplit][samples][hidden] block (slices run concurrently)
+    const uint64_t base = fb.part_off * nsplit * static_cast<uint64_t>(c.fc_hidden);
+    if (t.part.bytes < (base + plane * nsplit) * sizeof(float)) throw ApiError("internal: split-K buffer not prepared");
+    float* part = t.part.as<float>() + base;
+    TcGemmParams p{};
+    p.m = static_cast<int>(samples);
+    p.m_tiles = static_cast<int>((samples + kBM - 1) / kBM);
+    p.n = fc_tile;
+    p.chunks = per;
+    p.ksteps_last = 4;
+    p.bias = nullptr;
+    p.relu = 0;
+    p.out = part;
+    p.ldo = c.fc_hidden;
+    p.out_bf16 = 0;
+    p.out_split_stride = plane;
+    if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
+    if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
+    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
+    ++launches;
+    const int od = m.L.out_dim;
+    if (od > kMaxOut || c.fc_hidden % 4 != 0)
+      throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
+    const size_t tail_smem =
+        (static_cast<size_t>(od) * (c.fc_hidden + 4) + kTailSamples * c.fc_hidden + kTailSamples * kMaxOut) * 4;
+    TailParams tp{};
+    tp.part = part;
+    tp.nsplit = nsplit;
+    tp.split_stride = plane;
+    tp.hidden = c.fc_hidden;
+    tp.b1 = P + m.L.fc1_b;
+    tp.w2t = t.w2t.as<float>();
+    tp.b2 = P + m.L.fc2_b;
+    tp.od = od;
+    tp.y = fb.y;
+    tp.samples = static_cast<int>(samples);
+    if (fuse) tp.dec = *fuse;
+    launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
+               dim3(kTailThreads), tail_smem, s, tp);
+    ++launches;
+  }
+  return launches;
+}
+
+bool tc_fused_front(const TcModel* t) { return t != nullptr && t->chain; }
+
+// Fused round front (K1 apply + gather + conv chain) for the chunk of
+// sub-traces [fp.first, fp.last); writes the flat conv2 output to fb.act[2].
+uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, cudaStream_t s) {
+  TcModel& t = *m.tc;
+  if (!t.chain) throw ApiError("internal: fused round front needs the C3 conv chain");
+  const float* P = m.params.as<float>();
+  fp.b0 = P + m.L.b[0];
+  fp.b1 = P + m.L.b[1];
+  fp.b2 = P + m.L.b[2];
+  fp.out = fb.act[2];
+  const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
+                            t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
+  fp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
+  static const int knockout = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
+  fp.knockout = knockout;
+  launch_round_front(t.mode, w, fp, num_sms(), s);
+  return 1;
+}
 
 uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_stride, uint64_t samples,
                     const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse, uint64_t x_lo_off) {
@@ -617,12 +712,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
                               t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
     ChainParams cp{static_cast<int>(samples), P + m.L.b[0], P + m.L.b[1], P + m.L.b[2], fb.act[2], nullptr};
-    static long long* trace_buf = nullptr;  // SIMNET_CHAIN_TRACE: event clocks of the last launch
-    if (std::getenv("SIMNET_CHAIN_TRACE")) {
-      if (!trace_buf) CUDA_OK(cudaMalloc(&trace_buf, 148 * 32 * sizeof(long long)));
-      cp.trace = trace_buf;
-      chain_trace_ptr() = trace_buf;
-    }
+    cp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE diagnostics (null: off)
     launch_conv_chain(mode, xmap, xlo, w, cp, num_sms(), s);
     ++launches;
     in = fb.act[2];
@@ -667,58 +757,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     cin = cout;
     len = olen;
   }
-  // FC1 split-K partials
-  const int flat = m.L.flat;
-  const int total_chunks = (flat * esz + 127) / 128;
-  const int per = kMaxChunks;
-  const int nsplit = (total_chunks + per - 1) / per;
-  const int fc_tile = t.fc1.npad >= 64 ? 64 : t.fc1.npad;
-  {
-    const uint64_t dims[2] = {static_cast<uint64_t>(flat), samples};
-    const uint64_t strides[1] = {static_cast<uint64_t>(flat) * esz};
-    const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
-    const CUtensorMap amap = make_map(in, bf, 2, dims, strides, box);
-    const uint64_t plane = samples * static_cast<uint64_t>(c.fc_hidden);
-    if (t.part.bytes < plane * nsplit * sizeof(float)) throw ApiError("internal: split-K buffer not prepared");
-    float* part = t.part.as<float>();
-    TcGemmParams p{};
-    p.m = static_cast<int>(samples);
-    p.m_tiles = static_cast<int>((samples + kBM - 1) / kBM);
-    p.n = fc_tile;
-    p.chunks = per;
-    p.ksteps_last = 4;
-    p.bias = nullptr;
-    p.relu = 0;
-    p.out = part;
-    p.ldo = c.fc_hidden;
-    p.out_bf16 = 0;
-    p.out_split_stride = plane;
-    if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
-    if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
-    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
-    ++launches;
-    const int od = m.L.out_dim;
-    if (od > kMaxOut || c.fc_hidden % 4 != 0)
-      throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
-    const size_t tail_smem =
-        (static_cast<size_t>(od) * (c.fc_hidden + 4) + kTailSamples * c.fc_hidden + kTailSamples * kMaxOut) * 4;
-    TailParams tp{};
-    tp.part = part;
-    tp.nsplit = nsplit;
-    tp.split_stride = plane;
-    tp.hidden = c.fc_hidden;
-    tp.b1 = P + m.L.fc1_b;
-    tp.w2t = t.w2t.as<float>();
-    tp.b2 = P + m.L.fc2_b;
-    tp.od = od;
-    tp.y = fb.y;
-    tp.samples = static_cast<int>(samples);
-    if (fuse) tp.dec = *fuse;
-    launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
-               dim3(kTailThreads), tail_smem, s, tp);
-    ++launches;
-  }
-  return launches;
+  return launches + tc_fc(m, in, samples, fb, s, fuse);
 }
 
 }  // namespace simnet

@@ -158,7 +158,24 @@ ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, D
   fb.y_stride = static_cast<uint32_t>(m.L.out_dim);
   fb.y = static_cast<float*>(y.need(chunk * fb.y_stride * sizeof(float)));
   if (m.tc) tc_prepare(m, chunk);
+  fb.act_esz = m.tc ? tc_act_bytes(m.tc) : 4u;
+  fb.part_off = 0;
   return fb;
+}
+
+ForwardBuffers fb_slice(const DevModel& m, const ForwardBuffers& fb, uint64_t off) {
+  const ilsim_cnn_config& c = m.cfg;
+  ForwardBuffers s = fb;
+  int len = c.sequence_length;
+  for (int l = 0; l < c.n_conv; ++l) {
+    len /= 2;
+    const uint64_t bytes = off * static_cast<uint64_t>(len) * c.conv[l] * fb.act_esz;
+    s.act[l] = reinterpret_cast<float*>(reinterpret_cast<char*>(fb.act[l]) + bytes);
+  }
+  s.act[c.n_conv] = fb.act[c.n_conv] + off * static_cast<uint64_t>(c.fc_hidden);
+  s.y = fb.y + off * fb.y_stride;
+  s.part_off = fb.part_off + off;
+  return s;
 }
 
 uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32_t x_stride,

@@ -7,6 +7,7 @@
 
 #include "../../include/ilsim_gpu.h"
 #include "host_util.cuh"
+#include "round_front.cuh"
 #include "sim_kernels.cuh"
 
 namespace simnet {
@@ -54,11 +55,16 @@ struct ForwardBuffers {
   float* act[9];       // conv outputs (act[0..n_conv-1]), hidden (act[n_conv])
   float* y;            // head outputs
   uint32_t y_stride;
+  uint32_t act_esz;    // bytes per conv activation element (2: bf16 tensor-core path)
+  uint64_t part_off;   // first sample of this slice in the split-K partial buffer
 };
 
 void model_upload(DevModel& m, const ilsim_cnn_config& c, const float* params, int precision,
                   cudaStream_t s);
 ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, DevBuf& y);
+// The buffers of samples [off, ...) of a chunk: concurrent sub-trace groups
+// each work on their own slice.
+ForwardBuffers fb_slice(const DevModel& m, const ForwardBuffers& fb, uint64_t off);
 // Runs the forward for `samples` gathered rows; returns kernels launched.
 // With `fuse`, the tensor-core path also performs K3 (decode + clock) in its
 // tail and returns true in *fused.
@@ -77,5 +83,14 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
                     uint64_t samples, const ForwardBuffers& fb, cudaStream_t s, const DecodeParams* fuse,
                     uint64_t x_lo_off);
 bool tc_split_input(const TcModel* t);
+uint32_t tc_act_bytes(const TcModel* t);
+// Fused round front available (C3 chain on the tensor-core path).
+bool tc_fused_front(const TcModel* t);
+// K1 apply + gather + conv chain in one kernel (round_front.cu); the K1
+// fields of fp are the caller's, the conv fields are filled in here.
+uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, cudaStream_t s);
+// FC1 + FC tail (+ fused K3 when fuse != null) on the flat conv output.
+uint64_t tc_fc(const DevModel& m, const void* flat, uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
+               const DecodeParams* fuse);
 
 }  // namespace simnet

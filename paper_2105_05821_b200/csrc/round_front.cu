@@ -1,0 +1,574 @@
+// Fused round front = K1 + the conv chain of K2, one kernel per round.
+//
+// Per work item (8 sub-traces), in one CTA:
+//   1. apply   — warp w applies the pending step of sub-trace w (retire /
+//                stall / push / drain, simcore.cpp:112-159) and builds its
+//                context-column table (next_request, simcore.cpp:25-66):
+//                instruction index + the 9 dynamic slots, newest first.
+//   2. gather  — the 256 compute threads write the normalised input straight
+//                into the conv0 A operand (K-major SWIZZLE_128B, 3xTF32 hi/lo
+//                planes or bf16) in shared memory.  conv0 tiles are
+//                row-major over (sample, row-of-two-columns): tile t holds rows
+//                16t..16t+15 of all 8 samples, so a tile beyond every
+//                sample's context is all zeros and is skipped: its conv0
+//                output is exactly ReLU(b0) (a zero row accumulates exactly 0).
+//   3. conv0 -> conv1 -> conv2 on tcgen05 with TMEM accumulators and the
+//                epilogue restaging each layer's output as the next A operand
+//                (cnn.cpp:90-110), as in conv_chain.cu.  Only the final conv2
+//                activations (4 KB / sample) leave the SM.
+// Per-row results are identical to the unfused path (ctx_kernel + TMA
+// conv_chain_kernel): every accumulator row depends only on its own A row.
+//
+//   TMEM (f32 columns): conv0 4 x 64 [0,256) | conv1 2 x 64 [256,384) | conv2 [384,448)
+//   SMEM: R1 128 KB  conv0 A tile (hi | lo) / restaged conv1 / conv2 A tile
+//         R2  64 KB  current layer's weights (hi | lo), TMA
+//         T   20 KB  column tables
+//   warps 0-7   compute: apply, gather, epilogue (TMEM lane quarter w%4)
+//   warp 8      TMA producer (weights)
+//   warp 9      TMEM allocator + tcgen05.mma issuer
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "k1_device.cuh"
+#include "launch.cuh"
+#include "round_front.cuh"
+#include "tc_common.cuh"
+
+namespace simnet {
+
+namespace {
+
+constexpr int kItem = 8;      // sub-traces per work item
+constexpr int kC = 64;        // channels of every conv layer (C3)
+constexpr int kRowsT = 16;    // conv0 rows per sample per tile
+constexpr int kTblCols = 128; // max columns (max_context + 1)
+constexpr uint32_t kR1 = 128 * 1024;
+constexpr uint32_t kR2 = 64 * 1024;
+constexpr uint32_t kTbl = kItem * kTblCols * (4 + 16);
+constexpr int kThreadsRF = 320;
+constexpr int kCompute = 256;
+
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// byte offset of f32 element (row r, k) in a K-major SW128 tile of 128 rows
+// whose K extent is split into chunk-major 128-byte chunks of 32 floats.
+__device__ __forceinline__ uint32_t sw128_f32(int r, int k) {
+  const int chunk = k >> 5, kk = k & 31;
+  return chunk * (128 * 128) + r * 128 + ((((kk >> 2) ^ (r & 7)) << 4) | ((kk & 3) << 2));
+}
+// bf16 element (row r, k), 64 elements per chunk
+__device__ __forceinline__ uint32_t sw128_bf16(int r, int k) {
+  const int chunk = k >> 6, kk = k & 63;
+  return chunk * (128 * 128) + r * 128 + ((((kk >> 3) ^ (r & 7)) << 4) | ((kk & 7) << 1));
+}
+
+template <int kMode>
+struct Shape {
+  static constexpr bool kSplit = kMode == kTF32x3;
+  static constexpr int kElems = kMode == kBF16 ? 64 : 32;   // elements per 128 B chunk
+  static constexpr int kK0Chunks = kMode == kBF16 ? 2 : 4;  // conv0 K = 100 (+pad)
+  static constexpr int kK0Steps = kMode == kBF16 ? 7 : 13;  // 32 B k-steps covering K = 100
+  static constexpr int kPadUnits = kMode == kBF16 ? 6 : 2;  // float2 units of zeros after K = 100
+  static constexpr int kKChunks = kMode == kBF16 ? 2 : 4;   // conv1/2 K = 128
+  static constexpr uint32_t kWBytes = kC * 128 * kKChunks;  // one weight copy (hi or lo)
+  static constexpr uint32_t kStage = 128 * 128;             // one A chunk (128 rows x 128 B)
+  static constexpr uint32_t kALo = kKChunks * kStage;       // lo plane of a restaged A
+  static constexpr uint32_t kA0Lo = 4 * kStage;             // lo plane of the conv0 A tile
+};
+
+// Store the float pair (v0, v1) of A row r at K offset k (even) into the
+// operand planes: 3xTF32 hi = cvt.rna, lo = v - hi (exact); tf32 plain; bf16 rn.
+template <int kMode>
+__device__ __forceinline__ void put2(uint8_t* a, uint32_t lo_off, int r, int k, float v0, float v1) {
+  if constexpr (kMode == kBF16) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
+    *reinterpret_cast<__nv_bfloat162*>(a + sw128_bf16(r, k)) = b;
+  } else {
+    const uint32_t o = sw128_f32(r, k);
+    if constexpr (kMode == kTF32x3) {
+      const float h0 = __uint_as_float((__float_as_uint(v0) + 0x1000u) & 0xffffe000u);
+      const float h1 = __uint_as_float((__float_as_uint(v1) + 0x1000u) & 0xffffe000u);
+      *reinterpret_cast<float2*>(a + o) = make_float2(h0, h1);
+      *reinterpret_cast<float2*>(a + lo_off + o) = make_float2(v0 - h0, v1 - h1);
+    } else {
+      *reinterpret_cast<float2*>(a + o) = make_float2(v0, v1);
+    }
+  }
+}
+
+// Four floats of A row r at K offset k (multiple of 4): one 16-B store per plane.
+template <int kMode>
+__device__ __forceinline__ void put4(uint8_t* a, uint32_t lo_off, int r, int k, float v0, float v1, float v2,
+                                     float v3) {
+  if constexpr (kMode == kBF16) {
+    put2<kMode>(a, lo_off, r, k, v0, v1);
+    put2<kMode>(a, lo_off, r, k + 2, v2, v3);
+  } else {
+    const uint32_t o = sw128_f32(r, k);
+    if constexpr (kMode == kTF32x3) {
+      float4 hi;
+      hi.x = __uint_as_float((__float_as_uint(v0) + 0x1000u) & 0xffffe000u);
+      hi.y = __uint_as_float((__float_as_uint(v1) + 0x1000u) & 0xffffe000u);
+      hi.z = __uint_as_float((__float_as_uint(v2) + 0x1000u) & 0xffffe000u);
+      hi.w = __uint_as_float((__float_as_uint(v3) + 0x1000u) & 0xffffe000u);
+      *reinterpret_cast<float4*>(a + o) = hi;
+      *reinterpret_cast<float4*>(a + lo_off + o) = make_float4(v0 - hi.x, v1 - hi.y, v2 - hi.z, v3 - hi.w);
+    } else {
+      *reinterpret_cast<float4*>(a + o) = make_float4(v0, v1, v2, v3);
+    }
+  }
+}
+
+// Restage 64 accumulator columns of TMEM lane-row `tl` (one conv output row;
+// `constant`: a skipped all-zero row, accumulator exactly 0) into the A
+// operand at row `ar`, K offset `k0`, with bias + ReLU.
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+template <int kMode>
+__device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, bool constant, int ar, int k0,
+                                            const float* bias) {
+  using S = Shape<kMode>;
+  uint32_t raw[kC];
+  if (constant) {
+#pragma unroll
+    for (int i = 0; i < kC; ++i) raw[i] = 0u;
+  } else {  // all four 16-column loads in flight, one wait
+#pragma unroll
+    for (int c0 = 0; c0 < kC; c0 += 16) tmem_ld16_async(tl + c0, raw + c0);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  }
+#pragma unroll
+  for (int c0 = 0; c0 < kC; c0 += 16) {
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaxf(__uint_as_float(raw[c0 + i]) + bias[c0 + i], 0.0f);
+    if constexpr (kMode == kBF16) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint4 pk;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * h + 2 * i], v[8 * h + 2 * i + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        const int k = k0 + c0 + 8 * h;
+        const int chunk = k >> 6, kk = k & 63;
+        *reinterpret_cast<uint4*>(a + chunk * (128 * 128) + ar * 128 + (((kk >> 3) ^ (ar & 7)) << 4)) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + c0 + 4 * q;
+        float4 hi;
+        if constexpr (S::kSplit) {
+          uint32_t u[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) u[i] = (__float_as_uint(v[4 * q + i]) + 0x1000u) & 0xffffe000u;
+          hi = make_float4(__uint_as_float(u[0]), __uint_as_float(u[1]), __uint_as_float(u[2]), __uint_as_float(u[3]));
+          const float4 lo = make_float4(v[4 * q] - hi.x, v[4 * q + 1] - hi.y, v[4 * q + 2] - hi.z, v[4 * q + 3] - hi.w);
+          *reinterpret_cast<float4*>(a + S::kALo + sw128_f32(ar, k)) = lo;
+        } else {
+          hi = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        *reinterpret_cast<float4*>(a + sw128_f32(ar, k)) = hi;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+template <int kMode>
+__global__ void __launch_bounds__(kThreadsRF, 1)
+round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW0lo,
+                   const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW1lo,
+                   const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW2lo,
+                   FrontParams p) {
+  using S = Shape<kMode>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* R1 = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
+  uint8_t* R2 = R1 + kR1;
+  uint32_t* tbl_inst = reinterpret_cast<uint32_t*>(R2 + kR2);                // [kItem][kTblCols]
+  float4* tbl_dyn = reinterpret_cast<float4*>(tbl_inst + kItem * kTblCols);  // [kItem][kTblCols]
+  // One barrier per event kind; each waiter consumes every completion in order.
+  __shared__ __align__(8) uint64_t bar_w[3];       // layer weights landed (TMA tx), 1 / item
+  __shared__ __align__(8) uint64_t bar_a0, bar_t0; // conv0 tile gathered (256) / its MMAs done: T / item
+  __shared__ __align__(8) uint64_t bar_c0;         // all conv0 MMAs done (W0 + conv0 A free), 1 / item
+  __shared__ __align__(8) uint64_t bar_a1, bar_m1; // conv1 A restaged / its MMAs done: 2 / item
+  __shared__ __align__(8) uint64_t bar_w1f;        // conv1 MMAs done (W1 free), 1 / item
+  __shared__ __align__(8) uint64_t bar_a2, bar_m2; // conv2 A restaged / MMAs done: 1 / item
+  __shared__ uint32_t tmem_slot;
+  __shared__ float sbias[3][kC];
+  __shared__ float s_zero[kSlots], s_one[kSlots];
+  __shared__ int s_ncols[kItem];  // context columns of each sample this round, -1: inactive
+  __shared__ int s_T;             // conv0 tiles needed this item
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t samples = p.last - p.first;
+  const int n_items = static_cast<int>((samples + kItem - 1) / kItem);
+  // PDL: the FC kernels may launch now (their prologue only touches weights);
+  // this kernel's prologue (barriers, TMEM, biases, W0) overlaps the previous
+  // round's tail, and only the compute warps wait for its results.
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x < 3 * kC) {
+    const int l = threadIdx.x / kC, c = threadIdx.x % kC;
+    sbias[l][c] = (l == 0 ? p.b0 : (l == 1 ? p.b1 : p.b2))[c];
+  } else if (threadIdx.x < 3 * kC + kSlots) {
+    const int k = threadIdx.x - 3 * kC;
+    s_zero[k] = p.nc->zero[k];
+    s_one[k] = p.nc->one[k];
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bar_w[i], 1);
+    mbar_init(&bar_a0, kCompute);
+    mbar_init(&bar_t0, 1);
+    mbar_init(&bar_c0, 1);
+    mbar_init(&bar_a1, kCompute);
+    mbar_init(&bar_m1, 1);
+    mbar_init(&bar_w1f, 1);
+    mbar_init(&bar_a2, kCompute);
+    mbar_init(&bar_m2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 8) {
+    // ---------------- TMA producer: layer weights ----------------
+    if (lane == 0) {
+      auto load_w = [&](int layer, const CUtensorMap* hi, const CUtensorMap* lo, int chunks) {
+        uint64_t* b = &bar_w[layer];
+        mbar_expect_tx(b, S::kWBytes * (S::kSplit ? 2u : 1u) / S::kKChunks * chunks);
+        for (int c = 0; c < chunks; ++c) {
+          tma_load_2d(R2 + c * (kC * 128), hi, b, c * S::kElems, 0);
+          if (S::kSplit) tma_load_2d(R2 + S::kWBytes + c * (kC * 128), lo, b, c * S::kElems, 0);
+        }
+      };
+      int it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(&bar_m2, (it - 1) & 1);  // previous conv2 done: R2 free
+        load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
+        mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
+        load_w(1, &tmW1, &tmW1lo, S::kKChunks);
+        mbar_wait(&bar_w1f, it & 1);  // conv1 MMAs done: W1 no longer read
+        load_w(2, &tmW2, &tmW2lo, S::kKChunks);
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, kC);
+      const uint32_t r1 = su32(R1), r2 = su32(R2);
+      uint32_t n_a0 = 0;
+      int it = 0;
+      auto gemm = [&](uint32_t d, uint32_t alo, int ksteps) {  // A in R1 (lo plane at +alo), W in R2
+        for (int s = 0; s < ksteps; ++s) {
+          const int c = s >> 2, j = s & 3;
+          const uint32_t ao = c * S::kStage + j * 32, wo = c * (kC * 128) + j * 32;
+          const uint64_t ad = smem_desc_sw128(r1 + ao), bd = smem_desc_sw128(r2 + wo);
+          if (S::kSplit) {
+            mma<kMode>(d, smem_desc_sw128(r1 + alo + ao), bd, idesc, s > 0);
+            mma<kMode>(d, ad, smem_desc_sw128(r2 + S::kWBytes + wo), idesc, 1);
+            mma<kMode>(d, ad, bd, idesc, 1);
+          } else {
+            mma<kMode>(d, ad, bd, idesc, s > 0);
+          }
+        }
+      };
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        // conv0: T tiles of 128 rows (8 samples x 16 rows), gathered by the compute warps
+        mbar_wait(&bar_a0, n_a0++ & 1);
+        const int T = s_T;  // written before the first bar_a0 arrival of this item
+        mbar_wait(&bar_w[0], it & 1);
+        tc_fence_after();
+        for (int t = 0; t < T; ++t) {
+          if (t > 0) {
+            mbar_wait(&bar_a0, n_a0++ & 1);
+            tc_fence_after();
+          }
+          gemm(tmem + t * kC, S::kA0Lo, S::kK0Steps);
+          mma_commit(&bar_t0);
+        }
+        mma_commit(&bar_c0);
+        // conv1: two tiles (16 positions x 8 samples each), A restaged by the epilogue
+        for (int u = 0; u < 2; ++u) {
+          mbar_wait(&bar_a1, u);
+          if (u == 0) mbar_wait(&bar_w[1], it & 1);
+          tc_fence_after();
+          gemm(tmem + 256 + u * kC, S::kALo, 4 * S::kKChunks);
+          mma_commit(&bar_m1);
+        }
+        mma_commit(&bar_w1f);
+        // conv2: one tile of 128 rows (8 samples x 16 positions)
+        mbar_wait(&bar_a2, it & 1);
+        mbar_wait(&bar_w[2], it & 1);
+        tc_fence_after();
+        gemm(tmem + 384, S::kALo, 4 * S::kKChunks);
+        mma_commit(&bar_m2);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- compute warps 0-7 ----------------
+    const int tid = threadIdx.x;  // 0..255
+    const int quad = warp & 3, half = warp >> 2;
+    const int m = quad * 32 + lane;  // TMEM lane owned by this thread
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const k1::ApplyArgs aa{p.bw, p.max_context, p.per_cycle, 1, p.iflags, p.nc};
+    const NormConsts& nc = *p.nc;
+    uint32_t n_t0 = 0;
+    int it = 0;
+    long long* tr = p.trace ? p.trace + blockIdx.x * 32 : nullptr;
+    // diagnostics: phase-boundary clocks of the first item, taken after a
+    // barrier of the compute warps so a mark means "all of them are done"
+    auto mark = [&](int i) {
+      if (tr && it == 0) {
+        compute_sync();
+        if (tid == 0) tr[i] = clock64();
+      }
+    };
+    mark(0);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // SubState / rings of the previous round
+    if (tr && tid == 0) tr[15] = clock64();
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      // ---- 1. apply + column table: warp w owns sub-trace item*8 + w ----
+      {
+        const uint64_t s = p.first + static_cast<uint64_t>(item) * kItem + warp;
+        int ncs = -1;
+        if (s < p.last) {
+          const k1::Rings r = k1::rings_of(p.proc, p.wq, p.pmask, p.wmask, s);
+          SubState* sp = p.state + s;
+          SubState st = *sp;
+          if (st.status == kOk && st.has_pend && !(p.knockout & 2)) {
+            k1::apply_step(st, r, aa);
+            if (lane == 0) *sp = st;
+            __syncwarp();
+          }
+          if (tr && it == 0 && lane == 0) tr[16 + warp] = clock64();  // per-warp apply done
+          if (st.status == kOk && st.pos < st.len) {
+            const uint64_t tgt = st.begin + st.pos;
+            const uint32_t ncols = min(static_cast<uint32_t>(p.max_context), (st.pt - st.ph) + (st.wt - st.wh));
+            const uint64_t tpc = p.pc[tgt], taddr = p.addr[tgt];
+            const uint8_t tfl = p.iflags[tgt];
+            const bool tmemop = (tfl & kFlagMem) != 0;
+            uint32_t* ti = tbl_inst + warp * kTblCols;
+            float4* td = tbl_dyn + warp * kTblCols;
+            for (uint32_t c = lane; c <= ncols; c += 32) {
+              if (c == 0) {
+                ti[0] = static_cast<uint32_t>(tgt);
+                td[0] = make_float4(s_zero[kSlotResidence], s_zero[kSlotExecution], s_zero[kSlotStore], 0.0f);
+                continue;
+              }
+              const RingEntry e = k1::context_entry(st, r, c - 1);
+              const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e.push));
+              const uint32_t f = k1::dep_flags(tpc, taddr, tmemop, e, p.line, p.page);
+              ti[c] = static_cast<uint32_t>(st.begin + e.idx);
+              td[c] = make_float4(norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]), e.nexec, e.nstore,
+                                  __uint_as_float(f));
+            }
+            if (lane == 0) {  // the next round's push carries these into the ring entry
+              sp->xcols = ncols + 1;
+              sp->t_pc = tpc;
+              sp->t_addr = taddr;
+              sp->t_flags = tfl;
+            }
+            ncs = static_cast<int>(ncols);
+          }
+        }
+        if (lane == 0) s_ncols[warp] = ncs;
+      }
+      compute_sync();
+      mark(1);
+      int T = 1;  // conv0 tiles with any non-zero row (rows of 2 columns: ceil((ncols + 1) / 2))
+#pragma unroll
+      for (int w = 0; w < kItem; ++w) {
+        const int rows = (s_ncols[w] + 2) >> 1;
+        T = max(T, (rows + kRowsT - 1) / kRowsT);
+      }
+      if (tid == 0) s_T = T;
+
+      // ---- 2. gather conv0 tiles straight into the A operand ----
+      // Thread = (sample `warp`, column 32t + lane): one A half-row (50 slots of
+      // one context column) per thread per tile: 11 float4 static-slot loads in
+      // flight, the 9 dynamic slots from the column table, 16-B stores.
+      for (int t = 0; t < T; ++t) {
+        if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);  // conv0 MMAs of tile t-1 done reading R1
+        const int col = 32 * t + lane;
+        const int r = warp * kRowsT + (lane >> 1), h = lane & 1;
+        const bool live = col <= s_ncols[warp];
+        float v[kSlots];
+        {
+          float4 q[11];
+          const float4* srow = reinterpret_cast<const float4*>(
+              p.stat + static_cast<uint64_t>(live ? tbl_inst[warp * kTblCols + col] : 0u) * kStatStride);
+#pragma unroll
+          for (int i = 0; i < 11; ++i) q[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (live && !(p.knockout & 1)) {
+#pragma unroll
+            for (int i = 0; i < 11; ++i) q[i] = __ldg(srow + i);
+          }
+#pragma unroll
+          for (int i = 0; i < 10; ++i) {
+            v[4 * i] = q[i].x;
+            v[4 * i + 1] = q[i].y;
+            v[4 * i + 2] = q[i].z;
+            v[4 * i + 3] = q[i].w;
+          }
+          v[40] = q[10].x;
+          const float4 d = tbl_dyn[warp * kTblCols + (live ? col : 0)];
+          const uint32_t f = __float_as_uint(d.w);
+          v[kSlotResidence] = d.x;
+          v[kSlotExecution] = d.y;
+          v[kSlotStore] = d.z;
+#pragma unroll
+          for (int b2 = 0; b2 < 5; ++b2)
+            v[kSlotFlag0 + b2] = ((f >> b2) & 1u) ? s_one[kSlotFlag0 + b2] : s_zero[kSlotFlag0 + b2];
+          v[kSlotReserved] = s_zero[kSlotReserved];
+          if (!live) {
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k) v[k] = 0.0f;
+          }
+        }
+        if (h == 0) {  // K 0..49
+#pragma unroll
+          for (int i = 0; i < 12; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          put2<kMode>(R1, S::kA0Lo, r, 48, v[48], v[49]);
+        } else {  // K 50..99, then the zero pad up to the last k-step
+          put2<kMode>(R1, S::kA0Lo, r, 50, v[0], v[1]);
+#pragma unroll
+          for (int i = 0; i < 12; ++i)
+            put4<kMode>(R1, S::kA0Lo, r, 52 + 4 * i, v[2 + 4 * i], v[3 + 4 * i], v[4 + 4 * i], v[5 + 4 * i]);
+#pragma unroll
+          for (int k = 100; k < 100 + 2 * S::kPadUnits; k += 2) put2<kMode>(R1, S::kA0Lo, r, k, 0.0f, 0.0f);
+        }
+        if (p.dump) {
+          const int row = t * kRowsT + (lane >> 1);
+          const uint64_t smp = static_cast<uint64_t>(item) * kItem + warp;
+          if (smp < samples && (row + 1) * 100 <= static_cast<int>(p.dump_stride)) {
+            float* o = p.dump + smp * p.dump_stride + row * 100 + 50 * h;
+#pragma unroll
+            for (int k = 0; k < kSlots; k += 2) *reinterpret_cast<float2*>(o + k) = make_float2(v[k], v[k + 1]);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&bar_a0);
+        mark(2 + t);
+      }
+      if (tr && it == 0 && tid == 0) tr[20] = T;
+      // ---- 3. restage conv0 -> conv1 A (two tiles), conv1 -> conv2 A ----
+      mbar_wait(&bar_t0, n_t0++ & 1);  // last conv0 tile done: all conv0 accumulators final, R1 free
+      tc_fence_after();
+      mark(6);
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1) {
+          mbar_wait(&bar_m1, 0);  // conv1 tile 0 consumed R1
+          tc_fence_after();
+        }
+        // conv0 tile t = 2u + half, row m = (sample m/16, position 16t + m%16)
+        //   -> conv1 tile u row (m/16)*16 + 8*half + (m%16)/2, K half (m%2)
+        const int t = 2 * u + half;
+        restage_row<kMode>(R1, tmem + lane_off + t * kC, t >= T, (m >> 4) * 16 + 8 * half + ((m & 15) >> 1),
+                           (m & 1) * kC, sbias[0]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&bar_a1);
+        mark(7 + u);
+      }
+      mbar_wait(&bar_m1, 1);
+      tc_fence_after();
+      mark(9);
+      // conv1 tile `half`, row m = (sample m/16, position 16*half + m%16)
+      //   -> conv2 row (m/16)*16 + 8*half + (m%16)/2, K half (m%2)
+      restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, false, (m >> 4) * 16 + 8 * half + ((m & 15) >> 1),
+                         (m & 1) * kC, sbias[1]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&bar_a2);
+      mark(10);
+
+      // ---- 4. conv2 -> flat[sample][pos*64 + c]: row m is flat row item*128 + m ----
+      mbar_wait(&bar_m2, it & 1);
+      tc_fence_after();
+      mark(11);
+      const uint64_t sample = static_cast<uint64_t>(item) * kItem + (m >> 4);
+      for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + lane_off + 384 + c0, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
+        if (sample < samples) {
+          const uint64_t off = static_cast<uint64_t>(item) * (kItem * 16 * kC) + m * kC + c0;
+          if (kMode == kBF16) {
+            uint4 pk[2];
+            uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+            o[0] = pk[0];
+            o[1] = pk[1];
+          } else {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      compute_sync();  // TMEM conv2 columns and the tables are free for the next item
+      mark(12);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+namespace {
+size_t front_smem_bytes() { return kR1 + kR2 + kTbl + 1024; }
+}  // namespace
+
+void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s) {
+  const uint64_t samples = p.last - p.first;
+  if (samples == 0) return;
+  if (p.max_context + 1 > kTblCols) throw ApiError("fused round front: max_context too large");
+  const uint64_t items = (samples + kItem - 1) / kItem;
+  const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
+  const size_t sm = front_smem_bytes();
+  if (mode == kBF16)
+    launch_pdl(round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+  else if (mode == kTF32)
+    launch_pdl(round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+  else
+    launch_pdl(round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+}
+
+void round_front_set_attributes() {
+  const int sm = static_cast<int>(front_smem_bytes());
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+}
+
+}  // namespace simnet

@@ -1,0 +1,45 @@
+// Fused round front: K1 (apply step + drain + context gather) and the conv
+// chain of K2 in one kernel.  The gathered input never leaves the SM: it is
+// written straight into the SWIZZLE_128B conv0 operand in shared memory.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "common.cuh"
+#include "host_util.cuh"
+
+namespace simnet {
+
+struct FrontParams {
+  // K1 (same meaning as CtxParams)
+  SubState* state;
+  RingEntry* proc;
+  RingEntry* wq;
+  uint32_t pmask, wmask;
+  uint64_t first, last;      // sub-trace range of this launch (chunk)
+  const float* stat;         // [n][kStatStride] normalised static slots
+  const uint64_t* pc;
+  const uint64_t* addr;
+  const uint8_t* iflags;
+  const NormConsts* nc;
+  int32_t max_context;
+  uint32_t bw, line, page;
+  int32_t per_cycle;
+  // conv chain
+  const float* b0;
+  const float* b1;
+  const float* b2;
+  void* out;                 // flat [last-first][1024] (f32, or bf16 for the bf16 path)
+  // optional: write the gathered input (exact f32 values) in the standard
+  // row layout [last-first][dump_stride] (rows of 100 floats) — input capture
+  float* dump;
+  uint32_t dump_stride;
+  long long* trace;          // optional: per-CTA event clocks of the first item (diagnostics)
+  int32_t knockout;          // diagnostics only (SIMNET_KNOCKOUT): 1 = no static loads, 2 = no apply
+};
+
+// w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
+void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s);
+void round_front_set_attributes();
+
+}  // namespace simnet

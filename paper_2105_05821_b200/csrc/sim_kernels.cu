@@ -14,81 +14,12 @@
 
 #include "common.cuh"
 #include "decode.cuh"
+#include "k1_device.cuh"
 #include "launch.cuh"
 #include "sim_kernels.cuh"
 
 namespace simnet {
 
-namespace {
-
-constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
-
-__device__ __forceinline__ uint32_t leading_run(uint32_t mask) {
-  return mask == kFull ? 32u : static_cast<uint32_t>(__ffs(~mask) - 1);
-}
-
-struct Rings {
-  RingEntry* proc;
-  RingEntry* wq;
-  uint32_t pmask, wmask, wcap;
-};
-
-// SimCore::retire (simcore.cpp:68-84).  Warp-uniform in/out; returns the
-// number of queue transitions.  Sets *err on write-ring overflow.
-__device__ uint32_t warp_retire(uint64_t cur, uint64_t budget, const Rings& r, uint32_t& ph,
-                                uint32_t pt, uint32_t& wh, uint32_t& wt, uint32_t* err) {
-  const uint32_t lane = lane_id();
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t events = 0;
-  while (budget > 0 && ph != pt) {
-    const uint32_t n = min(pt - ph, 32u);
-    RingEntry e;
-    bool ready = false;
-    if (lane < n) {
-      e = r.proc[(ph + lane) & r.pmask];
-      ready = (cur - e.push) >= e.exec;
-    }
-    const uint32_t run = leading_run(__ballot_sync(kFull, ready));
-    const uint32_t take = static_cast<uint32_t>(min(static_cast<uint64_t>(run), budget));
-    const bool mv = lane < take && (e.flags & kFlagStore);
-    const uint32_t sm = __ballot_sync(kFull, mv);
-    const uint32_t nmv = __popc(sm);
-    if (wt + nmv - wh > r.wcap) {
-      *err = kErrWriteRing;
-      return events;
-    }
-    if (mv) r.wq[(wt + __popc(sm & lt)) & r.wmask] = e;
-    wt += nmv;
-    ph += take;
-    budget -= take;
-    events += take;
-    if (take < n) break;
-  }
-  while (wh != wt) {
-    const uint32_t n = min(wt - wh, 32u);
-    bool ready = false;
-    if (lane < n) {
-      const RingEntry& e = r.wq[(wh + lane) & r.wmask];
-      ready = (cur - e.push) >= e.store;
-    }
-    const uint32_t run = leading_run(__ballot_sync(kFull, ready));
-    wh += run;
-    events += run;
-    if (run < n) break;
-  }
-  __syncwarp();
-  return events;
-}
-
-// readiness gap of a head entry (simcore.cpp:95-110 per queue)
-__device__ __forceinline__ uint64_t head_gap(uint64_t cur, uint64_t push, uint32_t lat) {
-  const uint64_t res = cur - push;
-  return lat > res ? lat - res : 1;
-}
-
-}  // namespace
 
 // ---------------------------------------------------------------------------
 // K1: apply the pending step, drain finished sub-traces, gather the next input.
@@ -106,94 +37,21 @@ ctx_kernel(CtxParams p) {
 
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = k1::lane_id();
   const uint64_t s = blockIdx.x + p.first;
   if (s >= p.last) return;
 
   SubState* sp = p.state + s;
   const NormConsts& nc = *p.nc;
-  Rings r{p.proc + s * (p.pmask + 1ull), p.wq + s * (p.wmask + 1ull), p.pmask, p.wmask, p.wmask + 1u};
+  const k1::Rings r = k1::rings_of(p.proc, p.wq, p.pmask, p.wmask, s);
   if (warp == 0) {
     SubState st = *sp;  // every lane holds a copy; lane 0 writes back
-    uint32_t err = kOk;
-    if (st.status == kOk) {
-      if (st.has_pend) {
-        const uint32_t F = st.pend_f;
-        // fetch advance: K3 already moved cur by F (lumped); retire with budget bw*F
-        if (F > 0) {
-          if (p.per_cycle) {
-            for (uint32_t c = 0; c < F && err == kOk; ++c) {
-              st.cur += 1;
-              warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
-            }
-          } else {
-            warp_retire(st.cur, static_cast<uint64_t>(p.bw) * F, r, st.ph, st.pt, st.wh, st.wt, &err);
-          }
-        }
-        // forced stall (simcore.cpp:127-136): budget bw, not bw*gap
-        while (err == kOk && st.pt - st.ph >= static_cast<uint32_t>(p.max_context)) {
-          const uint32_t before = st.pt - st.ph;
-          const RingEntry& h = r.proc[st.ph & r.pmask];
-          const uint64_t gap = head_gap(st.cur, h.push, h.exec);
-          st.cur += gap;
-          st.overflow += gap;
-          warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
-          if (err == kOk && st.pt - st.ph >= before) {
-            err = kErrStall;
-            st.err_tick = st.cur;
-          }
-        }
-        if (err == kOk) {  // push (simcore.cpp:138-145)
-          if (lane == 0) {
-            RingEntry e;
-            e.push = st.cur;
-            e.idx = st.pos;
-            e.exec = st.pend_e;
-            e.store = st.pend_s;
-            e.nexec = norm_slot(static_cast<int32_t>(st.pend_e), nc.mean[kSlotExecution], nc.sd[kSlotExecution]);
-            e.nstore = norm_slot(static_cast<int32_t>(st.pend_s), nc.mean[kSlotStore], nc.sd[kSlotStore]);
-            e.pc = st.t_pc;  // stashed by this sub-trace's previous gather (0 when none ran)
-            e.addr = st.t_addr;
-            e.flags = p.gather ? st.t_flags : p.iflags[st.begin + st.pos];
-            r.proc[st.pt & r.pmask] = e;
-          }
-          st.pt += 1;
-          st.pos += 1;
-          st.has_pend = 0;
-          if (st.pos == st.warm) {  // warm-up extension: counting starts after this step
-            st.base_cur = st.cur;
-            st.base_overflow = st.overflow;
-          }
-          // drain right after the last step (parallel.cpp:79, simcore.cpp:152-159)
-          if (st.pos == st.len && st.count_drain) {
-            while (err == kOk && (st.ph != st.pt || st.wh != st.wt)) {
-              uint64_t gap = ~uint64_t{0};
-              if (st.ph != st.pt) {
-                const RingEntry& h = r.proc[st.ph & r.pmask];
-                { const uint64_t g = head_gap(st.cur, h.push, h.exec); gap = g < gap ? g : gap; }
-              }
-              if (st.wh != st.wt) {
-                const RingEntry& h = r.wq[st.wh & r.wmask];
-                { const uint64_t g = head_gap(st.cur, h.push, h.store); gap = g < gap ? g : gap; }
-              }
-              if (gap < 1) gap = 1;
-              st.cur += gap;
-              st.drain += gap;
-              const uint32_t ev = warp_retire(st.cur, p.bw, r, st.ph, st.pt, st.wh, st.wt, &err);
-              if (err == kOk && ev == 0) {
-                err = kErrDrain;
-                st.err_tick = st.cur;
-              }
-            }
-          }
-        }
-        if (err != kOk) st.status = err;
-        __syncwarp();
-        if (lane == 0) *sp = st;
-        __syncwarp();
-      }
+    if (st.status == kOk && st.has_pend) {
+      const k1::ApplyArgs aa{p.bw, p.max_context, p.per_cycle, p.gather, p.iflags, p.nc};
+      k1::apply_step(st, r, aa);
+      if (lane == 0) *sp = st;
+      __syncwarp();
     }
-    (void)err;
     if (lane == 0) s_st = st;
   }
   __syncthreads();
@@ -219,17 +77,9 @@ ctx_kernel(CtxParams p) {
       for (int k = kStatic; k < kSlots; ++k) s_dyn[0][k - kStatic] = nc.zero[k];
       continue;
     }
-    const uint32_t j = c - 1;
-    const RingEntry e = j < nproc ? r.proc[(st.pt - 1 - j) & r.pmask] : r.wq[(st.wt - 1 - (j - nproc)) & r.wmask];
+    const RingEntry e = k1::context_entry(st, r, c - 1);
     const int32_t res = static_cast<int32_t>(static_cast<uint32_t>(st.cur - e.push));
-    // memory_dependency_flags (dataset.cpp:47-60)
-    uint32_t f = (tpc / p.line) == (e.pc / p.line) ? 1u : 0u;
-    if (tmem && (e.flags & kFlagMem)) {
-      f |= (taddr == e.addr) ? 2u : 0u;
-      f |= (taddr / p.line) == (e.addr / p.line) ? 4u : 0u;
-      f |= (taddr / p.page) == (e.addr / p.page) ? 8u : 0u;
-    }
-    f |= (tpc / p.page) == (e.pc / p.page) ? 16u : 0u;
+    const uint32_t f = k1::dep_flags(tpc, taddr, tmem, e, p.line, p.page);
     float* d = s_dyn[c];
     s_inst[c] = static_cast<uint32_t>(st.begin + e.idx);
     d[0] = norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]);

@@ -20,6 +20,7 @@ p.add_argument("--n", type=int, default=300_000)
 p.add_argument("--k", type=int, default=1024)
 p.add_argument("--regime", default="default")
 p.add_argument("--runs", type=int, default=1)
+p.add_argument("--unfused", action="store_true")
 a = p.parse_args()
 kind = "memory" if a.regime == "memory" else "mix"
 t = synthetic_trace(a.n, 101, kind=kind)
@@ -29,6 +30,7 @@ g.load_model(m)
 pc = ParallelConfig(k=a.k, sim=SimConfig(max_context=m.config.max_context))
 g.load_trace(t, pc)
 for _ in range(a.runs):
-    r = g.run(pc)
-print(f"{a.precision} n={a.n} k={a.k}: {r.rounds} rounds, {r.device_ms:.1f} ms, "
+    r = g.run(pc, fused=not a.unfused)
+import os
+print(f"{a.precision}{' unfused' if a.unfused else ''} n={a.n} k={a.k}: {r.rounds} rounds, {r.device_ms:.1f} ms, "
       f"{1000 * r.device_ms / max(r.rounds, 1):.2f} us/round, launches {r.launches}")

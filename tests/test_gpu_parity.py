@@ -260,3 +260,58 @@ def test_tensor_core_batch_tail_and_small_model(gpu, port, precision):
         out, _ = g.predict(want["cap_inputs"], want["cap_is_store"])
         err = np.abs(out - want["cap_outputs"]) / np.maximum(1.0, np.abs(want["cap_outputs"]))
         assert err.max() <= (1e-4 if precision == "tf32x3" else 1.5e-1), (k, err.max())
+
+
+# ---- fused round front (K1 + conv chain in one kernel) -----------------------
+def _fused_cases(port, golden):
+    m = c3_model(port, golden)
+    return m, [(read_trace(GOLD / "mix_3000_s4.trace"), 5), (read_trace(GOLD / "branchy_2000_s8.trace"), 130),
+               (store_heavy(31, 1500), 3), (read_trace(GOLD / "pointer_chase_2000_s3.trace"), 1)]
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16", "tf32"])
+def test_fused_front_matches_unfused(gpu, port, golden, precision):
+    """The fused round front (gather straight into the conv0 operand, skipped
+    all-zero tiles) must reproduce the unfused tensor-core round bit for bit:
+    every accumulator row depends only on its own input row."""
+    g = gpu(precision)
+    m, cases = _fused_cases(port, golden)
+    g.load_model(m)
+    for t, k in cases:
+        pc = pcfg(k)
+        g.load_trace(t, pc)
+        a = g.run(pc, fused=True)
+        b = g.run(pc, fused=False)
+        assert np.array_equal(gpu_subs(a), gpu_subs(b)), (t.n, k)
+        assert np.array_equal(a.predicted_fetch, b.predicted_fetch), (t.n, k)
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_fused_front_inputs_bit_exact(gpu, port, golden, precision):
+    """Inputs gathered by the fused kernel (captured from its shared-memory
+    operand as exact f32) equal the reference's next_request tensors for every
+    round up to the first decode divergence from the CPU oracle."""
+    g = gpu(precision)
+    m = c3_model(port, golden)
+    g.load_model(m)
+    for t, k in ((read_trace(GOLD / "mix_3000_s4.trace"), 5), (store_heavy(31, 1500), 3)):
+        pc = pcfg(k)
+        g.load_trace(t, pc)
+        got = g.run(pc)
+        want = port.simulate(t, m, k=k, capture=t.n, capture_inputs=True)
+        # rounds before the first differing fetch latency see identical queues
+        diff = np.nonzero(got.predicted_fetch != want["predicted_fetch"])[0]
+        idx = want["cap_index"]
+        rounds = want["cap_round"]
+        first_bad = int(rounds[np.isin(idx, diff)].min()) if diff.size else int(rounds.max()) + 1
+        checked = 0
+        for r in (0, 1, 7, 50, 200, 480, int(rounds.max())):
+            if r >= first_bad:
+                continue
+            rows = np.nonzero(rounds == r)[0]
+            buf = g.capture_round(r, k)
+            g.run(pc)
+            g.clear_capture()
+            assert np.array_equal(buf[: rows.size], want["cap_inputs"][rows]), f"round {r}"
+            checked += 1
+        assert checked >= 2, (first_bad, precision)

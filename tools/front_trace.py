@@ -1,0 +1,24 @@
+# diagnostics: fused round-front phase clocks in graph mode (SIMNET_CHAIN_TRACE=1)
+import sys, ctypes as C, numpy as np, os
+os.environ["SIMNET_CHAIN_TRACE"] = "1"
+sys.path.insert(0, '/root/repo')
+from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, _lib
+from paper_2105_05821_b200.synth import synthetic_trace, synthetic_model
+N = int(os.environ.get("N", "300000")); t = synthetic_trace(N, 101); m = synthetic_model(synthetic_trace(200_000, 101), 1)
+for prec in ("tf32x3", "bf16"):
+    g = GpuSimulator(0, prec); g.load_model(m)
+    pc = ParallelConfig(k=1024); g.load_trace(t, pc); g.run(pc)
+    buf = np.zeros(148 * 32, np.int64)
+    _lib.lib().simnet_debug_chain_trace(C.c_void_p(buf.ctypes.data))
+    tr = buf.reshape(148, 32)[:128].astype(np.float64)
+    T = tr[:, 20]
+    base = tr[:, :1]
+    names = {0: "start", 15: "dep wait done", 16: "apply done (warp0)", 1: "table done", 2: "tile0 gathered",
+             3: "tile1 gathered", 6: "conv0 done", 7: "a1 tile0", 8: "a1 tile1", 9: "conv1 done", 10: "a2",
+             11: "conv2 done", 12: "out done"}
+    print(prec, "T histogram", np.bincount(T.astype(int)))
+    ap = tr[:, 16:24] - base
+    print(f"  apply per warp: median {np.median(ap):.0f}, max over warps median {np.median(ap.max(1)):.0f}")
+    for i in (0, 15, 16, 1, 2, 3, 6, 7, 8, 9, 10, 11, 12):
+        col = (tr[:, i] - base[:, 0])[tr[:, i] > 0]
+        if col.size: print(f"  {names[i]:18s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
