@@ -225,7 +225,9 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   uint32_t* d_pf = cfg.record_fetch ? static_cast<uint32_t*>(c->pred_fetch.need(owned * 4)) : nullptr;
 
   // chunking of the batch (bounds activation memory; results are batch-independent)
-  const uint64_t chunk = std::min<uint64_t>(K, 65536);
+  uint64_t chunk_cap = 65536;
+  if (const char* e = std::getenv("SIMNET_CHUNK")) chunk_cap = std::max<long long>(8, std::atoll(e));  // tests
+  const uint64_t chunk = std::min<uint64_t>(K, chunk_cap);
   // Fused round front (tensor-core C3): K1 apply + gather + conv chain in one
   // kernel, the gathered input stays in shared memory.  reserved[2] = 1 forces
   // the unfused path (ctx_kernel + TMA conv chain), e.g. for A/B checks.
@@ -248,6 +250,14 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   }
   ForwardBuffers fb{};
   if (!oracle) fb = forward_buffers(c->model, chunk, c->act, c->y);
+  // fused rounds keep every chunk's FC1 partials until the next round's front
+  // decodes them: partial planes for all K sub-traces, chunk f at part_off f
+  if (fused && K > chunk) tc_prepare(c->model, K);
+  auto fb_chunk = [&](uint64_t f) {
+    ForwardBuffers b = fb;
+    if (fused) b.part_off = f;
+    return b;
+  };
 
   // A "span" is a contiguous range [f, l) of sub-traces whose buffers start at
   // sample `off` of the chunk buffers, launched on stream `st`.
@@ -302,7 +312,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     return dp;
   };
   bool k3_fused = false;  // tensor-core tails run K3 themselves
-  auto do_front = [&](uint64_t f, uint64_t l, float* dump, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
+  auto front_params = [&](uint64_t f, uint64_t l, float* dump, const ForwardBuffers& fbs) -> FrontParams {
     FrontParams fp{};
     fp.state = d_state;
     fp.proc = d_proc;
@@ -323,12 +333,15 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     fp.per_cycle = cfg.per_cycle_advance;
     fp.dump = dump;
     fp.dump_stride = dump_stride;
-    return tc_front(c->model, fp, fbs, st);
+    fp.fc = tc_fc_decode_args(c->model, l - f, fbs);
+    fp.fc.pred_fetch = d_pf;
+    fp.fc.per_cycle = cfg.per_cycle_advance;
+    return fp;
   };
+  // fused round: front (decode + apply of the previous round, gather, conv) -> FC1
   auto do_fc = [&](uint64_t f, uint64_t l, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
-    const DecodeParams dp = decode_params(f, l, fbs);
     k3_fused = true;
-    return tc_fc(c->model, fbs.act[2], l - f, fbs, st, &dp);
+    return tc_fc(c->model, fbs.act[2], l - f, fbs, st, nullptr, false);
   };
   auto do_forward = [&](uint64_t f, uint64_t l, uint64_t off, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
     if (oracle) return 0;
@@ -340,9 +353,13 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     launch_decode(decode_params(f, l, fbs), st);
     return 1;
   };
-  // one round of one span: K1 -> K2 -> K3 (fused: front -> FC)
+  auto do_front = [&](uint64_t f, uint64_t l, float* dump, const ForwardBuffers& fbs, cudaStream_t st) -> uint64_t {
+    return tc_front(c->model, front_params(f, l, dump, fbs), fbs, st);
+  };
+  // one round of one span: K1 -> K2 -> K3 (fused: front -> FC1)
   auto run_span = [&](uint64_t f, uint64_t l, uint64_t off, cudaStream_t st) -> uint64_t {
-    const ForwardBuffers fbs = oracle ? fb : fb_slice(c->model, fb, off);
+    ForwardBuffers fbs = oracle ? fb : fb_slice(c->model, fb, off);
+    if (fused) fbs.part_off = f;
     if (fused) {
       static const int ko = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
       return ((ko & 8) ? 0 : do_front(f, l, nullptr, fbs, st)) + ((ko & 4) ? 0 : do_fc(f, l, fbs, st));
@@ -395,7 +412,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
         if (profile) CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
         if (fused) {
           if (cap_now) CUDA_OK(cudaMemsetAsync(d_x, 0, chunk * dump_stride * sizeof(float), c->stream));
-          launches += do_front(f, l, cap_now ? static_cast<float*>(d_x) : nullptr, fb, c->stream);
+          launches += do_front(f, l, cap_now ? static_cast<float*>(d_x) : nullptr, fb_chunk(f), c->stream);
         } else {
           launches += do_ctx(f, l, true, 0, c->stream);
         }
@@ -407,7 +424,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
           CUDA_OK(cudaMemcpy2DAsync(c->cap_host, width * sizeof(float), d_x, pitch * sizeof(float),
                                     width * sizeof(float), rows, cudaMemcpyDeviceToHost, c->stream));
         }
-        launches += fused ? do_fc(f, l, fb, c->stream) : do_forward(f, l, 0, fb, c->stream);
+        launches += fused ? do_fc(f, l, fb_chunk(f), c->stream) : do_forward(f, l, 0, fb, c->stream);
         if (profile) CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
         launches += do_decode(f, l, fb, c->stream);
         if (profile) {
@@ -435,7 +452,15 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
       launches += launches_1;
     }
   }
-  for (uint64_t f = 0; f < K; f += chunk) launches += do_ctx(f, std::min(K, f + chunk), false, 0, c->stream);  // apply final step, drain
+  for (uint64_t f = 0; f < K; f += chunk) {  // apply final step, drain
+    const uint64_t l = std::min(K, f + chunk);
+    if (fused) {
+      launch_final_decode(front_params(f, l, nullptr, fb_chunk(f)), c->stream);
+      ++launches;
+    } else {
+      launches += do_ctx(f, l, false, 0, c->stream);
+    }
+  }
   CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
   CUDA_OK(cudaGetLastError());
   CUDA_OK(cudaEventSynchronize(c->ev[1]));

@@ -52,7 +52,8 @@ struct __align__(16) SubState {
   uint64_t err_tick;
   uint64_t t_pc, t_addr;             // pc / data address of instruction `pos` (set by the gather)
   uint32_t t_flags;                  // its flags, copied into the ring entry at push
-  uint32_t pad_[3];
+  uint32_t awaiting;                 // fused round: input gathered, prediction not yet decoded
+  uint32_t pad_[2];
 };
 static_assert(sizeof(SubState) == 160, "SubState layout");
 

@@ -1,0 +1,176 @@
+// Warp-cooperative FC tail for one sample: h = ReLU(sum of FC1 split-K
+// partials + b1), y = W2 h + b2, hybrid decode (cnn.cpp:106-125, 388-417).
+// Shared by the FC tail kernel (unfused path, teacher-forced predict), the
+// fused round front (decoding the previous round's prediction right before
+// applying it) and the final decode/drain kernel, so every path computes the
+// same bits.  Fixed, batch-independent arithmetic order:
+//   lane l owns hidden units 4c..4c+3 for c = l, l + 32 (c < hidden/4);
+//   h_j = ReLU((sum_q part[q][j], q ascending from 0) + b1[j]);
+//   y_o = (transpose-reduction over lanes of each lane's fma chain over its
+//          units: exchange stages xor 16, 8, 4, 2, 1) + b2[o].
+#pragma once
+#include "common.cuh"
+#include "decode.cuh"
+
+namespace simnet {
+
+constexpr int kFcMaxHidden = 256;
+constexpr int kFcMaxSplit = 8;
+constexpr int kFcMaxOut = 64;
+
+struct FcDecodeArgs {
+  const float* part;      // [nsplit][split_stride] : [samples][hidden] per split plane
+  int32_t nsplit;
+  uint64_t split_stride;
+  int32_t hidden;         // multiple of 4, <= 256
+  const float* b1;
+  const float* w2t;       // [od][hidden] (global; callers stage it in shared memory)
+  const float* b2;
+  int32_t od;             // output_dim <= 64
+  int32_t class_fetch, class_exec, class_store;
+  uint32_t* pred_fetch;   // owned predicted fetch series (may be null)
+  int32_t per_cycle;
+};
+
+__device__ __forceinline__ void fc_sync256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// Hybrid decode of one sample's head outputs y (decode_triple, decode.cuh),
+// the three heads on lanes 0-2 in parallel; returns the triple in every lane.
+// lab: label mean[3], stdev[3] (NormStats, dataset.hpp:54-65), in shared memory.
+__device__ __forceinline__ void warp_decode_triple(const float* y, const double* lab, int cf, int ce, int cs,
+                                                   bool is_store, uint32_t* t) {
+  const int lane = threadIdx.x & 31;
+  uint32_t mine = 0;
+  if (lane < 3) {
+    const int base = lane == 0 ? 3 : (lane == 1 ? 3 + cf : 3 + cf + ce);
+    const int n = lane == 0 ? cf : (lane == 1 ? ce : cs);
+    mine = decode_head(y, base, n, y[lane], lab[lane], lab[3 + lane]);
+    if (lane == 1) mine = mine < 1u ? 1u : mine;  // execution >= 1
+    if (lane == 2 && !is_store) mine = 0u;       // store latency only for stores
+  }
+  t[0] = __shfl_sync(0xffffffffu, mine, 0);
+  t[1] = __shfl_sync(0xffffffffu, mine, 1);
+  t[2] = __shfl_sync(0xffffffffu, mine, 2);
+}
+
+// FC tail of 8 samples by the 8 warps (256 threads, named barrier 1) of a
+// CTA; warp w owns sample w.  s_local[w]: the sample's row in the partial
+// planes (any valid row for an unused warp).  w2s: W2 [od][hidden] in shared
+// memory; hs: 8 x hidden floats and ys: 8 x 64 floats of shared scratch (ys
+// holds y on return).  Arithmetic order (fixed, batch-independent):
+//   h[s][j] = ReLU((sum over q ascending of part[q][s][j]) + b1[j]);
+//   lane l owns hidden units 4c..4c+3, c = l, l + 32: its partial for (s, o) is
+//   an fma chain over those units in order; the 32 lane partials of the 8
+//   samples are combined by a transpose reduction (xor 16, 8, 4) then a
+//   butterfly (xor 2, 1); y[s][o] = that + b2[o].
+__device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const float* w2s, float* hs, float* ys,
+                               long long* trace = nullptr) {
+  const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
+  const int hid = a.hidden, c4 = hid >> 2;
+  // biases fetched with the partials (no dependent global load later): lane j
+  // holds b2 of this warp's j-th output, b1 of its own hidden units
+  const float b2v = (lane < 8 && warp + 8 * lane < a.od) ? __ldg(a.b2 + warp + 8 * lane) : 0.0f;
+  float4 b1v[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    b1v[u] = lane + 32 * u < c4 ? __ldg(reinterpret_cast<const float4*>(a.b1) + lane + 32 * u)
+                                : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  {  // h of this warp's sample
+    float4 pv[2][kFcMaxSplit];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = lane + 32 * u;
+#pragma unroll
+      for (int q = 0; q < kFcMaxSplit; ++q)
+        pv[u][q] = (c < c4 && q < a.nsplit)
+                       ? __ldg(reinterpret_cast<const float4*>(a.part + q * a.split_stride + s_local * hid) + c)
+                       : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = lane + 32 * u;
+      if (c >= c4) continue;
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < kFcMaxSplit; ++q) {  // fixed order (zeros past nsplit are exact)
+        acc.x += pv[u][q].x;
+        acc.y += pv[u][q].y;
+        acc.z += pv[u][q].z;
+        acc.w += pv[u][q].w;
+      }
+      const float4 b = b1v[u];
+      reinterpret_cast<float4*>(hs + warp * hid)[c] =
+          make_float4(fmaxf(acc.x + b.x, 0.0f), fmaxf(acc.y + b.y, 0.0f), fmaxf(acc.z + b.z, 0.0f),
+                      fmaxf(acc.w + b.w, 0.0f));
+    }
+  }
+  fc_sync256();
+  if (trace && threadIdx.x == 0) trace[0] = clock64();
+  {  // FC2: warp w computes outputs o = w, w + 8, ... for all 8 samples
+    float4 hr[8][2];
+#pragma unroll
+    for (int sm = 0; sm < 8; ++sm)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
+        hr[sm][u] = c < c4 ? reinterpret_cast<const float4*>(hs + sm * hid)[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+    for (int j = 0, o = warp; o < a.od; ++j, o += 8) {
+      const float b2o = __shfl_sync(0xffffffffu, b2v, j);
+      float4 wv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
+        wv[u] = c < c4 ? reinterpret_cast<const float4*>(w2s + o * hid)[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+      float v[8];
+#pragma unroll
+      for (int sm = 0; sm < 8; ++sm) {
+        float p = 0.0f;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          p = fmaf(wv[u].x, hr[sm][u].x, p);
+          p = fmaf(wv[u].y, hr[sm][u].y, p);
+          p = fmaf(wv[u].z, hr[sm][u].z, p);
+          p = fmaf(wv[u].w, hr[sm][u].w, p);
+        }
+        v[sm] = p;
+      }
+#pragma unroll
+      for (int m = 16, n = 4; m >= 4; m >>= 1, n >>= 1) {  // transpose: 8 -> 4 -> 2 -> 1 values per lane
+        const bool upper = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const float keep = upper ? v[i + n] : v[i];
+          const float send = upper ? v[i] : v[i + n];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+      }
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+      if ((lane & 3) == 0) {
+        const int sm = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        ys[sm * kFcMaxOut + o] = v[0] + b2o;
+      }
+    }
+  }
+  fc_sync256();
+}
+
+// apply_decoded (decode.cuh) on a register copy of the state; lane 0 records
+// the predicted fetch latency.
+__device__ __forceinline__ void apply_decoded_reg(SubState& st, const uint32_t* t, uint32_t* pred_fetch,
+                                                  int per_cycle) {
+  const uint32_t pos = st.pos;
+  st.pend_f = t[0];
+  st.pend_e = t[1];
+  st.pend_s = t[2];
+  st.has_pend = 1;
+  if (!per_cycle && t[0] > 0) st.cur += t[0];
+  if (pos >= st.warm) {
+    st.sum_fetch += t[0];
+    if (pred_fetch && (threadIdx.x & 31) == 0) pred_fetch[st.fetch_off + (pos - st.warm)] = t[0];
+  }
+}
+
+}  // namespace simnet

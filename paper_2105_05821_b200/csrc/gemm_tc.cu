@@ -274,109 +274,51 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
 }
 
-// FC tail (+ fused K3): h = ReLU(sum of split-K partials + b1), summed in a
-// fixed order; y = W2 h + b2 in fp32 with four interleaved accumulators
-// combined in a fixed order (deterministic, batch-independent); then, when
-// simulating, the hybrid decode and clock advance of K3 for each sample.
-constexpr int kTailSamples = 4;
-constexpr int kMaxSplit = 8;  // split-K planes of FC1 (flat 1024 f32 = 32 chunks / 4)
-constexpr int kTailThreads = 256;
-constexpr int kMaxOut = 64;
+// FC tail (+ fused K3): 8 samples per block through cta8_fc (fc_decode.cuh:
+// split-K reduction, ReLU, FC2 in a fixed batch-independent order), then,
+// when simulating, the hybrid decode and clock advance of K3 per sample.
+constexpr int kTailWarps = 8;
+constexpr int kTailThreads = 32 * kTailWarps;
+constexpr int kMaxSplit = kFcMaxSplit;  // split-K planes of FC1 (flat 1024 f32 = 32 chunks / 4)
+constexpr int kMaxOut = kFcMaxOut;
 
 struct TailParams {
-  const float* part;
-  int nsplit;
-  uint64_t split_stride;
-  int hidden;
-  const float* b1;
-  const float* w2t;  // [od][hidden]
-  const float* b2;
-  int od;
+  FcDecodeArgs fc;
   float* y;
   int samples;
   DecodeParams dec;  // dec.state == nullptr: outputs only
 };
 
-// dynamic smem: W2 [od][hidden + 4] | h [kTailSamples][hidden] | y [kTailSamples][kMaxOut]
+// dynamic smem: W2 [od][hidden] | h [kTailWarps][hidden] | y [kTailWarps][kMaxOut]
 __global__ void __launch_bounds__(kTailThreads) fc_tail_kernel(TailParams p) {
   extern __shared__ __align__(16) float tail_sm[];
-  const int hid = p.hidden, ws = hid + 4;  // +4: conflict-free float4 row reads
+  __shared__ double s_lab[6];
+  const int hid = p.fc.hidden, od = p.fc.od;
+  if (threadIdx.x < 6 && p.dec.nc)
+    s_lab[threadIdx.x] = threadIdx.x < 3 ? p.dec.nc->label_mean[threadIdx.x] : p.dec.nc->label_sd[threadIdx.x - 3];
   float* w2s = tail_sm;
-  float* hs = w2s + p.od * ws;
-  float* ys = hs + kTailSamples * hid;
+  float* hs = w2s + od * hid;
+  float* ys = hs + kTailWarps * hid;
   asm volatile("griddepcontrol.launch_dependents;");
-  // W2 (a constant) is staged before the dependency wait: all float4 loads in flight
-  {
-    const int per_row = hid / 4, total = p.od * per_row;
-    const float4* src = reinterpret_cast<const float4*>(p.w2t);
-    for (int base = threadIdx.x; base < total; base += kTailThreads * 8) {
-      float4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = base + u * kTailThreads;
-        if (i < total) v[u] = __ldg(src + i);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = base + u * kTailThreads;
-        if (i < total) {
-          const int o = i / per_row, k4 = i - o * per_row;
-          *reinterpret_cast<float4*>(w2s + o * ws + 4 * k4) = v[u];
-        }
-      }
-    }
+  {  // W2 (a constant) is staged before the dependency wait
+    const int total = od * hid / 4;
+    const float4* src = reinterpret_cast<const float4*>(p.fc.w2t);
+    for (int i = threadIdx.x; i < total; i += kTailThreads) reinterpret_cast<float4*>(w2s)[i] = __ldg(src + i);
   }
+  __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int s0 = blockIdx.x * kTailSamples;
-  const int ns = min(kTailSamples, p.samples - s0);
-  // hidden unit j of every sample in the block: kTailSamples x kMaxSplit loads in flight
-  for (int j = threadIdx.x; j < hid; j += kTailThreads) {
-    float pv[kTailSamples][kMaxSplit];
-#pragma unroll
-    for (int ls = 0; ls < kTailSamples; ++ls)
-#pragma unroll
-      for (int q = 0; q < kMaxSplit; ++q)
-        pv[ls][q] = (ls < ns && q < p.nsplit)
-                        ? __ldg(p.part + q * p.split_stride + static_cast<uint64_t>(s0 + ls) * hid + j)
-                        : 0.0f;
-    const float bj = __ldg(p.b1 + j);
-#pragma unroll
-    for (int ls = 0; ls < kTailSamples; ++ls) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int q = 0; q < kMaxSplit; ++q) acc += pv[ls][q];  // fixed order (zeros past nsplit are exact)
-      hs[ls * hid + j] = fmaxf(acc + bj, 0.0f);
-    }
-  }
-  __syncthreads();
-  for (int task = threadIdx.x; task < ns * p.od; task += kTailThreads) {
-    const int ls = task / p.od, o = task - ls * p.od;
-    const float4* w = reinterpret_cast<const float4*>(w2s + o * ws);
-    const float4* h = reinterpret_cast<const float4*>(hs + ls * hid);
-    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-#pragma unroll 8
-    for (int k4 = 0; k4 < hid / 4; ++k4) {
-      const float4 wv = w[k4], hv = h[k4];
-      a0 = fmaf(wv.x, hv.x, a0);
-      a1 = fmaf(wv.y, hv.y, a1);
-      a2 = fmaf(wv.z, hv.z, a2);
-      a3 = fmaf(wv.w, hv.w, a3);
-    }
-    const float v = ((a0 + a1) + (a2 + a3)) + __ldg(p.b2 + o);
-    ys[ls * kMaxOut + o] = v;
-    p.y[static_cast<uint64_t>(s0 + ls) * p.od + o] = v;
-  }
-  if (p.dec.state == nullptr) return;
-  __syncthreads();
-  if (threadIdx.x < ns) {  // K3: decode + clock for this sample's sub-trace
-    const DecodeParams& d = p.dec;
-    SubState* sp = d.state + d.first + s0 + threadIdx.x;
-    if (sp->status == kOk && sp->pos < sp->len) {
-      uint32_t t[3];
-      decode_triple(ys + threadIdx.x * kMaxOut, *d.nc, d.class_fetch, d.class_exec, d.class_store,
-                    (d.iflags[sp->begin + sp->pos] & kFlagStore) != 0, t);
-      apply_decoded(sp, t, d.pred_fetch, d.per_cycle);
-    }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kTailWarps + warp;
+  cta8_fc(p.fc, static_cast<uint64_t>(s < p.samples ? s : 0), w2s, hs, ys);  // all 8 warps take part
+  if (s >= p.samples) return;
+  const float* y = ys + warp * kMaxOut;
+  for (int o = lane; o < od; o += 32) p.y[static_cast<uint64_t>(s) * od + o] = y[o];
+  SubState* sp = p.dec.state ? p.dec.state + p.dec.first + s : nullptr;
+  if (sp && sp->status == kOk && sp->pos < sp->len) {
+    uint32_t t[3];
+    warp_decode_triple(y, s_lab, p.fc.class_fetch, p.fc.class_exec, p.fc.class_store,
+                       (p.dec.iflags[sp->begin + sp->pos] & kFlagStore) != 0, t);
+    if (lane == 0) apply_decoded(sp, t, p.dec.pred_fetch, p.dec.per_cycle);
   }
 }
 
@@ -454,6 +396,8 @@ struct TcModel {
   TcWeights fc1;
   DevBuf w2t;   // fc2 weights transposed to [out_dim][hidden] (k contiguous)
   DevBuf part;  // split-K partials
+  DevBuf c1acc; // calibrated conv1 accumulator row of an all-constant window (fused front)
+  DevBuf calib_out;
 };
 
 namespace {
@@ -596,7 +540,7 @@ uint32_t tc_act_bytes(const TcModel* t) { return t->mode == kBF16 ? 2u : 4u; }
 // FC1 (split-K tcgen05 partials) and the FC tail (FC2 + fused K3) on the
 // flat conv output `in`.
 uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
-               const DecodeParams* fuse) {
+               const DecodeParams* fuse, bool with_tail) {
   if (!m.tc) throw ApiError("internal: tensor-core model missing");
   TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
@@ -638,24 +582,14 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
     launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
-    const int od = m.L.out_dim;
-    if (od > kMaxOut || c.fc_hidden % 4 != 0)
-      throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
-    const size_t tail_smem =
-        (static_cast<size_t>(od) * (c.fc_hidden + 4) + kTailSamples * c.fc_hidden + kTailSamples * kMaxOut) * 4;
+    if (!with_tail) return launches;  // the fused round front reduces the partials next round
     TailParams tp{};
-    tp.part = part;
-    tp.nsplit = nsplit;
-    tp.split_stride = plane;
-    tp.hidden = c.fc_hidden;
-    tp.b1 = P + m.L.fc1_b;
-    tp.w2t = t.w2t.as<float>();
-    tp.b2 = P + m.L.fc2_b;
-    tp.od = od;
+    tp.fc = tc_fc_decode_args(m, samples, fb);
     tp.y = fb.y;
     tp.samples = static_cast<int>(samples);
     if (fuse) tp.dec = *fuse;
-    launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailSamples - 1) / kTailSamples)),
+    const size_t tail_smem = (static_cast<size_t>(tp.fc.od + kTailWarps) * tp.fc.hidden + kTailWarps * kMaxOut) * 4;
+    launch_pdl(fc_tail_kernel, dim3(static_cast<unsigned>((samples + kTailWarps - 1) / kTailWarps)),
                dim3(kTailThreads), tail_smem, s, tp);
     ++launches;
   }
@@ -663,6 +597,48 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
 }
 
 bool tc_fused_front(const TcModel* t) { return t != nullptr && t->chain; }
+
+// Calibration: one fused-front item with no sub-traces (all-zero input)
+// measures the conv1 accumulator row of an all-constant window with the very
+// MMA sequence the rounds use, so skipping that tile later is bit-exact.
+void tc_calibrate(const DevModel& m, cudaStream_t s) {
+  TcModel& t = *m.tc;
+  if (!t.chain) return;
+  FrontParams fp{};
+  fp.first = 0;
+  fp.last = 8;
+  fp.max_context = m.cfg.max_context;
+  fp.calibrate = 1;
+  fp.c1acc_out = static_cast<float*>(t.c1acc.need(64 * sizeof(float)));
+  ForwardBuffers fb{};
+  fb.act[2] = static_cast<float*>(t.calib_out.need(8 * 1024 * sizeof(float)));
+  tc_front(m, fp, fb, s);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaStreamSynchronize(s));
+}
+
+FcDecodeArgs tc_fc_decode_args(const DevModel& m, uint64_t samples, const ForwardBuffers& fb) {
+  const TcModel& t = *m.tc;
+  const ilsim_cnn_config& c = m.cfg;
+  const int esz = t.mode == kBF16 ? 2 : 4;
+  const int total_chunks = (m.L.flat * esz + 127) / 128;
+  const int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
+  if (m.L.out_dim > 64 || c.fc_hidden % 4 != 0) throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
+  if (c.fc_hidden > 256) throw ApiError("fused round front: fc_hidden must be <= 256");
+  FcDecodeArgs a{};
+  a.nsplit = nsplit;
+  a.split_stride = samples * static_cast<uint64_t>(c.fc_hidden);
+  a.part = t.part.as<float>() + fb.part_off * nsplit * static_cast<uint64_t>(c.fc_hidden);
+  a.hidden = c.fc_hidden;
+  a.b1 = m.params.as<float>() + m.L.fc1_b;
+  a.w2t = t.w2t.as<float>();
+  a.b2 = m.params.as<float>() + m.L.fc2_b;
+  a.od = m.L.out_dim;
+  a.class_fetch = c.class_fetch;
+  a.class_exec = c.class_exec;
+  a.class_store = c.class_store;
+  return a;
+}
 
 // Fused round front (K1 apply + gather + conv chain) for the chunk of
 // sub-traces [fp.first, fp.last); writes the flat conv2 output to fb.act[2].
@@ -677,6 +653,7 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
                             t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
   fp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
+  if (!fp.calibrate) fp.c1acc = t.c1acc.as<float>();
   static const int knockout = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
   fp.knockout = knockout;
   launch_round_front(t.mode, w, fp, num_sms(), s);
@@ -757,7 +734,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     cin = cout;
     len = olen;
   }
-  return launches + tc_fc(m, in, samples, fb, s, fuse);
+  return launches + tc_fc(m, in, samples, fb, s, fuse, true);
 }
 
 }  // namespace simnet

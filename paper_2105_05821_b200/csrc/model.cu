@@ -136,7 +136,10 @@ void model_upload(DevModel& m, const ilsim_cnn_config& c, const float* params, i
     tc_model_destroy(m.tc);
     m.tc = nullptr;
   }
-  if (precision != ILSIM_PREC_FP32) m.tc = tc_model_create(m, params, precision, s);
+  if (precision != ILSIM_PREC_FP32) {
+    m.tc = tc_model_create(m, params, precision, s);
+    tc_calibrate(m, s);
+  }
 }
 
 ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, DevBuf& y) {

@@ -86,11 +86,14 @@ bool tc_split_input(const TcModel* t);
 uint32_t tc_act_bytes(const TcModel* t);
 // Fused round front available (C3 chain on the tensor-core path).
 bool tc_fused_front(const TcModel* t);
+void tc_calibrate(const DevModel& m, cudaStream_t s);
 // K1 apply + gather + conv chain in one kernel (round_front.cu); the K1
 // fields of fp are the caller's, the conv fields are filled in here.
 uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, cudaStream_t s);
 // FC1 + FC tail (+ fused K3 when fuse != null) on the flat conv output.
 uint64_t tc_fc(const DevModel& m, const void* flat, uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
-               const DecodeParams* fuse);
+               const DecodeParams* fuse, bool with_tail);
+// Where the fused round front finds the FC1 partials of a chunk (+ FC2 weights).
+FcDecodeArgs tc_fc_decode_args(const DevModel& m, uint64_t samples, const ForwardBuffers& fb);
 
 }  // namespace simnet

@@ -119,9 +119,10 @@ __device__ __forceinline__ void put4(uint8_t* a, uint32_t lo_off, int r, int k, 
   }
 }
 
-// Restage 64 accumulator columns of TMEM lane-row `tl` (one conv output row;
-// `constant`: a skipped all-zero row, accumulator exactly 0) into the A
-// operand at row `ar`, K offset `k0`, with bias + ReLU.
+// Restage 64 accumulator columns of TMEM lane-row `tl` (one conv output row)
+// into the A operand at row `ar`, K offset `k0`, with bias + ReLU.  `accv`
+// non-null: the accumulator row is given (a skipped all-zero conv0 row is
+// exactly 0; a skipped all-constant conv1 row is the calibrated c1acc).
 __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -131,13 +132,13 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
 }
 
 template <int kMode>
-__device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, bool constant, int ar, int k0,
+__device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float* accv, int ar, int k0,
                                             const float* bias) {
   using S = Shape<kMode>;
   uint32_t raw[kC];
-  if (constant) {
+  if (accv) {  // accumulator row known in advance (shared memory), no TMEM read
 #pragma unroll
-    for (int i = 0; i < kC; ++i) raw[i] = 0u;
+    for (int i = 0; i < kC; ++i) raw[i] = __float_as_uint(accv[i]);
   } else {  // all four 16-column loads in flight, one wait
 #pragma unroll
     for (int c0 = 0; c0 < kC; c0 += 16) tmem_ld16_async(tl + c0, raw + c0);
@@ -204,11 +205,15 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __shared__ __align__(8) uint64_t bar_a1, bar_m1; // conv1 A restaged / its MMAs done: 2 / item
   __shared__ __align__(8) uint64_t bar_w1f;        // conv1 MMAs done (W1 free), 1 / item
   __shared__ __align__(8) uint64_t bar_a2, bar_m2; // conv2 A restaged / MMAs done: 1 / item
+  __shared__ __align__(8) uint64_t bar_w2;         // FC2 weights landed in R1 (bulk copy), 1 / item
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[3][kC];
   __shared__ float s_zero[kSlots], s_one[kSlots];
   __shared__ int s_ncols[kItem];  // context columns of each sample this round, -1: inactive
   __shared__ int s_T;             // conv0 tiles needed this item
+  __shared__ float s_zacc[kC];    // zero accumulator row (skipped conv0 tiles)
+  __shared__ float s_c1[kC];      // calibrated conv1 accumulator of a constant row
+  __shared__ double s_lab[6];     // label mean / stdev (decode)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t samples = p.last - p.first;
@@ -222,8 +227,15 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     sbias[l][c] = (l == 0 ? p.b0 : (l == 1 ? p.b1 : p.b2))[c];
   } else if (threadIdx.x < 3 * kC + kSlots) {
     const int k = threadIdx.x - 3 * kC;
-    s_zero[k] = p.nc->zero[k];
-    s_one[k] = p.nc->one[k];
+    s_zero[k] = p.nc ? p.nc->zero[k] : 0.0f;
+    s_one[k] = p.nc ? p.nc->one[k] : 0.0f;
+  } else if (threadIdx.x >= 256 && threadIdx.x < 256 + kC) {
+    const int k = threadIdx.x - 256;
+    s_zacc[k] = 0.0f;
+    s_c1[k] = p.c1acc ? p.c1acc[k] : 0.0f;
+  } else if (threadIdx.x >= 3 * kC + kSlots && threadIdx.x < 3 * kC + kSlots + 6) {
+    const int k = threadIdx.x - 3 * kC - kSlots;
+    s_lab[k] = p.nc ? (k < 3 ? p.nc->label_mean[k] : p.nc->label_sd[k - 3]) : 0.0;
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < 3; ++i) mbar_init(&bar_w[i], 1);
@@ -235,6 +247,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     mbar_init(&bar_w1f, 1);
     mbar_init(&bar_a2, kCompute);
     mbar_init(&bar_m2, 1);
+    mbar_init(&bar_w2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -262,7 +275,20 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       };
       int it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        if (it > 0) mbar_wait(&bar_m2, (it - 1) & 1);  // previous conv2 done: R2 free
+        if (it > 0) mbar_wait(&bar_m2, (it - 1) & 1);  // previous conv2 done: R1, R2 free
+        {  // FC2 weights for the decode of the previous round's predictions (R1 is idle until the gather)
+          const uint32_t bytes = static_cast<uint32_t>(p.fc.od * p.fc.hidden * 4);
+          if (bytes == 0) {
+            mbar_arrive(&bar_w2);
+          } else {
+            mbar_expect_tx(&bar_w2, bytes);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    su32(R1)),
+                "l"(p.fc.w2t), "r"(bytes), "r"(su32(&bar_w2))
+                : "memory");
+          }
+        }
         load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
         mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
         load_w(1, &tmW1, &tmW1lo, S::kKChunks);
@@ -275,7 +301,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     if (lane == 0) {
       const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, kC);
       const uint32_t r1 = su32(R1), r2 = su32(R2);
-      uint32_t n_a0 = 0;
+      uint32_t n_a0 = 0, n_a1 = 0;
       int it = 0;
       auto gemm = [&](uint32_t d, uint32_t alo, int ksteps) {  // A in R1 (lo plane at +alo), W in R2
         for (int s = 0; s < ksteps; ++s) {
@@ -306,9 +332,11 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           mma_commit(&bar_t0);
         }
         mma_commit(&bar_c0);
-        // conv1: two tiles (16 positions x 8 samples each), A restaged by the epilogue
-        for (int u = 0; u < 2; ++u) {
-          mbar_wait(&bar_a1, u);
+        // conv1: two tiles (16 positions x 8 samples each), A restaged by the
+        // epilogue; tile 1 is all-constant (skipped) when every context fits in tiles 0-1
+        const int n_c1 = (T <= 2 && p.c1acc) ? 1 : 2;
+        for (int u = 0; u < n_c1; ++u) {
+          mbar_wait(&bar_a1, n_a1++ & 1);
           if (u == 0) mbar_wait(&bar_w[1], it & 1);
           tc_fence_after();
           gemm(tmem + 256 + u * kC, S::kALo, 4 * S::kKChunks);
@@ -332,7 +360,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const k1::ApplyArgs aa{p.bw, p.max_context, p.per_cycle, 1, p.iflags, p.nc};
     const NormConsts& nc = *p.nc;
-    uint32_t n_t0 = 0;
+    uint32_t n_t0 = 0, n_m1 = 0;
     int it = 0;
     long long* tr = p.trace ? p.trace + blockIdx.x * 32 : nullptr;
     // diagnostics: phase-boundary clocks of the first item, taken after a
@@ -347,16 +375,40 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     asm volatile("griddepcontrol.wait;" ::: "memory");  // SubState / rings of the previous round
     if (tr && tid == 0) tr[15] = clock64();
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      // ---- 1. apply + column table: warp w owns sub-trace item*8 + w ----
+      // ---- 1. decode the previous round (FC tail of the item's 8 samples, all
+      //         warps), then apply + column table: warp w owns sub-trace item*8 + w ----
       {
         const uint64_t s = p.first + static_cast<uint64_t>(item) * kItem + warp;
+        const bool mine = s < p.last && !p.calibrate;
+        // R1 is idle until the gather: W2 (bulk copy) | h [8][hidden] | y [8][64]
+        mbar_wait(&bar_w2, it & 1);
+        if (tr && it == 0 && lane == 0 && warp == 0) tr[24] = clock64();
+        float* hs = reinterpret_cast<float*>(R1) + kFcMaxOut * kFcMaxHidden;
+        float* ys = hs + kItem * kFcMaxHidden;
+        cta8_fc(p.fc, (mine ? s : p.first) - p.first, reinterpret_cast<const float*>(R1), hs, ys,
+                (tr && it == 0) ? tr + 28 : nullptr);
+        if (tr && it == 0 && lane == 0 && warp == 0) tr[25] = clock64();
         int ncs = -1;
-        if (s < p.last) {
+        if (mine) {
           const k1::Rings r = k1::rings_of(p.proc, p.wq, p.pmask, p.wmask, s);
           SubState* sp = p.state + s;
           SubState st = *sp;
+          bool dirty = false;
+          if (st.status == kOk && st.awaiting) {  // K3 of the previous round for this sub-trace
+            uint32_t tri[3];
+            warp_decode_triple(ys + warp * kFcMaxOut, s_lab, p.fc.class_fetch, p.fc.class_exec, p.fc.class_store,
+                               (st.t_flags & kFlagStore) != 0, tri);
+            if (tr && it == 0 && lane == 0 && warp == 0) tr[26] = clock64();
+            apply_decoded_reg(st, tri, p.fc.pred_fetch, p.per_cycle);
+            st.awaiting = 0;
+            dirty = true;
+          }
           if (st.status == kOk && st.has_pend && !(p.knockout & 2)) {
             k1::apply_step(st, r, aa);
+            dirty = true;
+          }
+          if (tr && it == 0 && lane == 0 && warp == 0) tr[27] = clock64();
+          if (dirty) {
             if (lane == 0) *sp = st;
             __syncwarp();
           }
@@ -383,6 +435,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
                                   __uint_as_float(f));
             }
             if (lane == 0) {  // the next round's push carries these into the ring entry
+              sp->awaiting = 1;
               sp->xcols = ncols + 1;
               sp->t_pc = tpc;
               sp->t_addr = taddr;
@@ -475,28 +528,37 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       mbar_wait(&bar_t0, n_t0++ & 1);  // last conv0 tile done: all conv0 accumulators final, R1 free
       tc_fence_after();
       mark(6);
-      for (int u = 0; u < 2; ++u) {
+      const int n_c1 = (T <= 2 && p.c1acc) ? 1 : 2;  // same rule as the MMA warp
+      for (int u = 0; u < n_c1; ++u) {
         if (u == 1) {
-          mbar_wait(&bar_m1, 0);  // conv1 tile 0 consumed R1
+          mbar_wait(&bar_m1, n_m1++ & 1);  // conv1 tile 0 consumed R1
           tc_fence_after();
         }
         // conv0 tile t = 2u + half, row m = (sample m/16, position 16t + m%16)
         //   -> conv1 tile u row (m/16)*16 + 8*half + (m%16)/2, K half (m%2)
         const int t = 2 * u + half;
-        restage_row<kMode>(R1, tmem + lane_off + t * kC, t >= T, (m >> 4) * 16 + 8 * half + ((m & 15) >> 1),
-                           (m & 1) * kC, sbias[0]);
+        restage_row<kMode>(R1, tmem + lane_off + t * kC, t >= T ? s_zacc : nullptr,
+                           (m >> 4) * 16 + 8 * half + ((m & 15) >> 1), (m & 1) * kC, sbias[0]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&bar_a1);
         mark(7 + u);
       }
-      mbar_wait(&bar_m1, 1);
+      mbar_wait(&bar_m1, n_m1++ & 1);  // last conv1 tile done
       tc_fence_after();
       mark(9);
+      if (p.c1acc_out && item == 0 && warp == 0) {  // calibration: conv1 row (sample 0, position 0)
+        uint32_t raw[kC];
+#pragma unroll
+        for (int c0 = 0; c0 < kC; c0 += 16) tmem_ld16_async(tmem + lane_off + 256 + c0, raw + c0);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (lane == 0)
+          for (int c = 0; c < kC; ++c) p.c1acc_out[c] = __uint_as_float(raw[c]);
+      }
       // conv1 tile `half`, row m = (sample m/16, position 16*half + m%16)
       //   -> conv2 row (m/16)*16 + 8*half + (m%16)/2, K half (m%2)
-      restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, false, (m >> 4) * 16 + 8 * half + ((m & 15) >> 1),
-                         (m & 1) * kC, sbias[1]);
+      restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, (half == 1 && n_c1 == 1) ? s_c1 : nullptr,
+                         (m >> 4) * 16 + 8 * half + ((m & 15) >> 1), (m & 1) * kC, sbias[1]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&bar_a2);
@@ -543,6 +605,44 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
+}
+
+// One warp per sub-trace: decode the last outstanding prediction, apply it,
+// drain (simcore.cpp:152-159).
+__global__ void __launch_bounds__(256) final_decode_kernel(FrontParams p) {
+  extern __shared__ __align__(16) float fin_sm[];  // W2 [od][hidden] | h [8][hidden] | y [8][64]
+  __shared__ double s_lab[6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 6) s_lab[threadIdx.x] = threadIdx.x < 3 ? p.nc->label_mean[threadIdx.x] : p.nc->label_sd[threadIdx.x - 3];
+  float* w2s = fin_sm;
+  float* hs = fin_sm + p.fc.od * p.fc.hidden;
+  float* ys = hs + 8 * p.fc.hidden;
+  for (int i = threadIdx.x; i < p.fc.od * p.fc.hidden / 4; i += 256)
+    reinterpret_cast<float4*>(w2s)[i] = __ldg(reinterpret_cast<const float4*>(p.fc.w2t) + i);
+  __syncthreads();
+  const uint64_t s = p.first + static_cast<uint64_t>(blockIdx.x) * 8 + warp;
+  cta8_fc(p.fc, (s < p.last ? s : p.first) - p.first, w2s, hs, ys);
+  if (s >= p.last) return;
+  const k1::ApplyArgs aa{p.bw, p.max_context, p.per_cycle, 1, p.iflags, p.nc};
+  const k1::Rings r = k1::rings_of(p.proc, p.wq, p.pmask, p.wmask, s);
+  SubState* sp = p.state + s;
+  SubState st = *sp;
+  if (st.status == kOk && st.awaiting) {
+    uint32_t tri[3];
+    warp_decode_triple(ys + warp * kFcMaxOut, s_lab, p.fc.class_fetch, p.fc.class_exec, p.fc.class_store,
+                       (st.t_flags & kFlagStore) != 0, tri);
+    apply_decoded_reg(st, tri, p.fc.pred_fetch, p.per_cycle);
+    st.awaiting = 0;
+  }
+  if (st.status == kOk && st.has_pend) k1::apply_step(st, r, aa);
+  if (lane == 0) *sp = st;
+}
+
+void launch_final_decode(const FrontParams& p, cudaStream_t s) {
+  const uint64_t n = p.last - p.first;
+  if (n == 0) return;
+  const size_t sm = (static_cast<size_t>(p.fc.od + 8) * p.fc.hidden + 8 * kFcMaxOut) * 4;
+  final_decode_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, sm, s>>>(p);
 }
 
 namespace {

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "fc_decode.cuh"
 #include "host_util.cuh"
 
 namespace simnet {
@@ -34,6 +35,15 @@ struct FrontParams {
   // row layout [last-first][dump_stride] (rows of 100 floats) — input capture
   float* dump;
   uint32_t dump_stride;
+  // FC tail of the previous round (decoded here, right before its apply step)
+  FcDecodeArgs fc;
+  // conv1 accumulator row of an all-constant input window (conv0 = ReLU(b0) on
+  // both taps), measured once per model by a calibration launch; lets an item
+  // whose contexts fit in 64 columns skip the all-constant conv1 tile.  Null:
+  // never skip.
+  const float* c1acc;
+  float* c1acc_out;          // calibration launch: where to write it
+  int32_t calibrate;         // 1: no sub-traces, all-zero input (calibration)
   long long* trace;          // optional: per-CTA event clocks of the first item (diagnostics)
   int32_t knockout;          // diagnostics only (SIMNET_KNOCKOUT): 1 = no static loads, 2 = no apply
 };
@@ -41,5 +51,8 @@ struct FrontParams {
 // w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
 void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s);
 void round_front_set_attributes();
+// After the last round: decode the outstanding predictions, apply them and
+// drain (the fused-path replacement of the final K1 pass).
+void launch_final_decode(const FrontParams& p, cudaStream_t s);
 
 }  // namespace simnet

@@ -269,6 +269,33 @@ def _fused_cases(port, golden):
                (store_heavy(31, 1500), 3), (read_trace(GOLD / "pointer_chase_2000_s3.trace"), 1)]
 
 
+def _bench_like(regime="default", n=24_000):
+    """The bench's synthetic workload shape at test size: head biases put many
+    decodes on the overflow class (fp64 regression path) and contexts are long."""
+    from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace
+    kind = "memory" if regime == "memory" else "mix"
+    return synthetic_model(synthetic_trace(20_000, 101, kind=kind), 1, regime=regime), synthetic_trace(n, 7, kind=kind)
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+@pytest.mark.parametrize("regime", ["default", "memory"])
+def test_fused_front_bench_workload(gpu, port, precision, regime):
+    """Fused vs unfused bit-exact, and total cycles vs the CPU oracle, on the
+    bench's own synthetic workload (frequent regression decodes, full contexts)."""
+    g = gpu(precision)
+    m, t = _bench_like(regime)
+    g.load_model(m)
+    pc = pcfg(64)
+    g.load_trace(t, pc)
+    a = g.run(pc)
+    b = g.run(pc, fused=False)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    if precision == "tf32x3":
+        want = port.simulate(t, m, k=64)
+        assert abs(a.total_cycles - want["total_cycles"]) <= 1e-3 * want["total_cycles"]
+        assert np.mean(a.predicted_fetch == want["predicted_fetch"]) >= 0.999
+
+
 @pytest.mark.parametrize("precision", ["tf32x3", "bf16", "tf32"])
 def test_fused_front_matches_unfused(gpu, port, golden, precision):
     """The fused round front (gather straight into the conv0 operand, skipped
@@ -315,3 +342,20 @@ def test_fused_front_inputs_bit_exact(gpu, port, golden, precision):
             assert np.array_equal(buf[: rows.size], want["cap_inputs"][rows]), f"round {r}"
             checked += 1
         assert checked >= 2, (first_bad, precision)
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_chunked_rounds_match(gpu, port, golden, precision, monkeypatch):
+    """Batches larger than one chunk (65536 sub-traces in production; 24 here)
+    run chunk after chunk each round; results must not change."""
+    g = gpu(precision)
+    m, _ = _fused_cases(port, golden)
+    g.load_model(m)
+    t = read_trace(GOLD / "branchy_2000_s8.trace")
+    pc = pcfg(100)
+    g.load_trace(t, pc)
+    a = g.run(pc)
+    monkeypatch.setenv("SIMNET_CHUNK", "24")
+    for fused in (True, False):
+        b = g.run(pc, fused=fused)
+        assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)

@@ -19,6 +19,9 @@ for prec in ("tf32x3", "bf16"):
     print(prec, "T histogram", np.bincount(T.astype(int)))
     ap = tr[:, 16:24] - base
     print(f"  apply per warp: median {np.median(ap):.0f}, max over warps median {np.median(ap.max(1)):.0f}")
+    for i, n in ((24, "W2 landed w0"), (28, "h ready (synced)"), (25, "cta8 fc done w0"), (26, "decode done w0"), (27, "apply done w0")):
+        col = (tr[:, i] - base[:, 0])[tr[:, i] > 0]
+        if col.size: print(f"  {n:18s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
     for i in (0, 15, 16, 1, 2, 3, 6, 7, 8, 9, 10, 11, 12):
         col = (tr[:, i] - base[:, 0])[tr[:, i] > 0]
         if col.size: print(f"  {names[i]:18s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
