@@ -34,6 +34,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 MFLOP_C3 = 2 * 1_073_408  # 2 x model_flops(preset_c3), cnn.cpp:319-333
+CONV_MACS_C3 = 64 * 64 * 100 + 32 * 64 * 128 + 16 * 64 * 128  # conv0-2 multiplications per instruction (802,816)
 N_INSTR = 10_000_000
 K_SUB = 1024
 
@@ -106,6 +107,15 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def ncu_traffic(precision: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    try:
+        return json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).get(precision)
+    except (OSError, ValueError):
+        return None
 
 
 def peaks():
@@ -254,24 +264,35 @@ def main():
     n_all = tot.instructions
     value = n_all / (step_ms_max / 1e3) / 1e6
 
-    # kernel breakdown + roofline of the dominant kernel (instrumented pass)
+    # kernel breakdown + roofline of the dominant kernel (instrumented pass:
+    # events around every launch of every round, no graphs)
     prof = g.run(pc, profile=True)
     rounds = max(prof.rounds, 1)
-    k_ms = {"context": prof.kernel_ms[0], "inference": prof.kernel_ms[1], "decode": prof.kernel_ms[2]}
-    infer_ms_round = prof.kernel_ms[1] / rounds
-    flops_round = MFLOP_C3 * args.k
-    pk = peaks()
     tc = args.precision != "fp32"
+    if tc:  # fused round: front (K3 of the previous round + K1 + conv chain) -> FC1
+        k_ms = {"round_front": prof.kernel_ms[0], "fc1": prof.kernel_ms[1]}
+        dom_ms, dom_name = prof.kernel_ms[0], "round_front_kernel (K3 decode + K1 apply/gather + conv0-2 chain)"
+        flops_launch = CONV_MACS_C3 * 2 * args.k
+    else:
+        k_ms = {"context": prof.kernel_ms[0], "inference": prof.kernel_ms[1], "decode": prof.kernel_ms[2]}
+        dom_ms, dom_name = prof.kernel_ms[1], "K2 inference (SIMT fp32, all layers)"
+        flops_launch = MFLOP_C3 * args.k
+    launch_ms = dom_ms / rounds
+    pk = peaks()
     if tc:
-        peak_val, peak_src = pk.get("bf16_tflops_sustained", 1400.0) / (1.0 if args.precision == "bf16" else 2.0), \
-            "MEASURED_PEAKS.json bf16_tflops_sustained" + ("" if args.precision == "bf16" else " / 2 (tf32 rate)")
+        div = 1.0 if args.precision == "bf16" else 2.0
+        peak_val = pk.get("bf16_tflops_sustained", 1365.8) / div
+        peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" + ("" if div == 1.0 else " / 2 (tf32 rate)")
+        if args.precision == "tf32x3":
+            peak_src += "; 3xTF32 issues 3 tensor ops per algorithmic op"
     else:
         sm_mhz = pk.get("sm_max_mhz", 1965.0)
         peak_val, peak_src = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "derived FFMA peak 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
-    achieved = flops_round / (infer_ms_round / 1e3) / 1e12
-    roofline = {"bound": "tensor" if tc else "fp32-ffma", "kernel": "K2 inference (per round, all layers)",
-                "achieved": achieved, "peak": peak_val, "unit": "TFLOP/s", "frac": achieved / peak_val,
-                "peak_source": peak_src, "traffic": None}
+    achieved = flops_launch / (launch_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor" if tc else "fp32-ffma", "kernel": dom_name, "achieved": achieved, "peak": peak_val,
+                "unit": "TFLOP/s", "frac": achieved / peak_val, "peak_source": peak_src,
+                "algorithmic_flops_per_launch": flops_launch, "launch_us": 1e3 * launch_ms,
+                "traffic": ncu_traffic(args.precision)}
 
     # e2e through the public C-ABI with host buffers (pinned), copies inside
     e2e_line = None
