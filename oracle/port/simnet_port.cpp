@@ -40,9 +40,12 @@ struct Net {
   int out_dim = 0, flat = 0;
 
   explicit Net(const port_model* mm) : m(mm) {
-    if (m->n_conv < 1 || m->n_conv > 8) throw PortError("at least one conv layer required");
+    // n_conv == 0: the FC-only predictor (paper FC2), an extension
+    // with no reference implementation: FC1 reads the unpadded input.
+    if (m->n_conv < 0 || m->n_conv > 8) throw PortError("conv layer count out of range");
     out_dim = 3 + m->class_fetch + m->class_exec + m->class_store;
-    flat = m->conv[m->n_conv - 1] * (m->sequence_length >> m->n_conv);
+    flat = m->n_conv == 0 ? m->input_channels * (m->max_context + 1)
+                          : m->conv[m->n_conv - 1] * (m->sequence_length >> m->n_conv);
     size_t off = 0;
     int cin = m->input_channels;
     for (int l = 0; l < m->n_conv; ++l) {

@@ -98,8 +98,8 @@ def partition_starts(n: int, k: int) -> list[int]:
 
 
 def _cnn_cfg(c: CnnConfig) -> _lib.CnnCfg:
-    if not 1 <= len(c.conv_channels) <= 8:
-        raise IlsimError("at least one conv layer required")
+    if len(c.conv_channels) > 8:
+        raise IlsimError("at most 8 conv layers supported")
     cfg = _lib.CnnCfg()
     cfg.input_channels = c.input_channels
     cfg.max_context = c.max_context
@@ -122,6 +122,8 @@ def model_flops(cfg: CnnConfig | str = "c3") -> int:
         cfg = CnnConfig.preset_c3()
         if name == "c3-rb":
             cfg.residual_blocks = True
+        elif name == "fc2":
+            cfg = CnnConfig.preset_fc2()
         elif name != "c3":
             raise IlsimError("unknown preset: " + name)
     return int(_lib.lib().ilsim_gpu_model_flops(C.byref(_cnn_cfg(cfg))))

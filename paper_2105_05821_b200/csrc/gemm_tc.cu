@@ -473,6 +473,7 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   const ilsim_cnn_config& c = m.cfg;
   const int mode = mode_of(precision);
   const int esz = mode == kBF16 ? 2 : 4;
+  if (c.n_conv == 0) throw ApiError("tensor-core path: the FC-only predictor runs with precision fp32");
   // constraints of this kernel family (the FP32 SIMT path has none)
   int cin = c.input_channels;
   for (int l = 0; l < c.n_conv; ++l) {

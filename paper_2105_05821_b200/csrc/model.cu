@@ -10,7 +10,10 @@ namespace simnet {
 ParamLayout param_layout(const ilsim_cnn_config& c) {  // cnn.cpp:44-86
   ParamLayout L;
   L.out_dim = 3 + c.class_fetch + c.class_exec + c.class_store;
-  L.flat = c.conv[c.n_conv - 1] * (c.sequence_length >> c.n_conv);
+  // n_conv == 0: the FC-only predictor (extension; PAPER.md:794 FC2), FC1 on
+  // the unpadded input of 50 x (max_context + 1) slots
+  L.flat = c.n_conv == 0 ? c.input_channels * (c.max_context + 1)
+                         : c.conv[c.n_conv - 1] * (c.sequence_length >> c.n_conv);
   uint64_t off = 0;
   int cin = c.input_channels;
   for (int l = 0; l < c.n_conv; ++l) {
@@ -41,7 +44,7 @@ ParamLayout param_layout(const ilsim_cnn_config& c) {  // cnn.cpp:44-86
 void validate_config(const ilsim_cnn_config& c) {
   if (c.input_channels < 1) throw ApiError("input_channels must be >= 1");
   if (c.max_context < 0) throw ApiError("max_context must be >= 0");
-  if (c.n_conv < 1) throw ApiError("at least one conv layer required");
+  if (c.n_conv < 0) throw ApiError("conv layer count must be >= 0");
   if (c.n_conv > 8) throw ApiError("at most 8 conv layers supported");
   for (int l = 0; l < c.n_conv; ++l)
     if (c.conv[l] < 1) throw ApiError("conv channel counts must be >= 1");
@@ -227,7 +230,7 @@ uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32
   f1.rows_per_sample = 1;
   f1.valid_rows = 1;
   f1.kdim = m.L.flat;
-  f1.sample_stride = m.L.flat;
+  f1.sample_stride = c.n_conv == 0 ? x_stride : m.L.flat;  // FC-only: FC1 reads the gathered rows
   f1.w = P + m.L.fc1_w;
   f1.bias = P + m.L.fc1_b;
   f1.c = fb.act[c.n_conv];

@@ -146,6 +146,10 @@ class CnnConfig:
 
     @property
     def flat_dim(self) -> int:
+        # FC-only predictor (extension, no reference implementation): FC1 reads
+        # the unpadded input, 50 slots x (max_context + 1) columns
+        if not self.conv_channels:
+            return self.input_channels * (self.max_context + 1)
         return self.conv_channels[-1] * self.final_positions
 
     @staticmethod
@@ -155,6 +159,18 @@ class CnnConfig:
         while seq < max_context + 1:
             seq <<= 1
         return CnnConfig(max_context=max_context, sequence_length=max(seq, 1 << 3))
+
+    @staticmethod
+    def preset_fc2(max_context: int = 110, hidden: int = 1024) -> "CnnConfig":
+        """The paper's FC2 latency predictor: 5550 -> 1024 -> 33,
+        5,716,992 multiplications.  No reference implementation (the reference's
+        validate_or_throw rejects zero conv layers, cnn.cpp:245): an extension
+        defined identically here, in the oracle port and on the GPU."""
+        seq = 1
+        while seq < max_context + 1:
+            seq <<= 1
+        return CnnConfig(max_context=max_context, sequence_length=max(seq, 1 << 3), conv_channels=[],
+                         fc_hidden=hidden)
 
     def hash(self) -> int:
         """``CnnConfig::hash`` (cnn.cpp:245-259): FNV-1a over u64 fields."""
