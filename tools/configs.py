@@ -1,0 +1,124 @@
+"""Runs BASELINE.json's other configurations on one GPU and prints JSON lines
+(the bench line covers c2).  Synthetic traces / random-init weights as bench.py.
+
+  python tools/configs.py [--only c1,c3,c4,c5] [--precision tf32x3]
+
+c1  FC-only predictor (paper FC2), one sub-trace (sequential), GPU fp32 path,
+    next to the CPU oracle port on a bounded sample.
+c3  per-GPU shard of the 8-GPU config: 100M instructions / 65,536 sub-traces
+    over 8 GPUs = 12.5M instructions as 8,192 sub-traces per GPU.
+c4  memory-heavy regime (store head active, long queues, full contexts).
+c5  sub-trace count sweep x warm-up overlap x drain-trim: MIPS vs CPI error
+    against the K=1 run with the same weights (acceptance_main.cpp:326-334).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig  # noqa: E402
+from paper_2105_05821_b200.formats import CnnConfig, Model  # noqa: E402
+from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace  # noqa: E402
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def run(g, t, pc, reps=2):
+    g.load_trace(t, pc)
+    r = None
+    for _ in range(reps):
+        r = g.run(pc)
+    return r
+
+
+def c1(args):
+    from oracle.oracle import Port
+
+    t = synthetic_trace(args.c1_n, 101)
+    base = synthetic_model(synthetic_trace(200_000, 101), 1)
+    cfg = CnnConfig.preset_fc2()
+    port = Port()
+    m = Model(cfg, base.norm, port.init_params(cfg, 1))
+    g = GpuSimulator(0, "fp32")
+    g.load_model(m)
+    pc = ParallelConfig(k=1, sim=SimConfig(max_context=cfg.max_context))
+    r = run(g, t, pc, reps=1)
+    n_cpu = min(args.c1_n, 2000)
+    t0 = time.perf_counter()
+    want = port.simulate(t.slice(0, n_cpu), m, sequential=True)
+    cpu_s = time.perf_counter() - t0
+    emit({"config": "c1", "predictor": "FC2 5550-1024-33 (5,716,992 mults)", "precision": "fp32 (SIMT)",
+          "instructions": t.n, "sub_traces": 1, "gpu_mips": t.n / (r.device_ms / 1e3) / 1e6, "gpu_cpi": r.cpi,
+          "cpu_port_mips": n_cpu / cpu_s / 1e6, "cpu_sample_instructions": n_cpu,
+          "cpu_port_cpi_on_sample": want["total_cycles"] / n_cpu})
+
+
+def c3(args):
+    n, k = 12_500_000, 8192
+    t = synthetic_trace(n, 101)
+    m = synthetic_model(synthetic_trace(200_000, 101), 1)
+    g = GpuSimulator(0, args.precision)
+    g.load_model(m)
+    r = run(g, t, ParallelConfig(k=k, sim=SimConfig(max_context=m.config.max_context)))
+    emit({"config": "c3 (per-GPU shard)", "precision": args.precision, "instructions": n, "sub_traces": k,
+          "rounds": r.rounds, "mips_per_gpu": n / (r.device_ms / 1e3) / 1e6,
+          "us_per_round": 1e3 * r.device_ms / r.rounds, "cpi": r.cpi,
+          "note": "8 GPUs run 8 such shards with no communication until one all-reduce of the totals"})
+
+
+def c4(args):
+    n, k = 2_000_000, 1024
+    t = synthetic_trace(n, 101, kind="memory")
+    m = synthetic_model(synthetic_trace(200_000, 101, kind="memory"), 1, regime="memory")
+    g = GpuSimulator(0, args.precision)
+    g.load_model(m)
+    r = run(g, t, ParallelConfig(k=k, sim=SimConfig(max_context=m.config.max_context)))
+    emit({"config": "c4 memory-heavy", "precision": args.precision, "instructions": n, "sub_traces": k,
+          "mips": n / (r.device_ms / 1e3) / 1e6, "us_per_round": 1e3 * r.device_ms / r.rounds, "cpi": r.cpi,
+          "overflow_stall_cycles": sum(s.overflow_stall_cycles for s in r.sub_results),
+          "drain_cycles": sum(s.drain_cycles for s in r.sub_results)})
+
+
+def c5(args):
+    n = args.c5_n
+    t = synthetic_trace(n, 101)
+    m = synthetic_model(synthetic_trace(200_000, 101), 1)
+    g = GpuSimulator(0, args.precision)
+    g.load_model(m)
+    mc = m.config.max_context
+    ref = run(g, t, ParallelConfig(k=1, sim=SimConfig(max_context=mc)), reps=1)
+    emit({"config": "c5 reference", "precision": args.precision, "instructions": n, "sub_traces": 1, "cpi": ref.cpi,
+          "mips": n / (ref.device_ms / 1e3) / 1e6})
+    for k in (1024, 4096, 16384, 65536, 262144):
+        if k > n:
+            continue
+        for w in (0, 110, 500):
+            for trim in (False, True):
+                pc = ParallelConfig(k=k, warmup=w, drain_trim=trim, sim=SimConfig(max_context=mc))
+                r = run(g, t, pc)
+                emit({"config": "c5", "precision": args.precision, "instructions": n, "sub_traces": k, "warmup": w,
+                      "drain_trim": trim, "mips_owned": n / (r.device_ms / 1e3) / 1e6, "rounds": r.rounds,
+                      "cpi": r.cpi, "cpi_error_pct_vs_k1": 100.0 * (r.cpi - ref.cpi) / ref.cpi})
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--only", default="c1,c3,c4,c5")
+    p.add_argument("--precision", default="tf32x3")
+    p.add_argument("--c1-n", type=int, default=20_000)
+    p.add_argument("--c5-n", type=int, default=1_000_000)
+    args = p.parse_args()
+    for name in args.only.split(","):
+        globals()[name.strip()](args)
+
+
+if __name__ == "__main__":
+    main()

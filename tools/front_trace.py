@@ -22,6 +22,7 @@ for prec in ("tf32x3", "bf16"):
     for i, n in ((24, "W2 landed w0"), (28, "h ready (synced)"), (25, "cta8 fc done w0"), (26, "decode done w0"), (27, "apply done w0")):
         col = (tr[:, i] - base[:, 0])[tr[:, i] > 0]
         if col.size: print(f"  {n:18s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
-    for i in (0, 15, 16, 1, 2, 3, 6, 7, 8, 9, 10, 11, 12):
+    names.update({21: "fc1 barrier enter", 22: "fc1 barrier exit", 23: "fc1 MMAs done", 31: "fc1 partials written"})
+    for i in (0, 15, 16, 1, 2, 3, 6, 7, 8, 9, 10, 11, 12, 21, 22, 23, 31):
         col = (tr[:, i] - base[:, 0])[tr[:, i] > 0]
         if col.size: print(f"  {names[i]:18s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
