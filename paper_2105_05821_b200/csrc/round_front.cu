@@ -29,6 +29,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "k1_device.cuh"
 #include "launch.cuh"
 #include "round_front.cuh"
@@ -239,7 +241,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t samples = p.last - p.first;
-  const int n_items = static_cast<int>((samples + kItem - 1) / kItem);
+  const int spi = p.spi;  // sub-traces per item: rows s*16.. of an operand tile for s < spi, zero above
+  const int n_items = static_cast<int>((samples + spi - 1) / spi);
   // PDL: the FC kernels may launch now (their prologue only touches weights);
   // this kernel's prologue (barriers, TMEM, biases, W0) overlaps the previous
   // round's tail, and only the compute warps wait for its results.
@@ -474,8 +477,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       // ---- 1. decode the previous round (FC tail of the item's 8 samples, all
       //         warps), then apply + column table: warp w owns sub-trace item*8 + w ----
       {
-        const uint64_t s = p.first + static_cast<uint64_t>(item) * kItem + warp;
-        const bool mine = s < p.last && !p.calibrate;
+        const uint64_t s = p.first + static_cast<uint64_t>(item) * spi + warp;
+        const bool mine = warp < spi && s < p.last && !p.calibrate;
         // R1 is idle until the gather: W2 (bulk copy) | h [8][hidden] | y [8][64]
         if (tr && it == 0 && lane == 0 && warp == 0) tr[24] = clock64();
         float* hs = reinterpret_cast<float*>(R1) + kFcMaxOut * kFcMaxHidden;
@@ -607,8 +610,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         }
         if (p.dump) {
           const int row = t * kRowsT + (lane >> 1);
-          const uint64_t smp = static_cast<uint64_t>(item) * kItem + warp;
-          if (smp < samples && (row + 1) * 100 <= static_cast<int>(p.dump_stride)) {
+          const uint64_t smp = static_cast<uint64_t>(item) * spi + warp;
+          if (warp < spi && smp < samples && (row + 1) * 100 <= static_cast<int>(p.dump_stride)) {
             float* o = p.dump + smp * p.dump_stride + row * 100 + 50 * h;
 #pragma unroll
             for (int k = 0; k < kSlots; k += 2) *reinterpret_cast<float2*>(o + k) = make_float2(v[k], v[k + 1]);
@@ -663,14 +666,14 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       mbar_wait(&bar_m2, it & 1);
       tc_fence_after();
       mark(11);
-      const uint64_t sample = static_cast<uint64_t>(item) * kItem + (m >> 4);
+      const uint64_t sample = static_cast<uint64_t>(item) * spi + (m >> 4);
       for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + lane_off + 384 + c0, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
-        if (sample < samples) {
-          const uint64_t off = static_cast<uint64_t>(item) * (kItem * 16 * kC) + m * kC + c0;
+        if ((m >> 4) < spi && sample < samples) {
+          const uint64_t off = sample * (16 * kC) + (m & 15) * kC + c0;
           if (kMode == kBF16) {
             uint4 pk[2];
             uint32_t* w = reinterpret_cast<uint32_t*>(pk);
@@ -808,11 +811,26 @@ namespace {
 size_t front_smem_bytes() { return kR1 + kR2 + kTbl + 1024; }
 }  // namespace
 
-void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s) {
-  const uint64_t samples = p.last - p.first;
+void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& pin, int num_sms, cudaStream_t s) {
+  const uint64_t samples = pin.last - pin.first;
   if (samples == 0) return;
+  FrontParams p = pin;
+  // Sub-traces per work item (SIMNET_SPI overrides; default 8).  Spreading
+  // K = 1024 as 147 items of 7 over every SM measured no faster than 128 items
+  // of 8: an item's round is latency-bound, not throughput-bound.
+  if (p.spi == 0) {
+    static const int env = std::getenv("SIMNET_SPI") ? std::atoi(std::getenv("SIMNET_SPI")) : 0;
+    if (env > 0) {
+      p.spi = env > kItem ? kItem : env;
+    } else if (env < 0) {
+      const uint64_t per = (samples + num_sms - 1) / num_sms;
+      p.spi = static_cast<int32_t>(per < 1 ? 1 : (per > kItem ? kItem : per));
+    } else {
+      p.spi = kItem;
+    }
+  }
   if (p.max_context + 1 > kTblCols) throw ApiError("fused round front: max_context too large");
-  const uint64_t items = (samples + kItem - 1) / kItem;
+  const uint64_t items = (samples + p.spi - 1) / p.spi;
   const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
   const size_t sm = front_smem_bytes();
   // The in-kernel FC1 phase needs every CTA resident (grid barrier): launched

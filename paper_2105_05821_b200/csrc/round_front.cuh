@@ -44,6 +44,7 @@ struct FrontParams {
   const float* c1acc;
   float* c1acc_out;          // calibration launch: where to write it
   int32_t calibrate;         // 1: no sub-traces, all-zero input (calibration)
+  int32_t spi;               // sub-traces per work item (1..8; set by the launcher)
   long long* trace;          // optional: per-CTA event clocks of the first item (diagnostics)
   int32_t knockout;          // diagnostics only (SIMNET_KNOCKOUT): 1 = no static loads, 2 = no apply
   // FC1 of this round, after a grid barrier (every CTA's flat written): tile =

@@ -381,3 +381,24 @@ def test_fc1_in_front_matches():
     ) % str(GOLD.parents[1])
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert out.stdout.strip().endswith("1"), out.stdout + out.stderr
+
+
+def test_items_of_fewer_samples_match():
+    """Work items of 3 sub-traces (SIMNET_SPI=3: partially filled operand tiles)
+    give the same bits as items of 8."""
+    import subprocess
+    import sys
+    code = (
+        "import os, sys, numpy as np\\n"
+        "sys.path.insert(0, %r)\\n"
+        "os.environ['SIMNET_SPI'] = '3'\\n"
+        "from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig\\n"
+        "from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace\\n"
+        "m = synthetic_model(synthetic_trace(20000, 101), 1); t = synthetic_trace(24000, 7)\\n"
+        "g = GpuSimulator(0, 'tf32x3'); g.load_model(m)\\n"
+        "pc = ParallelConfig(k=100, sim=SimConfig(max_context=110)); g.load_trace(t, pc)\\n"
+        "a = g.run(pc); b = g.run(pc, fused=False)\\n"
+        "print(int(np.array_equal(a.predicted_fetch, b.predicted_fetch) and a.total_cycles == b.total_cycles))\\n"
+    ) % str(GOLD.parents[1])
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.stdout.strip().endswith("1"), out.stdout + out.stderr
