@@ -557,6 +557,13 @@ int simnet_debug_chain_trace(long long* out) {
   return cudaMemcpy(out, p, 148 * 32 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
 }
 
+// Diagnostics only: copy n words of the trace buffer (front + FC1 event clocks).
+int simnet_debug_chain_trace_full(long long* out, int n) {
+  long long* p = chain_trace_ptr();
+  if (!p) return 1;
+  return cudaMemcpy(out, p, static_cast<size_t>(n) * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
+
 int ilsim_gpu_abi_version(void) { return ILSIM_GPU_ABI_VERSION; }
 
 int ilsim_gpu_create(const ilsim_gpu_options* o, ilsim_gpu_ctx** out, char* err, int errlen) {

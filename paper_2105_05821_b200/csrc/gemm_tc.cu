@@ -63,6 +63,8 @@ struct TcGemmParams {
   int ldo;
   int out_bf16;
   uint64_t out_split_stride;  // elements between split-K partial planes
+  long long* trace;           // diagnostics (SIMNET_CHAIN_TRACE): per-CTA event clocks, 16 per CTA
+  int stages;                 // A ring depth (2..kStages; 0 = kStages)
 };
 
 template <int kMode>
@@ -76,7 +78,8 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint8_t* sW = base;                                      // [chunks][n x 128 B]
   uint8_t* sWlo = sW + p.chunks * bBytes;                  // tf32x3 only
   uint8_t* sA = sWlo + (kSplit ? p.chunks * bBytes : 0);   // [stages][16 KB]
-  uint8_t* sAlo = sA + kStages * kAChunk;                  // tf32x3 only
+  const int ns = p.stages > 0 ? p.stages : kStages;       // A ring depth
+  uint8_t* sAlo = sA + ns * kAChunk;                       // tf32x3 only
 
   __shared__ __align__(8) uint64_t bar_w;
   __shared__ __align__(8) uint64_t bar_full[kStages], bar_split[kStages], bar_empty[kStages];
@@ -113,6 +116,9 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const int elems = kMode == kBF16 ? 64 : 32;  // elements per 128 B chunk
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  long long* tr = p.trace ? p.trace + 148 * 32 + cta * 16 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = clock64();
   // PDL: let the next kernel start its prologue; everything above overlapped
   // the previous kernel.  Weights are constants and may be fetched before the
   // dependency wait; activations only after it.
@@ -138,7 +144,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tma_load_3d(sA + stage * kAChunk, &tmA, &bar_full[stage], kx, 0, t * p.a_samples_box);
           else
             tma_load_2d(sA + stage * kAChunk, &tmA, &bar_full[stage], kx, t * kBM);
-          if (++stage == kStages) {
+          if (++stage == ns) {
             stage = 0;
             phase ^= 1;
           }
@@ -148,6 +154,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   } else if (warp == 1) {
     if (lane == 0) {
       mbar_wait(&bar_w, 0);
+      if (tr) tr[1] = clock64();
       const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, p.n);
       int stage = 0;
       uint32_t phase = 0;
@@ -160,6 +167,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t d = tmem + acc * p.n;
         for (int c = 0; c < p.chunks; ++c) {
           mbar_wait(kSplit ? &bar_split[stage] : &bar_full[stage], phase);
+          if (tr && it == 0 && c == 0) tr[2] = clock64();
           tc_fence_after();
           const int steps = c == p.chunks - 1 ? p.ksteps_last : 4;
           for (int j = 0; j < steps; ++j) {
@@ -176,12 +184,13 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
           }
           mma_commit(&bar_empty[stage]);  // the stage is free once these MMAs retire
-          if (++stage == kStages) {
+          if (++stage == ns) {
             stage = 0;
             phase ^= 1;
           }
         }
         mma_commit(&bar_acc_full[acc]);
+        if (tr && it < 2) tr[3 + 2 * it] = clock64();
       }
     }
     __syncwarp();
@@ -215,7 +224,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_arrive(&bar_split[stage]);
-          if (++stage == kStages) {
+          if (++stage == ns) {
             stage = 0;
             phase ^= 1;
           }
@@ -264,6 +273,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
+      if (tr && warp == 6 && lane == 0 && it < 2) tr[4 + 2 * it] = clock64();
     }
   }
   tc_fence_before();
@@ -439,9 +449,9 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
 }
 
-size_t smem_bytes(int mode, int n, int chunks) {
+size_t smem_bytes(int mode, int n, int chunks, int stages) {
   const size_t w = static_cast<size_t>(chunks) * n * 128 * (mode == kTF32x3 ? 2 : 1);
-  const size_t a = static_cast<size_t>(kStages) * kAChunk * (mode == kTF32x3 ? 2 : 1);
+  const size_t a = static_cast<size_t>(stages > 0 ? stages : kStages) * kAChunk * (mode == kTF32x3 ? 2 : 1);
   return w + a + 1024;
 }
 
@@ -461,7 +471,7 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   const int groups = ny * nz;
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
-  const size_t sm = smem_bytes(mode, p.n, p.chunks);
+  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages);
   if (mode == kBF16) launch_pdl(tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
   else if (mode == kTF32) launch_pdl(tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
   else launch_pdl(tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
@@ -493,7 +503,7 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   conv_chain_set_attributes();
   round_front_set_attributes();
   if (std::getenv("SIMNET_CHAIN_TRACE") && !chain_trace_ptr())  // diagnostics buffer, allocated outside capture
-    CUDA_OK(cudaMalloc(&chain_trace_ptr(), 148 * 32 * sizeof(long long)));
+    CUDA_OK(cudaMalloc(&chain_trace_ptr(), (148 * 32 + 256 * 16) * sizeof(long long)));
   auto* t = new TcModel();
   t->mode = mode;
   t->chain = c.n_conv == 3 && c.conv[0] == 64 && c.conv[1] == 64 && c.conv[2] == 64 && c.input_channels == 50 &&
@@ -526,16 +536,26 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
 
 void tc_model_destroy(TcModel* t) { delete t; }
 
+// 128-B K chunks per FC1 split-K plane (C3 flat dim: 8 planes for the f32
+// modes, 4 for bf16).  8 chunks per plane (one M tile per CTA, but only a
+// 2-stage A ring fits next to the 128 KB 3xTF32 W slice) measured slower:
+// the A loads are TMA-latency-bound and need the 4-stage ring.
+int fc1_cps(int mode) {
+  (void)mode;
+  return kMaxChunks;
+}
+
 // Allocations the forward needs, done before any graph capture.
 void tc_prepare(const DevModel& m, uint64_t samples) {
   TcModel& t = *m.tc;
   const int esz = t.mode == kBF16 ? 2 : 4;
   const int total_chunks = (m.L.flat * esz + 127) / 128;
-  const int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
+  const int nsplit = (total_chunks + fc1_cps(t.mode) - 1) / fc1_cps(t.mode);
   t.part.need(samples * static_cast<uint64_t>(m.cfg.fc_hidden) * nsplit * sizeof(float));
 }
 
 bool tc_split_input(const TcModel* t) { return t->chain && t->mode == kTF32x3; }
+
 uint32_t tc_act_bytes(const TcModel* t) { return t->mode == kBF16 ? 2u : 4u; }
 
 // FC1 (split-K tcgen05 partials) and the FC tail (FC2 + fused K3) on the
@@ -554,7 +574,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
   // FC1 split-K partials
   const int flat = m.L.flat;
   const int total_chunks = (flat * esz + 127) / 128;
-  const int per = kMaxChunks;
+  const int per = fc1_cps(mode);
   const int nsplit = (total_chunks + per - 1) / per;
   const int fc_tile = t.fc1.npad >= 64 ? 64 : t.fc1.npad;
   {
@@ -573,12 +593,14 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.n = fc_tile;
     p.chunks = per;
     p.ksteps_last = 4;
+    p.stages = (mode == kTF32x3 && per > 4) ? 2 : kStages;
     p.bias = nullptr;
     p.relu = 0;
     p.out = part;
     p.ldo = c.fc_hidden;
     p.out_bf16 = 0;
     p.out_split_stride = plane;
+    p.trace = chain_trace_ptr();
     if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
     launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
@@ -632,7 +654,7 @@ void tc_fc1_front_params(const DevModel& m, FrontParams& fp, uint32_t* gbar) {
   if (!tc_fc1_in_front(m)) return;
   const uint64_t samples = fp.last - fp.first;
   const int nsplit = fp.fc.nsplit;
-  fp.fc1_cps = kMaxChunks;
+  fp.fc1_cps = fc1_cps(m.tc->mode);
   fp.fc1_sp = nsplit >= 8 ? 2 : 1;  // 3xTF32 / tf32: 8 planes as 4 pairs; bf16: 4 planes
   fp.fc1_ntiles = m.cfg.fc_hidden / 64;
   fp.fc1_mtiles = static_cast<int>((samples + kBM - 1) / kBM);
@@ -648,7 +670,7 @@ FcDecodeArgs tc_fc_decode_args(const DevModel& m, uint64_t samples, const Forwar
   const ilsim_cnn_config& c = m.cfg;
   const int esz = t.mode == kBF16 ? 2 : 4;
   const int total_chunks = (m.L.flat * esz + 127) / 128;
-  const int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
+  const int nsplit = (total_chunks + fc1_cps(t.mode) - 1) / fc1_cps(t.mode);
   if (m.L.out_dim > 64 || c.fc_hidden % 4 != 0) throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
   if (c.fc_hidden > 256) throw ApiError("fused round front: fc_hidden must be <= 256");
   FcDecodeArgs a{};

@@ -1,0 +1,31 @@
+# diagnostics: FC1 (tc_layer_kernel) per-CTA event clocks in graph mode (SIMNET_CHAIN_TRACE=1)
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+os.environ["SIMNET_CHAIN_TRACE"] = "1"
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, _lib  # noqa: E402
+from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace  # noqa: E402
+
+t = synthetic_trace(300_000, 101)
+m = synthetic_model(synthetic_trace(200_000, 101), 1)
+for prec in ("tf32x3", "bf16"):
+    g = GpuSimulator(0, prec)
+    g.load_model(m)
+    pc = ParallelConfig(k=1024)
+    g.load_trace(t, pc)
+    g.run(pc)
+    buf = np.zeros(148 * 32 + 256 * 16, np.int64)
+    _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
+    tr = buf[148 * 32:].reshape(256, 16)[:128].astype(np.float64)
+    rel = tr[:, :8] - tr[:, :1]
+    names = ["start", "W landed", "A chunk0 ready", "tile0 MMAs issued", "tile0 epilogue done", "tile1 MMAs issued",
+             "tile1 epilogue done"]
+    print(prec)
+    for i, n in enumerate(names):
+        col = rel[:, i][tr[:, i] > 0]
+        if col.size:
+            print(f"  {n:20s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
