@@ -491,7 +491,6 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
     if (c.conv[l] % 16 != 0 || (c.conv[l] > 128 && c.conv[l] % 128 != 0))
       throw ApiError("tensor-core path: conv channels must be multiples of 16 (and of 128 above 128)");
     if ((k * esz + 127) / 128 > kMaxChunks) throw ApiError("tensor-core path: conv input width too large");
-    if (c.residual) throw ApiError("tensor-core path: residual blocks not supported yet");
     cin = c.conv[l];
   }
   if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
@@ -507,12 +506,20 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   auto* t = new TcModel();
   t->mode = mode;
   t->chain = c.n_conv == 3 && c.conv[0] == 64 && c.conv[1] == 64 && c.conv[2] == 64 && c.input_channels == 50 &&
-             c.sequence_length == 128 && !c.residual && std::getenv("SIMNET_NO_CHAIN") == nullptr;
+             c.sequence_length == 128 && std::getenv("SIMNET_NO_CHAIN") == nullptr;
   try {
     cin = c.input_channels;
     for (int l = 0; l < c.n_conv; ++l) t->conv.emplace_back();
     for (int l = 0; l < c.n_conv; ++l) {
-      upload_weights(t->conv[l], host_params + m.L.w[l], c.conv[l], 2 * cin, mode, std::min(c.conv[l], 128), s);
+      const size_t taps = static_cast<size_t>(c.conv[l]) * 2 * cin;
+      std::vector<float> w(host_params + m.L.w[l], host_params + m.L.w[l] + taps);
+      // Residual blocks (c3-rb, cnn.cpp:104-107): out = W in + P in + b.  Both
+      // taps read the same window, so the tensor-core path folds the shortcut
+      // into the weights once (W + P in fp32); the SIMT fp32 path keeps the
+      // reference's two products.
+      if (c.residual)
+        for (size_t i = 0; i < taps; ++i) w[i] += host_params[m.L.p[l] + i];
+      upload_weights(t->conv[l], w.data(), c.conv[l], 2 * cin, mode, std::min(c.conv[l], 128), s);
       cin = c.conv[l];
     }
     const int fc_tile = c.fc_hidden >= 64 ? 64 : c.fc_hidden;

@@ -391,3 +391,26 @@ def test_fc1_in_front_matches():
 def test_items_of_fewer_samples_match():
     """Work items of 3 sub-traces (partially filled operand tiles)."""
     _fresh_process_ab({"SIMNET_SPI": "3"}, 100)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3", "bf16"])
+def test_residual_c3(gpu, port, golden, precision):
+    """c3-rb (residual blocks, cnn.cpp:54-57, 104-107): the SIMT path computes
+    W in + P in, the tensor-core path folds P into W; both against the port."""
+    g = gpu(precision)
+    cfg = CnnConfig.preset_c3()
+    cfg.residual_blocks = True
+    gm = golden["models"]["c3_mix_seed1"]
+    m = Model(cfg, np.array(gm["norm"]), port.init_params(cfg, 3))
+    g.load_model(m)
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    want = port.simulate(t, m, k=16, capture=600, capture_inputs=True, capture_outputs=True)
+    out, tri = g.predict(want["cap_inputs"], want["cap_is_store"])
+    err = np.abs(out - want["cap_outputs"]) / np.maximum(1.0, np.abs(want["cap_outputs"]))
+    assert err.max() <= {"fp32": 2e-5, "tf32x3": 1e-4, "bf16": 1.5e-1}[precision], err.max()
+    if precision != "bf16":
+        pc = pcfg(16)
+        r = run_gpu(g, t, pc, oracle=False)
+        full = port.simulate(t, m, k=16)
+        assert abs(r.total_cycles - full["total_cycles"]) <= 1e-3 * full["total_cycles"]
+        assert np.mean(r.predicted_fetch == full["predicted_fetch"]) >= 0.999
