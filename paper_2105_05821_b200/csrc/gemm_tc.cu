@@ -124,6 +124,44 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // dependency wait; activations only after it.
   asm volatile("griddepcontrol.launch_dependents;");
 
+  // A CTA that owns exactly one M tile has its split warps (2-5) idle once the
+  // tile's chunks are split: they drain half of the accumulator columns.
+  const bool solo = blockIdx.x < p.m_tiles && blockIdx.x + gridDim.x >= p.m_tiles && p.n % 32 == 0;
+  auto epilogue = [&](int t, int acc, int cb, int ce) {
+    const int quad = warp & 3;
+    const int row = t * kBM + quad * 32 + lane;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * p.n;
+    for (int c0 = cb; c0 < ce; c0 += 16) {
+      float v[16];
+      tmem_ld16(tl + c0, v);
+      if (row < p.m) {
+        const int col = ntile * p.n + c0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (p.bias) v[i] += p.bias[col + i];
+          if (p.relu) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (p.out_bf16) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<uint64_t>(row) * p.ldo + col;
+          uint4 pk[2];
+          uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          reinterpret_cast<uint4*>(o)[0] = pk[0];
+          reinterpret_cast<uint4*>(o)[1] = pk[1];
+        } else {
+          float* o = static_cast<float*>(p.out) + ks * p.out_split_stride + static_cast<uint64_t>(row) * p.ldo + col;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+      }
+    }
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       // resident weights for this CTA's (N tile, K split)
@@ -231,46 +269,22 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
     }
+    if (solo) {  // second half of the single tile's accumulator columns
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      mbar_wait(&bar_acc_full[0], 0);
+      tc_fence_after();
+      epilogue(blockIdx.x, 0, p.n / 2, p.n);
+      tc_fence_before();
+    }
   } else {
     // epilogue warps 6..9: TMEM lane quadrant = warp % 4
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int quad = warp & 3;
     int it = 0;
     for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
       mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = t * kBM + quad * 32 + lane;
-      const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * p.n;
-      for (int c0 = 0; c0 < p.n; c0 += 16) {
-        float v[16];
-        tmem_ld16(tl + c0, v);
-        if (row < p.m) {
-          const int col = ntile * p.n + c0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (p.bias) v[i] += p.bias[col + i];
-            if (p.relu) v[i] = fmaxf(v[i], 0.0f);
-          }
-          if (p.out_bf16) {
-            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<uint64_t>(row) * p.ldo + col;
-            uint4 pk[2];
-            uint32_t* w = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-              w[i] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            reinterpret_cast<uint4*>(o)[0] = pk[0];
-            reinterpret_cast<uint4*>(o)[1] = pk[1];
-          } else {
-            float* o = static_cast<float*>(p.out) + ks * p.out_split_stride + static_cast<uint64_t>(row) * p.ldo + col;
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          }
-        }
-      }
+      epilogue(t, acc, 0, solo ? p.n / 2 : p.n);
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
       if (tr && warp == 6 && lane == 0 && it < 2) tr[4 + 2 * it] = clock64();
@@ -389,8 +403,9 @@ uint16_t bf16_rn_host(float x) {
 
 struct TcWeights {
   DevBuf hi, lo;  // K-major [npad][kpad] (f32 or bf16)
-  int n = 0, npad = 0, k = 0, kpad = 0;
-  CUtensorMap map_hi{}, map_lo{};
+  int n = 0, npad = 0, k = 0, kpad = 0, n_tile = 0;
+  CUtensorMap map_hi{}, map_lo{};  // box: one 128-B K chunk x n_tile rows
+  CUtensorMap map64_hi{}, map64_lo{};  // box rows 64 (fused front's in-kernel FC1)
 };
 
 int mode_of(int precision) {
@@ -445,8 +460,12 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
   const uint64_t dims[2] = {static_cast<uint64_t>(w.kpad), static_cast<uint64_t>(w.npad)};
   const uint64_t strides[1] = {static_cast<uint64_t>(w.kpad) * (mode == kBF16 ? 2 : 4)};
   const uint32_t box[2] = {static_cast<uint32_t>(elem_per_chunk), static_cast<uint32_t>(n_tile)};
+  w.n_tile = n_tile;
   w.map_hi = make_map(w.hi.p, mode == kBF16, 2, dims, strides, box);
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
+  const uint32_t box64[2] = {static_cast<uint32_t>(elem_per_chunk), static_cast<uint32_t>(n_tile < 64 ? n_tile : 64)};
+  w.map64_hi = make_map(w.hi.p, mode == kBF16, 2, dims, strides, box64);
+  w.map64_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box64) : w.map64_hi;
 }
 
 size_t smem_bytes(int mode, int n, int chunks, int stages) {
@@ -495,9 +514,9 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   }
   if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
   if (c.fc_hidden % 16 != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 16");
-  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(fc_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   conv_chain_set_attributes();
   round_front_set_attributes();
@@ -522,7 +541,10 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
       upload_weights(t->conv[l], w.data(), c.conv[l], 2 * cin, mode, std::min(c.conv[l], 128), s);
       cin = c.conv[l];
     }
-    const int fc_tile = c.fc_hidden >= 64 ? 64 : c.fc_hidden;
+    // FC1 N tile: 128 hidden units for the f32 modes (one M tile per CTA at
+    // K = 1024: 8 M x 2 N x 8 split planes = 128 CTAs), 64 for bf16 (4 planes),
+    // else the whole (small) layer
+    const int fc_tile = (c.fc_hidden % 128 == 0 && mode != kBF16) ? 128 : (c.fc_hidden >= 64 ? 64 : c.fc_hidden);
     if (c.fc_hidden % fc_tile != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 64 (or <= 64)");
     upload_weights(t->fc1, host_params + m.L.fc1_w, c.fc_hidden, m.L.flat, mode, fc_tile, s);
     // fc2 (reference column-major [od x hidden]) -> [od][hidden]
@@ -583,7 +605,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
   const int total_chunks = (flat * esz + 127) / 128;
   const int per = fc1_cps(mode);
   const int nsplit = (total_chunks + per - 1) / per;
-  const int fc_tile = t.fc1.npad >= 64 ? 64 : t.fc1.npad;
+  const int fc_tile = t.fc1.n_tile;
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(flat), samples};
     const uint64_t strides[1] = {static_cast<uint64_t>(flat) * esz};
@@ -600,7 +622,9 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.n = fc_tile;
     p.chunks = per;
     p.ksteps_last = 4;
-    p.stages = (mode == kTF32x3 && per > 4) ? 2 : kStages;
+    // A ring depth that fits next to the resident W slice (226 KB dynamic smem)
+    p.stages = kStages;
+    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages) > 226 * 1024) --p.stages;
     p.bias = nullptr;
     p.relu = 0;
     p.out = part;
@@ -706,7 +730,7 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   fp.b2 = P + m.L.b[2];
   fp.out = fb.act[2];
   CUtensorMap w[9] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi, t.conv[1].map_lo,
-                      t.conv[2].map_hi, t.conv[2].map_lo, t.fc1.map_hi,     t.fc1.map_lo, t.fc1.map_hi};
+                      t.conv[2].map_hi, t.conv[2].map_lo, t.fc1.map64_hi,   t.fc1.map64_lo, t.fc1.map64_hi};
   if (fp.fc1_tiles > 0) {  // FC1 operand: the flat conv output written by this very launch
     const bool bf = t.mode == kBF16;
     const uint64_t samples = fp.last - fp.first;
