@@ -112,7 +112,6 @@ struct ilsim_gpu_ctx {
 
   // run buffers
   DevBuf state, proc, wq, x, y, act, pred_fetch;
-  DevBuf gbar;  // grid-barrier arrival counters of the fused round front, one per chunk
 
   // capture hook
   uint32_t cap_round = UINT32_MAX;
@@ -251,10 +250,6 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   }
   ForwardBuffers fb{};
   if (!oracle) fb = forward_buffers(c->model, chunk, c->act, c->y);
-  if (fused) {  // grid-barrier counters: one u64 per chunk, zeroed per run
-    const uint64_t nchunks = (K + chunk - 1) / chunk;
-    CUDA_OK(cudaMemsetAsync(c->gbar.need(nchunks * 8), 0, nchunks * 8, c->stream));
-  }
   // fused rounds keep every chunk's FC1 partials until the next round's front
   // decodes them: partial planes for all K sub-traces, chunk f at part_off f
   if (fused && K > chunk) tc_prepare(c->model, K);
@@ -341,7 +336,6 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     fp.fc = tc_fc_decode_args(c->model, l - f, fbs);
     fp.fc.pred_fetch = d_pf;
     fp.fc.per_cycle = cfg.per_cycle_advance;
-    if (!dump) tc_fc1_front_params(c->model, fp, c->gbar.as<uint32_t>() + 2 * (f / chunk));  // FC1 in the same launch
     return fp;
   };
   // fused round: front (decode + apply of the previous round, gather, conv) -> FC1
@@ -369,7 +363,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     if (fused) {
       static const int ko = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
       const uint64_t n1 = (ko & 8) ? 0 : do_front(f, l, nullptr, fbs, st);
-      return n1 + (((ko & 4) || tc_fc1_in_front(c->model)) ? 0 : do_fc(f, l, fbs, st));
+      return n1 + ((ko & 4) ? 0 : do_fc(f, l, fbs, st));
     }
     return do_ctx(f, l, true, off, st) + do_forward(f, l, off, fbs, st) + do_decode(f, l, fbs, st);
   };
@@ -432,7 +426,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
                                     width * sizeof(float), rows, cudaMemcpyDeviceToHost, c->stream));
         }
         if (fused) {
-          if (cap_now || !tc_fc1_in_front(c->model)) launches += do_fc(f, l, fb_chunk(f), c->stream);
+          launches += do_fc(f, l, fb_chunk(f), c->stream);
         } else {
           launches += do_forward(f, l, 0, fb, c->stream);
         }

@@ -63,10 +63,8 @@ __device__ __forceinline__ void warp_decode_triple(const float* y, const double*
 //   an fma chain over those units in order; the 32 lane partials of the 8
 //   samples are combined by a transpose reduction (xor 16, 8, 4) then a
 //   butterfly (xor 2, 1); y[s][o] = that + b2[o].
-// w2_bar (optional): mbarrier (phase parity w2_parity) completing when w2s has
-// landed; waited only after the partial loads are in flight.
 __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const float* w2s, float* hs, float* ys,
-                               long long* trace = nullptr, uint64_t* w2_bar = nullptr, uint32_t w2_parity = 0) {
+                               long long* trace = nullptr) {
   const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
   const int hid = a.hidden, c4 = hid >> 2;
   // biases fetched with the partials (no dependent global load later): lane j
@@ -105,17 +103,6 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
           make_float4(fmaxf(acc.x + b.x, 0.0f), fmaxf(acc.y + b.y, 0.0f), fmaxf(acc.z + b.z, 0.0f),
                       fmaxf(acc.w + b.w, 0.0f));
     }
-  }
-  if (w2_bar) {  // before the first barrier: W2 lands in the region hs / ys follow
-    const uint32_t ba = static_cast<uint32_t>(__cvta_generic_to_shared(w2_bar));
-    uint32_t ok = 0;
-    do {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(ok)
-          : "r"(ba), "r"(w2_parity)
-          : "memory");
-    } while (!ok);
   }
   fc_sync256();
   if (trace && threadIdx.x == 0) trace[0] = clock64();

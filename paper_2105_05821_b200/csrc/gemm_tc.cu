@@ -405,7 +405,6 @@ struct TcWeights {
   DevBuf hi, lo;  // K-major [npad][kpad] (f32 or bf16)
   int n = 0, npad = 0, k = 0, kpad = 0, n_tile = 0;
   CUtensorMap map_hi{}, map_lo{};  // box: one 128-B K chunk x n_tile rows
-  CUtensorMap map64_hi{}, map64_lo{};  // box rows 64 (fused front's in-kernel FC1)
 };
 
 int mode_of(int precision) {
@@ -463,9 +462,6 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
   w.n_tile = n_tile;
   w.map_hi = make_map(w.hi.p, mode == kBF16, 2, dims, strides, box);
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
-  const uint32_t box64[2] = {static_cast<uint32_t>(elem_per_chunk), static_cast<uint32_t>(n_tile < 64 ? n_tile : 64)};
-  w.map64_hi = make_map(w.hi.p, mode == kBF16, 2, dims, strides, box64);
-  w.map64_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box64) : w.map64_hi;
 }
 
 size_t smem_bytes(int mode, int n, int chunks, int stages) {
@@ -671,31 +667,6 @@ void tc_calibrate(const DevModel& m, cudaStream_t s) {
   CUDA_OK(cudaStreamSynchronize(s));
 }
 
-// FC1 inside the fused front after a grid barrier (one launch per round).
-// Opt-in (SIMNET_FC1_INFRONT=1): on B200 at K=1024 it measured on par with the
-// separate FC1 launch (38.4 vs 37.5 us per tf32x3 round; the 2-stage A ring
-// that fits next to the resident W1 slice is TMA-latency-bound).
-bool tc_fc1_in_front(const DevModel& m) {
-  const TcModel& t = *m.tc;
-  static const bool on = std::getenv("SIMNET_FC1_INFRONT") != nullptr;
-  return on && t.chain && m.cfg.fc_hidden % 64 == 0 && t.fc1.npad == m.cfg.fc_hidden;
-}
-
-void tc_fc1_front_params(const DevModel& m, FrontParams& fp, uint32_t* gbar) {
-  if (!tc_fc1_in_front(m)) return;
-  const uint64_t samples = fp.last - fp.first;
-  const int nsplit = fp.fc.nsplit;
-  fp.fc1_cps = fc1_cps(m.tc->mode);
-  fp.fc1_sp = nsplit >= 8 ? 2 : 1;  // 3xTF32 / tf32: 8 planes as 4 pairs; bf16: 4 planes
-  fp.fc1_ntiles = m.cfg.fc_hidden / 64;
-  fp.fc1_mtiles = static_cast<int>((samples + kBM - 1) / kBM);
-  fp.fc1_tiles = fp.fc1_mtiles * fp.fc1_ntiles * (nsplit / fp.fc1_sp);
-  fp.fc1_part = const_cast<float*>(fp.fc.part);
-  fp.fc1_plane = fp.fc.split_stride;
-  fp.fc1_hidden = m.cfg.fc_hidden;
-  fp.gbar = gbar;
-}
-
 FcDecodeArgs tc_fc_decode_args(const DevModel& m, uint64_t samples, const ForwardBuffers& fb) {
   const TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
@@ -729,16 +700,8 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   fp.b1 = P + m.L.b[1];
   fp.b2 = P + m.L.b[2];
   fp.out = fb.act[2];
-  CUtensorMap w[9] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi, t.conv[1].map_lo,
-                      t.conv[2].map_hi, t.conv[2].map_lo, t.fc1.map64_hi,   t.fc1.map64_lo, t.fc1.map64_hi};
-  if (fp.fc1_tiles > 0) {  // FC1 operand: the flat conv output written by this very launch
-    const bool bf = t.mode == kBF16;
-    const uint64_t samples = fp.last - fp.first;
-    const uint64_t dims[2] = {static_cast<uint64_t>(m.L.flat), samples};
-    const uint64_t strides[1] = {static_cast<uint64_t>(m.L.flat) * (bf ? 2 : 4)};
-    const uint32_t box[2] = {static_cast<uint32_t>(bf ? 64 : 32), kBM};
-    w[8] = make_map(fb.act[2], bf, 2, dims, strides, box);
-  }
+  const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
+                            t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
   fp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
   if (!fp.calibrate) fp.c1acc = t.c1acc.as<float>();
   static const int knockout = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;

@@ -93,9 +93,6 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
 // FC1 + FC tail (+ fused K3 when fuse != null) on the flat conv output.
 uint64_t tc_fc(const DevModel& m, const void* flat, uint64_t samples, const ForwardBuffers& fb, cudaStream_t s,
                const DecodeParams* fuse, bool with_tail);
-// FC1 inside the fused front (after a grid barrier) instead of a separate launch.
-bool tc_fc1_in_front(const DevModel& m);
-void tc_fc1_front_params(const DevModel& m, FrontParams& fp, uint32_t* gbar);
 // Where the fused round front finds the FC1 partials of a chunk (+ FC2 weights).
 FcDecodeArgs tc_fc_decode_args(const DevModel& m, uint64_t samples, const ForwardBuffers& fb);
 

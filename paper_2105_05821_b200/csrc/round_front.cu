@@ -52,23 +52,6 @@ constexpr int kCompute = 256;
 
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-// Grid-wide barrier (one thread per CTA; every CTA of the launch is resident:
-// one CTA per SM, cooperative launch).  *gbar counts arrivals monotonically
-// across the barrier instances of one run (zeroed per run, one counter per
-// chunk so the grid size n is fixed): an arrival that saw c0 waits for the end
-// of its epoch, (c0 / n + 1) * n.  One atomic per CTA, no reset write.  A
-// barrier that cannot complete traps instead of hanging the GPU.
-__device__ inline void grid_barrier(unsigned long long* gbar, uint32_t n) {
-  unsigned long long c0;
-  asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(c0) : "l"(gbar) : "memory");
-  const unsigned long long target = (c0 / n + 1) * n;
-  unsigned long long c;
-  uint32_t spins = 0;
-  do {
-    asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(c) : "l"(gbar) : "memory");
-    if (++spins > (1u << 28)) __trap();
-  } while (c < target);
-}
 
 // byte offset of f32 element (row r, k) in a K-major SW128 tile of 128 rows
 // whose K extent is split into chunk-major 128-byte chunks of 32 floats.
@@ -211,8 +194,7 @@ __global__ void __launch_bounds__(kThreadsRF, 1)
 round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW0lo,
                    const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW1lo,
                    const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW2lo,
-                   const __grid_constant__ CUtensorMap tmF1, const __grid_constant__ CUtensorMap tmF1lo,
-                   const __grid_constant__ CUtensorMap tmFlat, FrontParams p) {
+                   FrontParams p) {
   using S = Shape<kMode>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* R1 = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
@@ -227,9 +209,6 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __shared__ __align__(8) uint64_t bar_w1f;        // conv1 MMAs done (W1 free), 1 / item
   __shared__ __align__(8) uint64_t bar_a2, bar_m2; // conv2 A restaged / MMAs done: 1 / item
   __shared__ __align__(8) uint64_t bar_w2;         // FC2 weights landed in R1 (bulk copy), 1 / item
-  // FC1 phase: grid barrier passed, W1 slice landed, A ring (2 stages), MMAs done
-  __shared__ __align__(8) uint64_t bar_grid, bar_f1w, bar_f1full[2], bar_f1split[2], bar_f1empty[2], bar_f1done;
-  __shared__ __align__(8) uint64_t bar_f1drained;
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[3][kC];
   __shared__ float s_zero[kSlots], s_one[kSlots];
@@ -241,8 +220,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t samples = p.last - p.first;
-  const int spi = p.spi;  // sub-traces per item: rows s*16.. of an operand tile for s < spi, zero above
-  const int n_items = static_cast<int>((samples + spi - 1) / spi);
+  const int n_items = static_cast<int>((samples + kItem - 1) / kItem);
   // PDL: the FC kernels may launch now (their prologue only touches weights);
   // this kernel's prologue (barriers, TMEM, biases, W0) overlaps the previous
   // round's tail, and only the compute warps wait for its results.
@@ -273,15 +251,6 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     mbar_init(&bar_a2, kCompute);
     mbar_init(&bar_m2, 1);
     mbar_init(&bar_w2, 1);
-    mbar_init(&bar_grid, 1);
-    mbar_init(&bar_f1w, 1);
-    mbar_init(&bar_f1done, 1);
-    mbar_init(&bar_f1drained, kCompute);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_f1full[i], 1);
-      mbar_init(&bar_f1split[i], kCompute);
-      mbar_init(&bar_f1empty[i], 1);
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -328,36 +297,6 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         load_w(1, &tmW1, &tmW1lo, S::kKChunks);
         mbar_wait(&bar_w1f, it & 1);  // conv1 MMAs done: W1 no longer read
         load_w(2, &tmW2, &tmW2lo, S::kKChunks);
-      }
-      // ---- FC1 phase: W1 slice into R1 (before the grid barrier), A chunks into R2 ----
-      if (p.fc1_tiles > 0) {
-        if (it > 0) mbar_wait(&bar_m2, (it - 1) & 1);  // last conv2 done: R1, R2 free
-        const int nch = p.fc1_sp * p.fc1_cps;
-        const uint32_t wplane = static_cast<uint32_t>(nch) * (kC * 128);
-        int stage = 0;
-        uint32_t ph = 0;
-        int ft = 0;
-        for (int tile = blockIdx.x; tile < p.fc1_tiles; tile += gridDim.x, ++ft) {
-          const int mt = tile % p.fc1_mtiles, rest = tile / p.fc1_mtiles;
-          const int nt = rest % p.fc1_ntiles, pair = rest / p.fc1_ntiles;
-          const int kc0 = pair * nch;
-          if (ft > 0) mbar_wait(&bar_f1done, (ft - 1) & 1);  // previous tile's MMAs done with W1 / R1
-          mbar_expect_tx(&bar_f1w, wplane * (S::kSplit ? 2u : 1u));
-          for (int c = 0; c < nch; ++c) {
-            tma_load_2d(R1 + c * (kC * 128), &tmF1, &bar_f1w, (kc0 + c) * S::kElems, nt * kC);
-            if (S::kSplit) tma_load_2d(R1 + wplane + c * (kC * 128), &tmF1lo, &bar_f1w, (kc0 + c) * S::kElems, nt * kC);
-          }
-          if (ft == 0) mbar_wait(&bar_grid, 0);  // every CTA's flat is written
-          for (int c = 0; c < nch; ++c) {
-            mbar_wait(&bar_f1empty[stage], ph ^ 1);
-            mbar_expect_tx(&bar_f1full[stage], S::kStage);
-            tma_load_2d(R2 + stage * 2 * S::kStage, &tmFlat, &bar_f1full[stage], (kc0 + c) * S::kElems, mt * 128);
-            if (++stage == 2) {
-              stage = 0;
-              ph ^= 1;
-            }
-          }
-        }
       }
     }
   } else if (warp == 9) {
@@ -414,41 +353,6 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         gemm(tmem + 384, S::kALo, 4 * S::kKChunks);
         mma_commit(&bar_m2);
       }
-      // ---- FC1 phase: split-K planes of one (M, N, pair) tile into TMEM 0.. ----
-      if (p.fc1_tiles > 0) {
-        const int nch = p.fc1_sp * p.fc1_cps;
-        const uint32_t wplane = static_cast<uint32_t>(nch) * (kC * 128);
-        int stage = 0;
-        uint32_t ph = 0;
-        int ft = 0;
-        for (int tile = blockIdx.x; tile < p.fc1_tiles; tile += gridDim.x, ++ft) {
-          mbar_wait(&bar_f1w, ft & 1);
-          if (ft > 0) mbar_wait(&bar_f1drained, (ft - 1) & 1);  // previous tile's accumulators read out
-          for (int c = 0; c < nch; ++c) {
-            mbar_wait(S::kSplit ? &bar_f1split[stage] : &bar_f1full[stage], ph);
-            tc_fence_after();
-            const uint32_t d = tmem + (c / p.fc1_cps) * kC;
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t ao = r2 + stage * 2 * S::kStage + j * 32, wo = r1 + c * (kC * 128) + j * 32;
-              const uint64_t ad = smem_desc_sw128(ao), bd = smem_desc_sw128(wo);
-              const uint32_t first = (c % p.fc1_cps == 0 && j == 0) ? 0u : 1u;
-              if (S::kSplit) {
-                mma<kMode>(d, smem_desc_sw128(ao + S::kStage), bd, idesc, first);  // small terms first
-                mma<kMode>(d, ad, smem_desc_sw128(wo + wplane), idesc, 1);
-                mma<kMode>(d, ad, bd, idesc, 1);
-              } else {
-                mma<kMode>(d, ad, bd, idesc, first);
-              }
-            }
-            mma_commit(&bar_f1empty[stage]);
-            if (++stage == 2) {
-              stage = 0;
-              ph ^= 1;
-            }
-          }
-          mma_commit(&bar_f1done);
-        }
-      }
     }
     __syncwarp();
   } else {
@@ -477,14 +381,15 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       // ---- 1. decode the previous round (FC tail of the item's 8 samples, all
       //         warps), then apply + column table: warp w owns sub-trace item*8 + w ----
       {
-        const uint64_t s = p.first + static_cast<uint64_t>(item) * spi + warp;
-        const bool mine = warp < spi && s < p.last && !p.calibrate;
+        const uint64_t s = p.first + static_cast<uint64_t>(item) * kItem + warp;
+        const bool mine = s < p.last && !p.calibrate;
         // R1 is idle until the gather: W2 (bulk copy) | h [8][hidden] | y [8][64]
+        mbar_wait(&bar_w2, it & 1);
         if (tr && it == 0 && lane == 0 && warp == 0) tr[24] = clock64();
         float* hs = reinterpret_cast<float*>(R1) + kFcMaxOut * kFcMaxHidden;
         float* ys = hs + kItem * kFcMaxHidden;
         cta8_fc(p.fc, (mine ? s : p.first) - p.first, reinterpret_cast<const float*>(R1), hs, ys,
-                (tr && it == 0) ? tr + 28 : nullptr, &bar_w2, it & 1);
+                (tr && it == 0) ? tr + 28 : nullptr);
         if (tr && it == 0 && lane == 0 && warp == 0) tr[25] = clock64();
         int ncs = -1;
         if (mine) {
@@ -610,8 +515,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         }
         if (p.dump) {
           const int row = t * kRowsT + (lane >> 1);
-          const uint64_t smp = static_cast<uint64_t>(item) * spi + warp;
-          if (warp < spi && smp < samples && (row + 1) * 100 <= static_cast<int>(p.dump_stride)) {
+          const uint64_t smp = static_cast<uint64_t>(item) * kItem + warp;
+          if (smp < samples && (row + 1) * 100 <= static_cast<int>(p.dump_stride)) {
             float* o = p.dump + smp * p.dump_stride + row * 100 + 50 * h;
 #pragma unroll
             for (int k = 0; k < kSlots; k += 2) *reinterpret_cast<float2*>(o + k) = make_float2(v[k], v[k + 1]);
@@ -666,14 +571,14 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       mbar_wait(&bar_m2, it & 1);
       tc_fence_after();
       mark(11);
-      const uint64_t sample = static_cast<uint64_t>(item) * spi + (m >> 4);
+      const uint64_t sample = static_cast<uint64_t>(item) * kItem + (m >> 4);
       for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + lane_off + 384 + c0, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
-        if ((m >> 4) < spi && sample < samples) {
-          const uint64_t off = sample * (16 * kC) + (m & 15) * kC + c0;
+        if (sample < samples) {
+          const uint64_t off = static_cast<uint64_t>(item) * (kItem * 16 * kC) + m * kC + c0;
           if (kMode == kBF16) {
             uint4 pk[2];
             uint32_t* w = reinterpret_cast<uint32_t*>(pk);
@@ -695,70 +600,6 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       tc_fence_before();
       compute_sync();  // TMEM conv2 columns and the tables are free for the next item
       mark(12);
-    }
-    // ---- FC1 phase ----
-    if (p.fc1_tiles > 0) {
-      // this CTA's flat stores -> every CTA's TMA loads (async proxy) after the grid barrier
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      compute_sync();
-      if (tid == 0) {
-        if (tr) tr[21] = clock64();
-        grid_barrier(reinterpret_cast<unsigned long long*>(p.gbar), gridDim.x);
-        if (tr) tr[22] = clock64();
-        mbar_arrive(&bar_grid);
-      }
-      const int nch = p.fc1_sp * p.fc1_cps;
-      int stage = 0;
-      uint32_t ph = 0;
-      int ft = 0;
-      for (int tile = blockIdx.x; tile < p.fc1_tiles; tile += gridDim.x, ++ft) {
-        const int mt = tile % p.fc1_mtiles, rest = tile / p.fc1_mtiles;
-        const int nt = rest % p.fc1_ntiles, pair = rest / p.fc1_ntiles;
-        for (int c = 0; c < nch; ++c) {
-          if constexpr (S::kSplit) {  // hi = cvt.rna tf32 in place, lo = x - hi next to it
-            mbar_wait(&bar_f1full[stage], ph);
-            uint4* a = reinterpret_cast<uint4*>(R2 + stage * 2 * S::kStage);
-            float4* alo = reinterpret_cast<float4*>(R2 + stage * 2 * S::kStage + S::kStage);
-#pragma unroll
-            for (int i = tid; i < static_cast<int>(S::kStage / 16); i += kCompute) {
-              const uint4 u = a[i];
-              uint4 h;
-              h.x = (u.x + 0x1000u) & 0xffffe000u;
-              h.y = (u.y + 0x1000u) & 0xffffe000u;
-              h.z = (u.z + 0x1000u) & 0xffffe000u;
-              h.w = (u.w + 0x1000u) & 0xffffe000u;
-              a[i] = h;
-              alo[i] = make_float4(__uint_as_float(u.x) - __uint_as_float(h.x), __uint_as_float(u.y) - __uint_as_float(h.y),
-                                   __uint_as_float(u.z) - __uint_as_float(h.z), __uint_as_float(u.w) - __uint_as_float(h.w));
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&bar_f1split[stage]);
-          }
-          if (++stage == 2) {
-            stage = 0;
-            ph ^= 1;
-          }
-        }
-        // epilogue: TMEM lane m = sample row, columns = 64 hidden units of split plane q
-        mbar_wait(&bar_f1done, ft & 1);
-        tc_fence_after();
-        if (tr && ft == 0 && tid == 0) tr[23] = clock64();
-        const uint64_t row = static_cast<uint64_t>(mt) * 128 + m;
-        for (int q = 0; q < p.fc1_sp; ++q) {
-          float v[32];
-          tmem_ld16(tmem + lane_off + q * kC + half * 32, v);
-          tmem_ld16(tmem + lane_off + q * kC + half * 32 + 16, v + 16);
-          if (row < samples) {
-            float* o = p.fc1_part + static_cast<uint64_t>(pair * p.fc1_sp + q) * p.fc1_plane + row * p.fc1_hidden +
-                       nt * kC + half * 32;
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&bar_f1drained);
-        if (tr && ft == 0 && tid == 0) tr[31] = clock64();
-      }
     }
   }
   tc_fence_before();
@@ -811,42 +652,19 @@ namespace {
 size_t front_smem_bytes() { return kR1 + kR2 + kTbl + 1024; }
 }  // namespace
 
-void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& pin, int num_sms, cudaStream_t s) {
-  const uint64_t samples = pin.last - pin.first;
+void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s) {
+  const uint64_t samples = p.last - p.first;
   if (samples == 0) return;
-  FrontParams p = pin;
-  // Sub-traces per work item (SIMNET_SPI overrides; default 8).  Spreading
-  // K = 1024 as 147 items of 7 over every SM measured no faster than 128 items
-  // of 8: an item's round is latency-bound, not throughput-bound.
-  if (p.spi == 0) {
-    static const int env = std::getenv("SIMNET_SPI") ? std::atoi(std::getenv("SIMNET_SPI")) : 0;
-    if (env > 0) {
-      p.spi = env > kItem ? kItem : env;
-    } else if (env < 0) {
-      const uint64_t per = (samples + num_sms - 1) / num_sms;
-      p.spi = static_cast<int32_t>(per < 1 ? 1 : (per > kItem ? kItem : per));
-    } else {
-      p.spi = kItem;
-    }
-  }
   if (p.max_context + 1 > kTblCols) throw ApiError("fused round front: max_context too large");
-  const uint64_t items = (samples + p.spi - 1) / p.spi;
+  const uint64_t items = (samples + kItem - 1) / kItem;
   const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
   const size_t sm = front_smem_bytes();
-  // The in-kernel FC1 phase needs every CTA resident (grid barrier): launched
-  // cooperatively (one CTA per SM is guaranteed by the shared-memory footprint).
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreadsRF);
-  cfg.dynamicSmemBytes = sm;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = p.fc1_tiles > 0 ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  auto* k = mode == kBF16 ? round_front_kernel<kBF16> : (mode == kTF32 ? round_front_kernel<kTF32> : round_front_kernel<kTF32x3>);
-  CUDA_OK(cudaLaunchKernelEx(&cfg, k, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], p));
+  if (mode == kBF16)
+    launch_pdl(round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+  else if (mode == kTF32)
+    launch_pdl(round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+  else
+    launch_pdl(round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
 }
 
 void round_front_set_attributes() {

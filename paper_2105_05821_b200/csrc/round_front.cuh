@@ -44,22 +44,12 @@ struct FrontParams {
   const float* c1acc;
   float* c1acc_out;          // calibration launch: where to write it
   int32_t calibrate;         // 1: no sub-traces, all-zero input (calibration)
-  int32_t spi;               // sub-traces per work item (1..8; set by the launcher)
   long long* trace;          // optional: per-CTA event clocks of the first item (diagnostics)
   int32_t knockout;          // diagnostics only (SIMNET_KNOCKOUT): 1 = no static loads, 2 = no apply
-  // FC1 of this round, after a grid barrier (every CTA's flat written): tile =
-  // (M tile of 128 samples, N tile of 64 hidden, pair of split-K planes); the
-  // partial planes are the unfused FC1's, bit for bit.  fc1_tiles == 0: none.
-  int32_t fc1_tiles, fc1_mtiles, fc1_ntiles, fc1_sp;  // sp: split-K planes per tile
-  int32_t fc1_cps;                                    // 128-B K chunks per split plane
-  float* fc1_part;                                    // [nsplit][samples][hidden]
-  uint64_t fc1_plane;                                 // samples * hidden
-  int32_t fc1_hidden;
-  uint32_t* gbar;                                     // grid barrier {count, generation}
 };
 
 // w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
-// w: 6 conv maps, then FC1 W hi / lo (box 1 chunk x 64 rows) and the flat map (box 1 chunk x 128 rows)
+// w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
 void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s);
 void round_front_set_attributes();
 // After the last round: decode the outstanding predictions, apply them and

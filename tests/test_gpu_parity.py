@@ -361,38 +361,6 @@ def test_chunked_rounds_match(gpu, port, golden, precision, monkeypatch):
         assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
 
 
-def _fresh_process_ab(env: dict, k: int) -> None:
-    """Fused (under `env`, read once per process) vs unfused on the bench-like
-    workload in a fresh process: results must be bit-identical."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import sys, numpy as np\n"
-        "sys.path.insert(0, %r)\n"
-        "from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig\n"
-        "from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace\n"
-        "m = synthetic_model(synthetic_trace(20000, 101), 1); t = synthetic_trace(24000, 7)\n"
-        "g = GpuSimulator(0, 'tf32x3'); g.load_model(m)\n"
-        "pc = ParallelConfig(k=%d, sim=SimConfig(max_context=110)); g.load_trace(t, pc)\n"
-        "a = g.run(pc); b = g.run(pc, fused=False)\n"
-        "print(int(np.array_equal(a.predicted_fetch, b.predicted_fetch) and a.total_cycles == b.total_cycles))\n"
-    ) % (str(GOLD.parents[1]), k)
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
-                         env=dict(os.environ, **env))
-    assert out.stdout.strip().endswith("1"), out.stdout + out.stderr
-
-
-def test_fc1_in_front_matches():
-    """The opt-in one-launch round (FC1 inside the front after a grid barrier)."""
-    _fresh_process_ab({"SIMNET_FC1_INFRONT": "1"}, 256)
-
-
-def test_items_of_fewer_samples_match():
-    """Work items of 3 sub-traces (partially filled operand tiles)."""
-    _fresh_process_ab({"SIMNET_SPI": "3"}, 100)
-
-
 @pytest.mark.parametrize("precision", ["fp32", "tf32x3", "bf16"])
 def test_residual_c3(gpu, port, golden, precision):
     """c3-rb (residual blocks, cnn.cpp:54-57, 104-107): the SIMT path computes
