@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--precision", default=os.environ.get("SIMNET_PRECISION", "tf32x3"),
                    choices=["fp32", "tf32x3", "tf32", "bf16"])
-    p.add_argument("--n", type=int, default=N_INSTR)
+    p.add_argument("--instructions", dest="n", type=int, default=N_INSTR)
     p.add_argument("--k", type=int, default=K_SUB)
     p.add_argument("--regime", default="default", choices=["default", "memory"])
     p.add_argument("--no-cpu-baseline", action="store_true")

@@ -382,3 +382,35 @@ def test_residual_c3(gpu, port, golden, precision):
         full = port.simulate(t, m, k=16)
         assert abs(r.total_cycles - full["total_cycles"]) <= 1e-3 * full["total_cycles"]
         assert np.mean(r.predicted_fetch == full["predicted_fetch"]) >= 0.999
+
+
+@pytest.mark.parametrize("extra", [dict(warmup=40), dict(warmup=300, drain_trim=True), dict(drain_trim=True),
+                                   dict(bw=3), dict(mc=110, per_cycle=True)])
+def test_fused_round_extensions_and_options(gpu, port, extra):
+    """Warm-up overlap, drain-trim, retire bandwidth and per-cycle advance
+    through the fused tensor-core round: bit-identical to the unfused round and
+    within 0.1% of the CPU oracle."""
+    g = gpu("tf32x3")
+    m, t = _bench_like("default", n=12_000)
+    g.load_model(m)
+    pc = pcfg(48, **extra)
+    g.load_trace(t, pc)
+    a = g.run(pc)
+    b = g.run(pc, fused=False)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    want = port.simulate(t, m, k=48, retire_bandwidth=pc.sim.retire_bandwidth,
+                         per_cycle=pc.sim.per_cycle_advance, warmup=pc.warmup, drain_trim=pc.drain_trim)
+    assert abs(a.total_cycles - want["total_cycles"]) <= 1e-3 * want["total_cycles"]
+
+
+def test_sharded_fused_rounds_compose(gpu, port):
+    """Shards (the multi-GPU partition) through the fused round reproduce the
+    single-device run sub-trace for sub-trace."""
+    g = gpu("tf32x3")
+    m, t = _bench_like("default", n=12_000)
+    g.load_model(m)
+    full = run_gpu(g, t, pcfg(40, warmup=64), oracle=False)
+    parts = [run_gpu(g, t, pcfg(40, warmup=64), oracle=False, shard=s) for s in ((0, 13), (13, 29), (29, 40))]
+    got = np.concatenate([gpu_subs(p) for p in parts])
+    assert np.array_equal(got, gpu_subs(full))
+    assert np.array_equal(np.concatenate([p.predicted_fetch for p in parts]), full.predicted_fetch)
