@@ -146,8 +146,9 @@ def pinned_trace(trace):
 
 
 def trace_h2d_bytes(t) -> int:
-    return int(t.pc.nbytes + t.op.nbytes + t.src.nbytes + t.dst.nbytes + t.data_addr.nbytes + t.hist.nbytes
-               + t.truth.nbytes)
+    """Bytes ilsim_gpu_simulate_parallel copies host->device per step (CNN
+    path: the recorded truth latencies are not uploaded)."""
+    return int(t.pc.nbytes + t.op.nbytes + t.src.nbytes + t.dst.nbytes + t.data_addr.nbytes + t.hist.nbytes)
 
 
 # ---------------------------------------------------------------------------

@@ -238,9 +238,12 @@ class GpuSimulator:
         c.reserved[2] = int(not fused)
         return c
 
-    def load_trace(self, trace: Trace, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None):
+    def load_trace(self, trace: Trace, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None,
+                   truth: bool = True):
+        """Upload this configuration's trace slice.  ``truth``: also upload the
+        recorded latencies (needed for oracle runs; the CNN path skips them)."""
         cfg = self._sim_cfg(pc, sequential=sequential, oracle=oracle, shard=shard)
-        view, keep = trace_view(trace, with_truth=oracle or True)
+        view, keep = trace_view(trace, with_truth=oracle or truth)
         self._check(self.L.ilsim_gpu_load_trace(self._h, C.byref(view), C.byref(cfg)))
         self._trace_n = trace.n
         del keep
@@ -305,13 +308,13 @@ class GpuSimulator:
                           shard=None) -> ParallelResult:
         """``simulate_parallel`` (parallel.cpp:26-93)."""
         pc = pc or ParallelConfig()
-        self.load_trace(trace, pc, oracle=oracle, shard=shard)
+        self.load_trace(trace, pc, oracle=oracle, shard=shard, truth=oracle)
         return self.run(pc, oracle=oracle, shard=shard)
 
     def simulate_trace(self, trace: Trace, sim: SimConfig | None = None, *, oracle=False) -> SimResult:
         """``simulate_trace`` (simcore.cpp:185-196)."""
         pc = ParallelConfig(k=1, sim=sim or SimConfig())
-        self.load_trace(trace, pc, sequential=True, oracle=oracle)
+        self.load_trace(trace, pc, sequential=True, oracle=oracle, truth=oracle)
         r = self.run(pc, sequential=True, oracle=oracle)
         return r.sub_results[0]
 
