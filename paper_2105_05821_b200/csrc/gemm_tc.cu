@@ -118,7 +118,10 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const int elems = kMode == kBF16 ? 64 : 32;  // elements per 128 B chunk
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   long long* tr = p.trace ? p.trace + 148 * 32 + cta * 16 : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = clock64();
+  if (tr && threadIdx.x == 0) {
+    tr[0] = clock64();
+    tr[8] = global_ns();
+  }
   // PDL: let the next kernel start its prologue; everything above overlapped
   // the previous kernel.  Weights are constants and may be fetched before the
   // dependency wait; activations only after it.
@@ -287,11 +290,15 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       epilogue(t, acc, 0, solo ? p.n / 2 : p.n);
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
-      if (tr && warp == 6 && lane == 0 && it < 2) tr[4 + 2 * it] = clock64();
+      if (tr && warp == 6 && lane == 0 && it < 2) {
+        tr[4 + 2 * it] = clock64();
+        tr[10 + it] = global_ns();
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[9] = global_ns();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
@@ -487,9 +494,9 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
   const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages);
-  if (mode == kBF16) launch_pdl(tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
-  else if (mode == kTF32) launch_pdl(tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
-  else launch_pdl(tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
+  if (mode == kBF16) launch_pdl_tag("layer_bf16", tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
+  else if (mode == kTF32) launch_pdl_tag("layer", tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
+  else launch_pdl_tag("layer", tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
 }
 
 }  // namespace

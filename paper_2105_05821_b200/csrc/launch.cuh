@@ -6,14 +6,30 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <string>
 
 #include "host_util.cuh"
 
 namespace simnet {
 
+// Programmatic dependent launch per launch tag.  Default: the fused round's
+// front ("front") and its f32 FC1 ("layer") -- measured A/B on B200 at K=1024:
+// tf32x3 35.9 -> 34.2 us per round (both), bf16 24.0 -> 23.4 (front only; PDL
+// on the bf16 FC1, "layer_bf16", measured slower).  SIMNET_PDL overrides:
+// "0" = none, "1" / "all" = every launch, else a comma list of tags.
+inline bool pdl_enabled(const char* tag) {
+  static const char* env = std::getenv("SIMNET_PDL");
+  const std::string t = tag ? tag : "";
+  if (!env) return t == "front" || t == "layer";
+  const std::string e(env);
+  if (e.empty() || e == "0") return false;
+  if (e == "1" || e == "all") return true;
+  return !t.empty() && ("," + e + ",").find("," + t + ",") != std::string::npos;
+}
+
 template <typename... KArgs, typename... Args>
-inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                       Args&&... args) {
+inline void launch_pdl_tag(const char* tag, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           cudaStream_t stream, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -22,12 +38,16 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  // Opt-in: measured slower on B200 for this round loop (early dependents
-  // launch and then contend with the running kernel), so off by default.
-  static const bool disabled = std::getenv("SIMNET_PDL") == nullptr;
   cfg.attrs = attr;
-  cfg.numAttrs = disabled ? 0 : 1;
+  cfg.numAttrs = pdl_enabled(tag) ? 1 : 0;
   CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
+// Untagged launches (the unfused path): PDL only when SIMNET_PDL=1/all.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  launch_pdl_tag(nullptr, kernel, grid, block, smem, stream, static_cast<Args&&>(args)...);
 }
 
 }  // namespace simnet

@@ -264,6 +264,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 13] = global_ns();  // diagnostics: kernel span
 
   if (warp == 8) {
     // ---------------- TMA producer: layer weights ----------------
@@ -604,6 +605,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 14] = global_ns();
   if (warp == 9) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
@@ -660,11 +662,11 @@ void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, in
   const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
   const size_t sm = front_smem_bytes();
   if (mode == kBF16)
-    launch_pdl(round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    launch_pdl_tag("front", round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
   else if (mode == kTF32)
-    launch_pdl(round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    launch_pdl_tag("front", round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
   else
-    launch_pdl(round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    launch_pdl_tag("front", round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
 }
 
 void round_front_set_attributes() {

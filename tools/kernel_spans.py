@@ -1,0 +1,41 @@
+# diagnostics: in-graph spans of the last round's two kernels from %globaltimer
+# (SIMNET_CHAIN_TRACE=1): first CTA start .. last CTA end, and the gaps.
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+os.environ["SIMNET_CHAIN_TRACE"] = "1"
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, _lib  # noqa: E402
+from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace  # noqa: E402
+
+t = synthetic_trace(300_000, 101)
+m = synthetic_model(synthetic_trace(200_000, 101), 1)
+for prec in ("tf32x3", "bf16"):
+    g = GpuSimulator(0, prec)
+    g.load_model(m)
+    pc = ParallelConfig(k=1024)
+    g.load_trace(t, pc)
+    r = g.run(pc)
+    buf = np.zeros(148 * 32 + 256 * 16, np.int64)
+    _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
+    fr = buf[:148 * 32].reshape(148, 32)[:128]
+    f1 = buf[148 * 32:].reshape(256, 16)[:128]
+    fs, fe = fr[:, 13].min(), fr[:, 14].max()
+    cs, ce = f1[:, 8].min(), f1[:, 9].max()
+    per_round = 1000 * r.device_ms / r.rounds
+    print(f"{prec}: round {per_round:.2f} us | front span {(fe - fs) / 1e3:.2f} us (CTA end spread "
+          f"{(fr[:, 14].max() - np.median(fr[:, 14])) / 1e3:.2f}) | gap front->fc1 {(cs - fe) / 1e3:.2f} us | "
+          f"fc1 span {(ce - cs) / 1e3:.2f} us | gap fc1->next front {per_round - (ce - fs) / 1e3:.2f} us (by subtraction)")
+    # clock64 vs globaltimer on the same CTA span (sanity): front marks 0 (start) .. 12 (out done)
+    cyc = (fr[:, 12] - fr[:, 0]).astype(np.float64)
+    ns = (fr[:, 14] - fr[:, 13]).astype(np.float64)
+    print(f"   front per-CTA: clock64 {np.median(cyc):.0f} cyc vs globaltimer {np.median(ns):.0f} ns -> "
+          f"{np.median(cyc) / max(np.median(ns), 1):.3f} cyc/ns")
+    cyc1 = (f1[:, 4] - f1[:, 0]).astype(np.float64)
+    ns1 = (f1[:, 9] - f1[:, 8]).astype(np.float64)
+    print(f"   fc1 per-CTA: clock64 {np.median(cyc1):.0f} cyc vs globaltimer {np.median(ns1):.0f} ns")
+    print(f"   fc1 start->tile0 epilogue: globaltimer {np.median(f1[:, 10] - f1[:, 8]):.0f} ns, clock64 "
+          f"{np.median(f1[:, 4] - f1[:, 0]):.0f} cyc; end-start {np.median(f1[:, 9] - f1[:, 8]):.0f} ns")
