@@ -10,20 +10,22 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, _lib  # noqa: E402
 from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace  # noqa: E402
 
-t = synthetic_trace(300_000, 101)
+K = int(os.environ.get("K", "1024"))
+t = synthetic_trace(max(300_000, 300 * K), 101)
 m = synthetic_model(synthetic_trace(200_000, 101), 1)
 for prec in ("tf32x3", "bf16"):
     g = GpuSimulator(0, prec)
     g.load_model(m)
-    pc = ParallelConfig(k=1024)
+    pc = ParallelConfig(k=K)
     g.load_trace(t, pc)
     g.run(pc)
     buf = np.zeros(148 * 32 + 256 * 16, np.int64)
     _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
-    tr = buf[148 * 32:].reshape(256, 16)[:128].astype(np.float64)
+    tr = buf[148 * 32:].reshape(256, 16)[:144].astype(np.float64)
     rel = tr[:, :8] - tr[:, :1]
     names = ["start", "W landed", "A chunk0 ready", "tile0 MMAs issued", "tile0 epilogue done", "tile1 MMAs issued",
-             "tile1 epilogue done"]
+             "tile1 epilogue done", "end (globaltimer ns)"]
+    tr[:, 7] = (tr[:, 9] - tr[:, 8]) * 1.87 + tr[:, 0]  # end, converted to cycles at ~1.87 cyc/ns
     print(prec)
     for i, n in enumerate(names):
         col = rel[:, i][tr[:, i] > 0]
