@@ -124,6 +124,14 @@ int ilsim_gpu_load_model(ilsim_gpu_ctx* ctx, const ilsim_cnn_config* cfg, const 
 int ilsim_gpu_load_trace(ilsim_gpu_ctx* ctx, const ilsim_trace_view* trace,
                          const ilsim_sim_config* cfg);
 
+/* GPU trace ingest: the same, straight from the SNT1 record bytes (the file
+ * body after its 24-byte header, trace.cpp:49-83 / 102-124).  The shard's
+ * 108-byte records are copied to the device and unpacked there (read_record
+ * semantics: address and size are zero without data); the host does no
+ * per-record work.  with_truth: also keep the recorded latencies (oracle).   */
+int ilsim_gpu_load_trace_records(ilsim_gpu_ctx* ctx, const void* records, uint64_t n,
+                                 const ilsim_sim_config* cfg, int32_t with_truth);
+
 /* Round loop over the loaded trace (simulate_parallel, parallel.cpp:26-93, or
  * simulate_trace, simcore.cpp:185-196, when cfg->sequential).
  * subs: one per simulated sub-trace (shard); predicted_fetch: per owned

@@ -108,6 +108,7 @@ EXPORTS = [
     "ilsim_gpu_last_error",
     "ilsim_gpu_load_model",
     "ilsim_gpu_load_trace",
+    "ilsim_gpu_load_trace_records",
     "ilsim_gpu_run",
     "ilsim_gpu_simulate_parallel",
     "ilsim_gpu_predict",
@@ -138,6 +139,7 @@ def lib() -> C.CDLL:
     L.ilsim_gpu_last_error.restype = C.c_char_p
     L.ilsim_gpu_load_model.argtypes = [vp, C.POINTER(CnnCfg), vp, vp, u64]
     L.ilsim_gpu_load_trace.argtypes = [vp, C.POINTER(TraceView), C.POINTER(SimCfg)]
+    L.ilsim_gpu_load_trace_records.argtypes = [vp, vp, u64, C.POINTER(SimCfg), i32]
     L.ilsim_gpu_run.argtypes = [vp, C.POINTER(SimCfg), vp, u64, vp, C.POINTER(Totals)]
     L.ilsim_gpu_simulate_parallel.argtypes = [vp, C.POINTER(TraceView), C.POINTER(SimCfg), vp, u64, vp,
                                               C.POINTER(Totals)]
@@ -149,7 +151,8 @@ def lib() -> C.CDLL:
     L.ilsim_gpu_param_count.argtypes = [C.POINTER(CnnCfg)]
     L.ilsim_gpu_param_count.restype = u64
     L.ilsim_gpu_init_weights.argtypes = [C.POINTER(CnnCfg), u64, vp, u64, C.c_char_p, C.c_int]
-    for f in (L.ilsim_gpu_create, L.ilsim_gpu_load_model, L.ilsim_gpu_load_trace, L.ilsim_gpu_run,
+    for f in (L.ilsim_gpu_create, L.ilsim_gpu_load_model, L.ilsim_gpu_load_trace, L.ilsim_gpu_load_trace_records,
+              L.ilsim_gpu_run,
               L.ilsim_gpu_simulate_parallel, L.ilsim_gpu_predict, L.ilsim_gpu_set_capture,
               L.ilsim_gpu_partition, L.ilsim_gpu_init_weights):
         f.restype = i32

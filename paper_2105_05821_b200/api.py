@@ -248,6 +248,20 @@ class GpuSimulator:
         self._trace_n = trace.n
         del keep
 
+    def load_trace_file(self, path: str, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None,
+                        truth: bool = False) -> int:
+        """GPU trace ingest: upload this configuration's slice of an SNT1 file's
+        raw records and unpack them on the device (no host parsing).  Returns
+        the trace length."""
+        from .formats import trace_records
+
+        body, n, _ = trace_records(path)
+        cfg = self._sim_cfg(pc, sequential=sequential, oracle=oracle, shard=shard)
+        ptr = body.ctypes.data if n else None
+        self._check(self.L.ilsim_gpu_load_trace_records(self._h, ptr, n, C.byref(cfg), int(oracle or truth)))
+        self._trace_n = n
+        return n
+
     def run(self, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None, profile=False,
             truth_inputs=False, n_total: int | None = None, fused=True) -> ParallelResult:
         """Round loop over the loaded trace.  ``truth_inputs``: test hook, truth
@@ -343,8 +357,11 @@ def throughput_csv(rows: list[tuple[int, int, float]]) -> str:
 def simulate(trace_path: str, model_path: str = "", oracle: bool = False, parallel: int = 1,
              subtrace_size: int = 0, batch_max: int = 4096, *, precision: str = "tf32x3", device: int = 0,
              warmup: int = 0, drain_trim: bool = False) -> dict:
-    """``ilsim.simulate`` (bindings/module.cpp:117-156) on the GPU."""
-    trace = read_trace(trace_path)
+    """``ilsim.simulate`` (bindings/module.cpp:117-156) on the GPU; the trace
+    file's records are unpacked on the device (GPU trace ingest)."""
+    from .formats import trace_records
+
+    n_trace = trace_records(trace_path)[1]
     sim = SimConfig()
     with GpuSimulator(device, precision) as g:
         if not oracle:
@@ -355,11 +372,14 @@ def simulate(trace_path: str, model_path: str = "", oracle: bool = False, parall
         if parallel > 1 or subtrace_size > 0:
             pc = ParallelConfig(k=parallel, subtrace_size=subtrace_size, batch_max=batch_max, sim=sim,
                                 warmup=warmup, drain_trim=drain_trim)
-            pr = g.simulate_parallel(trace, pc, oracle=oracle)
-            d = _agg_dict(pr.sub_results, pr.instructions, pr.total_cycles, pr.cpi, trace.n == 0)
+            g.load_trace_file(trace_path, pc, oracle=oracle)
+            pr = g.run(pc, oracle=oracle)
+            d = _agg_dict(pr.sub_results, pr.instructions, pr.total_cycles, pr.cpi, n_trace == 0)
             d["sub_traces"] = len(pr.sub_results)
             return d
-        r = g.simulate_trace(trace, sim, oracle=oracle)
+        pc = ParallelConfig(k=1, sim=sim)
+        g.load_trace_file(trace_path, pc, sequential=True, oracle=oracle)
+        r = g.run(pc, sequential=True, oracle=oracle).sub_results[0]
         return _agg_dict([r], r.instructions, r.total_cycles, r.cpi, r.empty)
 
 

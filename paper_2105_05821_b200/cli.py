@@ -21,7 +21,7 @@ import numpy as np
 
 from .api import GpuSimulator, ParallelConfig, SimConfig, throughput_csv
 from .errors import IlsimError
-from .formats import read_trace
+from .formats import trace_records
 
 
 def phase_cpi(fetch: np.ndarray, window: int) -> tuple[list[float], bool]:
@@ -55,7 +55,7 @@ def phase_cpi_csv(cpi: list[float]) -> str:
 
 
 def cmd_simulate(a) -> int:
-    trace = read_trace(a.trace)
+    n_trace = trace_records(a.trace)[1]  # header checks; the records are unpacked on the GPU
     sim = SimConfig()
     with GpuSimulator(a.device, a.precision) as g:
         if not a.oracle:
@@ -67,19 +67,22 @@ def cmd_simulate(a) -> int:
         if a.parallel > 1 or a.subtrace_size > 0:
             pc = ParallelConfig(k=a.parallel, subtrace_size=a.subtrace_size, batch_max=a.batch_max, sim=sim,
                                 warmup=a.warmup, drain_trim=a.drain_trim)
-            pr = g.simulate_parallel(trace, pc, oracle=a.oracle)
+            g.load_trace_file(a.trace, pc, oracle=a.oracle)
+            pr = g.run(pc, oracle=a.oracle)
             subs, n, total, cpi, fetch = pr.sub_results, pr.instructions, pr.total_cycles, pr.cpi, pr.predicted_fetch
         else:
-            r = g.simulate_trace(trace, sim, oracle=a.oracle)
+            pc = ParallelConfig(k=1, sim=sim)
+            g.load_trace_file(a.trace, pc, sequential=True, oracle=a.oracle)
+            r = g.run(pc, sequential=True, oracle=a.oracle).sub_results[0]
             subs, n, total, cpi, fetch = [r], r.instructions, r.total_cycles, r.cpi, r.predicted_fetch
         seconds = time.perf_counter() - t0
     agg = {"instructions": n, "total_cycles": total, "cpi": cpi,
            "sum_fetch": sum(s.sum_fetch for s in subs), "delta": sum(s.delta for s in subs),
            "drain_cycles": sum(s.drain_cycles for s in subs),
-           "overflow_stall_cycles": sum(s.overflow_stall_cycles for s in subs), "empty": trace.n == 0}
+           "overflow_stall_cycles": sum(s.overflow_stall_cycles for s in subs), "empty": n_trace == 0}
     with open(a.report, "w") as f:
         f.write(sim_report_csv(agg))
-    w = a.window if a.window > 0 else max(1, trace.n // 100)
+    w = a.window if a.window > 0 else max(1, n_trace // 100)
     if fetch is not None and len(fetch) > 0:
         cpis, _ = phase_cpi(fetch, w)
         with open(a.phase_report or a.report + ".phase.csv", "w") as f:

@@ -112,6 +112,7 @@ struct ilsim_gpu_ctx {
 
   // run buffers
   DevBuf state, proc, wq, x, y, act, pred_fetch;
+  DevBuf rec_stage;  // SNT1 record staging for the GPU trace ingest
 
   // capture hook
   uint32_t cap_round = UINT32_MAX;
@@ -514,6 +515,30 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   tot->launches = launches;
 }
 
+// Shared tail of the trace loaders: flags + (model loaded) normalised static
+// slots of the uploaded slice, then the trace is ready.
+void finish_trace_load(ilsim_gpu_ctx* c, uint64_t m) {
+  c->packed_gen = ~0ull;
+  c->iflags.need(m);
+  // static slots depend on the model's NormStats: pack now if a model is loaded
+  if (m) {
+    PackParams pp{};
+    pp.n = m;
+    pp.op = c->op.as<uint8_t>();
+    pp.src = c->src.as<uint16_t>();
+    pp.dst = c->dst.as<uint16_t>();
+    pp.hist = c->hist.as<uint16_t>();
+    pp.nc = c->nc_dev.as<NormConsts>();
+    pp.stat = c->has_model ? static_cast<float*>(c->stat.need(m * kStatStride * sizeof(float))) : nullptr;
+    pp.iflags = c->iflags.as<uint8_t>();
+    launch_pack(pp, c->stream);
+    CUDA_OK(cudaGetLastError());
+    if (c->has_model) c->packed_gen = c->model_gen;
+  }
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  c->has_trace = true;
+}
+
 }  // namespace
 
 // --------------------------------------------------------------------------
@@ -629,25 +654,49 @@ int ilsim_gpu_load_trace(ilsim_gpu_ctx* c, const ilsim_trace_view* t, const ilsi
     upload(c->hist, t->hist + 14 * g0, 14 * m, c->stream);
     c->has_truth = t->truth != nullptr;
     if (c->has_truth) upload(c->truth, t->truth + 3 * g0, 3 * m, c->stream);
-    c->packed_gen = ~0ull;
-    c->iflags.need(m);
-    // static slots depend on the model's NormStats: pack now if a model is loaded
+    finish_trace_load(c, m);
+  });
+}
+
+int ilsim_gpu_load_trace_records(ilsim_gpu_ctx* c, const void* records, uint64_t n, const ilsim_sim_config* cfg,
+                                 int32_t with_truth) {
+  return guard(c, [&] {
+    const Plan P = make_plan(*cfg, n);
+    c->has_trace = false;
+    c->t_total = n;
+    c->g0 = P.g0;
+    c->g1 = P.g1;
+    const uint64_t g0 = P.g0, m = P.g1 - P.g0;
+    constexpr uint64_t kRec = 108, kStageRecs = 1ull << 22;  // 432 MB staging at most
+    c->pc.need(m * 8);
+    c->addr.need(m * 8);
+    c->op.need(m * 13);
+    c->src.need(m * 16);
+    c->dst.need(m * 12);
+    c->hist.need(m * 28);
+    c->has_truth = with_truth != 0;
+    if (c->has_truth) c->truth.need(m * 12);
     if (m) {
-      PackParams pp{};
-      pp.n = m;
-      pp.op = c->op.as<uint8_t>();
-      pp.src = c->src.as<uint16_t>();
-      pp.dst = c->dst.as<uint16_t>();
-      pp.hist = c->hist.as<uint16_t>();
-      pp.nc = c->nc_dev.as<NormConsts>();
-      pp.stat = c->has_model ? static_cast<float*>(c->stat.need(m * kStatStride * sizeof(float))) : nullptr;
-      pp.iflags = c->iflags.as<uint8_t>();
-      launch_pack(pp, c->stream);
-      CUDA_OK(cudaGetLastError());
-      if (c->has_model) c->packed_gen = c->model_gen;
+      void* stage = c->rec_stage.need(std::min(m, kStageRecs) * kRec);
+      const uint8_t* src = static_cast<const uint8_t*>(records) + g0 * kRec;
+      for (uint64_t f = 0; f < m; f += kStageRecs) {
+        const uint64_t k = std::min(kStageRecs, m - f);
+        CUDA_OK(cudaMemcpyAsync(stage, src + f * kRec, k * kRec, cudaMemcpyHostToDevice, c->stream));
+        UnpackParams u{};
+        u.rec = static_cast<const uint8_t*>(stage);
+        u.n = k;
+        u.pc = c->pc.as<uint64_t>() + f;
+        u.addr = c->addr.as<uint64_t>() + f;
+        u.op = c->op.as<uint8_t>() + 13 * f;
+        u.src = c->src.as<uint16_t>() + 8 * f;
+        u.dst = c->dst.as<uint16_t>() + 6 * f;
+        u.hist = c->hist.as<uint16_t>() + 14 * f;
+        u.truth = c->has_truth ? c->truth.as<uint32_t>() + 3 * f : nullptr;
+        launch_unpack_records(u, c->stream);
+        CUDA_OK(cudaGetLastError());
+      }
     }
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    c->has_trace = true;
+    finish_trace_load(c, m);
   });
 }
 

@@ -255,6 +255,50 @@ void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t*
       y, y_stride, n, is_store, nc, cf, ce, cs, out);
 }
 
+// ---------------------------------------------------------------------------
+// GPU trace ingest: a block stages 256 records (27,648 B) in shared memory with
+// coalesced 16-B loads, then each thread extracts its record's fields
+// (read_record, trace.cpp:64-83: address / size read as 0 without data).
+// ---------------------------------------------------------------------------
+constexpr int kRecBytes = 108, kRecPerBlock = 256;
+
+__global__ void __launch_bounds__(kRecPerBlock) unpack_records_kernel(UnpackParams p) {
+  __shared__ __align__(16) uint8_t srec[kRecPerBlock * kRecBytes];
+  const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kRecPerBlock;
+  const uint64_t nrec = p.n - r0 < kRecPerBlock ? p.n - r0 : kRecPerBlock;
+  const uint32_t bytes = static_cast<uint32_t>(nrec * kRecBytes);
+  const uint8_t* src = p.rec + r0 * kRecBytes;  // 4-byte aligned (108 = 27 x 4)
+  for (uint32_t i = threadIdx.x; i < bytes / 4; i += kRecPerBlock)
+    reinterpret_cast<uint32_t*>(srec)[i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+  __syncthreads();
+  if (threadIdx.x >= nrec) return;
+  const uint8_t* b = srec + threadIdx.x * kRecBytes;
+  const uint64_t i = r0 + threadIdx.x;
+  auto u16 = [&](int o) { return static_cast<uint16_t>(b[o] | (b[o + 1] << 8)); };
+  auto u32 = [&](int o) { return static_cast<uint32_t>(u16(o)) | (static_cast<uint32_t>(u16(o + 2)) << 16); };
+  auto u64 = [&](int o) { return static_cast<uint64_t>(u32(o)) | (static_cast<uint64_t>(u32(o + 4)) << 32); };
+  p.pc[i] = u64(0);
+#pragma unroll
+  for (int k = 0; k < 13; ++k) p.op[i * 13 + k] = b[8 + k];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) p.src[i * 8 + k] = u16(21 + 2 * k);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) p.dst[i * 6 + k] = u16(37 + 2 * k);
+  const bool has = b[49] != 0;
+  p.addr[i] = has ? u64(50) : 0ull;
+#pragma unroll
+  for (int k = 0; k < 14; ++k) p.hist[i * 14 + k] = u16(60 + 2 * k);
+  if (p.truth) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p.truth[i * 3 + k] = u32(88 + 4 * k);
+  }
+}
+
+void launch_unpack_records(const UnpackParams& p, cudaStream_t stream) {
+  if (p.n == 0) return;
+  unpack_records_kernel<<<static_cast<unsigned>((p.n + kRecPerBlock - 1) / kRecPerBlock), kRecPerBlock, 0, stream>>>(p);
+}
+
 void launch_pack(const PackParams& p, cudaStream_t stream) {
   if (p.n == 0) return;
   dim3 block(64, 4);

@@ -63,6 +63,20 @@ void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t*
                         const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
                         cudaStream_t stream);
 void launch_pack(const PackParams& p, cudaStream_t stream);
+
+// SNT1 records (108 B, trace.cpp:49-83) -> device structure-of-arrays.
+struct UnpackParams {
+  const uint8_t* rec;  // n records
+  uint64_t n;
+  uint64_t* pc;
+  uint64_t* addr;
+  uint8_t* op;         // [n][13]
+  uint16_t* src;       // [n][8]
+  uint16_t* dst;       // [n][6]
+  uint16_t* hist;      // [n][14]
+  uint32_t* truth;     // [n][3] or null
+};
+void launch_unpack_records(const UnpackParams& p, cudaStream_t stream);
 // Caller inputs [n][width] f32 -> gathered-input layout (ilsim_gpu_predict).
 void launch_pack_inputs(const float* in, uint64_t n, uint32_t width, void* x, uint32_t x_stride, int x_bf16,
                         uint64_t x_lo_off, cudaStream_t stream);

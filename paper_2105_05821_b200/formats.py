@@ -112,6 +112,34 @@ def read_trace(path: str | Path) -> Trace:
     return Trace.from_records(rec, config_hash)
 
 
+def trace_records(path: str | Path) -> tuple[np.ndarray, int, int]:
+    """The raw 108-byte SNT1 records of a trace file, memory-mapped, after the
+    header checks of ``read_trace`` (trace.cpp:102-124): (uint8 body, count,
+    config hash).  No per-record work on the host (GPU trace ingest)."""
+    path = str(path)
+    try:
+        size = Path(path).stat().st_size
+        with open(path, "rb") as f:
+            head = f.read(24)
+    except OSError:
+        raise IlsimError("cannot open file for reading: " + path) from None
+    if len(head) < 4 or head[:4] != _TRACE_MAGIC:
+        raise IlsimError("bad trace magic in " + path)
+    if len(head) < 24:
+        raise IlsimError("truncated file: " + path)
+    version, config_hash, count = struct.unpack_from("<IQQ", head, 4)
+    if version != 1:
+        raise IlsimError(f"unsupported trace version {version} in {path}")
+    body = size - 24
+    if body < count * RECORD.itemsize:
+        raise IlsimError(f"trace truncated at record {body // RECORD.itemsize} in {path}")
+    if body > count * RECORD.itemsize:
+        raise IlsimError(f"trailing bytes after record {count} in {path}")
+    if count == 0:
+        return np.zeros(0, np.uint8), 0, config_hash
+    return np.memmap(path, dtype=np.uint8, mode="r", offset=24, shape=(count * RECORD.itemsize,)), count, config_hash
+
+
 def write_trace(path: str | Path, t: Trace, config_hash: int = 0) -> None:
     """``write_trace`` (trace.cpp:87-100); validation is the caller's job here."""
     with open(path, "wb") as f:

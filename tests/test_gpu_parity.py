@@ -414,3 +414,25 @@ def test_sharded_fused_rounds_compose(gpu, port):
     got = np.concatenate([gpu_subs(p) for p in parts])
     assert np.array_equal(got, gpu_subs(full))
     assert np.array_equal(np.concatenate([p.predicted_fetch for p in parts]), full.predicted_fetch)
+
+
+@pytest.mark.parametrize("oracle", [True, False])
+def test_gpu_trace_ingest_matches_host_path(gpu, port, golden, oracle):
+    """SNT1 records unpacked on the device (load_trace_file) = the host SoA path."""
+    g = gpu("tf32x3")
+    g.load_model(c3_model(port, golden))
+    path = GOLD / "pointer_chase_2000_s3.trace"
+    t = read_trace(path)
+    for pc in (pcfg(7), pcfg(5, warmup=30)):
+        g.load_trace(t, pc, oracle=oracle)
+        a = g.run(pc, oracle=oracle)
+        n = g.load_trace_file(str(path), pc, oracle=oracle)
+        b = g.run(pc, oracle=oracle)
+        assert n == t.n
+        assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    for shard in ((0, 3), (3, 7)):
+        g.load_trace(t, pcfg(7), oracle=oracle, shard=shard)
+        a = g.run(pcfg(7), oracle=oracle, shard=shard)
+        g.load_trace_file(str(path), pcfg(7), oracle=oracle, shard=shard)
+        b = g.run(pcfg(7), oracle=oracle, shard=shard)
+        assert np.array_equal(gpu_subs(a), gpu_subs(b))

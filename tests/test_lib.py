@@ -150,3 +150,22 @@ int main() {
     import torch
 
     assert out.startswith("ok" if torch.cuda.is_available() else "error:"), out
+
+
+def test_trace_records_header_checks(tmp_path):
+    """The GPU-ingest reader applies read_trace's header checks (trace.cpp:102-124)."""
+    import pytest as _pt
+
+    from paper_2105_05821_b200 import IlsimError
+    from paper_2105_05821_b200.formats import read_trace, trace_records
+
+    gold = __import__("conftest").GOLDEN / "mix_3000_s4.trace"
+    body, n, _ = trace_records(gold)
+    assert n == read_trace(gold).n and body.size == n * 108
+    raw = gold.read_bytes()
+    (tmp_path / "bad.trace").write_bytes(b"XXXX" + raw[4:])
+    with _pt.raises(IlsimError, match="bad trace magic"):
+        trace_records(tmp_path / "bad.trace")
+    (tmp_path / "short.trace").write_bytes(raw[:-5])
+    with _pt.raises(IlsimError, match="trace truncated at record"):
+        trace_records(tmp_path / "short.trace")
