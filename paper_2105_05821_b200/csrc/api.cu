@@ -361,11 +361,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   auto run_span = [&](uint64_t f, uint64_t l, uint64_t off, cudaStream_t st) -> uint64_t {
     ForwardBuffers fbs = oracle ? fb : fb_slice(c->model, fb, off);
     if (fused) fbs.part_off = f;
-    if (fused) {
-      static const int ko = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
-      const uint64_t n1 = (ko & 8) ? 0 : do_front(f, l, nullptr, fbs, st);
-      return n1 + ((ko & 4) ? 0 : do_fc(f, l, fbs, st));
-    }
+    if (fused) return do_front(f, l, nullptr, fbs, st) + do_fc(f, l, fbs, st);
     return do_ctx(f, l, true, off, st) + do_forward(f, l, off, fbs, st) + do_decode(f, l, fbs, st);
   };
 
@@ -491,7 +487,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     if (st.status == kErrWriteRing)
       throw ApiError("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
                      std::to_string(i) + "; raise write_ring");
-    if (st.pos != st.len && !std::getenv("SIMNET_KNOCKOUT")) throw ApiError("internal: sub-trace did not finish");
+    if (st.pos != st.len) throw ApiError("internal: sub-trace did not finish");
     ilsim_sub_result& r = subs[j];
     r.instructions = st.len - st.warm;
     r.total_cycles = st.cur - st.base_cur;

@@ -711,8 +711,6 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
                             t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
   fp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
   if (!fp.calibrate) fp.c1acc = t.c1acc.as<float>();
-  static const int knockout = std::getenv("SIMNET_KNOCKOUT") ? std::atoi(std::getenv("SIMNET_KNOCKOUT")) : 0;
-  fp.knockout = knockout;
   launch_round_front(t.mode, w, fp, num_sms(), s);
   return 1;
 }

@@ -407,7 +407,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
             st.awaiting = 0;
             dirty = true;
           }
-          if (st.status == kOk && st.has_pend && !(p.knockout & 2)) {
+          if (st.status == kOk && st.has_pend) {
             k1::apply_step(st, r, aa);
             dirty = true;
           }
@@ -476,7 +476,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
               p.stat + static_cast<uint64_t>(live ? tbl_inst[warp * kTblCols + col] : 0u) * kStatStride);
 #pragma unroll
           for (int i = 0; i < 11; ++i) q[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-          if (live && !(p.knockout & 1)) {
+          if (live) {
 #pragma unroll
             for (int i = 0; i < 11; ++i) q[i] = __ldg(srow + i);
           }

@@ -45,7 +45,6 @@ struct FrontParams {
   float* c1acc_out;          // calibration launch: where to write it
   int32_t calibrate;         // 1: no sub-traces, all-zero input (calibration)
   long long* trace;          // optional: per-CTA event clocks of the first item (diagnostics)
-  int32_t knockout;          // diagnostics only (SIMNET_KNOCKOUT): 1 = no static loads, 2 = no apply
 };
 
 // w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
