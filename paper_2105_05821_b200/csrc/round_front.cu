@@ -465,7 +465,6 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       // one context column) per thread per tile: 11 float4 static-slot loads in
       // flight, the 9 dynamic slots from the column table, 16-B stores.
       for (int t = 0; t < T; ++t) {
-        if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);  // conv0 MMAs of tile t-1 done reading R1
         const int col = 32 * t + lane;
         const int r = warp * kRowsT + (lane >> 1), h = lane & 1;
         const bool live = col <= s_ncols[warp];
@@ -502,6 +501,9 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
             for (int k = 0; k < kSlots; ++k) v[k] = 0.0f;
           }
         }
+        // loads and values above overlap the previous tile's MMAs; only the
+        // operand writes wait for them to finish reading R1
+        if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);
         if (h == 0) {  // K 0..49
 #pragma unroll
           for (int i = 0; i < 12; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
