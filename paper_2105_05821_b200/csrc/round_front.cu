@@ -209,6 +209,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __shared__ __align__(8) uint64_t bar_w1f;        // conv1 MMAs done (W1 free), 1 / item
   __shared__ __align__(8) uint64_t bar_a2, bar_m2; // conv2 A restaged / MMAs done: 1 / item
   __shared__ __align__(8) uint64_t bar_w2;         // FC2 weights landed in R1 (bulk copy), 1 / item
+  __shared__ __align__(8) uint64_t bar_st;         // the item's SubStates landed (bulk copy), 1 / item
+  __shared__ __align__(16) SubState s_state[kItem];
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[3][kC];
   __shared__ float s_zero[kSlots], s_one[kSlots];
@@ -251,6 +253,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     mbar_init(&bar_a2, kCompute);
     mbar_init(&bar_m2, 1);
     mbar_init(&bar_w2, 1);
+    mbar_init(&bar_st, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -294,6 +297,22 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           }
         }
         load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
+        {  // the item's sub-trace states, contiguous in HBM: one bulk copy, ahead of the decode
+          if (it == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round final (PDL)
+          const uint64_t s0 = p.first + static_cast<uint64_t>(item) * kItem;
+          const uint64_t cnt = p.calibrate ? 0 : (p.last - s0 < kItem ? p.last - s0 : kItem);
+          const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(SubState));
+          if (bytes == 0) {
+            mbar_arrive(&bar_st);
+          } else {
+            mbar_expect_tx(&bar_st, bytes);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    su32(s_state)),
+                "l"(p.state + s0), "r"(bytes), "r"(su32(&bar_st))
+                : "memory");
+          }
+        }
         mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
         load_w(1, &tmW1, &tmW1lo, S::kKChunks);
         mbar_wait(&bar_w1f, it & 1);  // conv1 MMAs done: W1 no longer read
@@ -396,7 +415,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         if (mine) {
           const k1::Rings r = k1::rings_of(p.proc, p.wq, p.pmask, p.wmask, s);
           SubState* sp = p.state + s;
-          SubState st = *sp;
+          mbar_wait(&bar_st, it & 1);  // prefetched by the producer during the decode
+          SubState st = s_state[warp];
           bool dirty = false;
           if (st.status == kOk && st.awaiting) {  // K3 of the previous round for this sub-trace
             uint32_t tri[3];
