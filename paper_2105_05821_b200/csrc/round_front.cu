@@ -211,6 +211,9 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __shared__ __align__(8) uint64_t bar_w2;         // FC2 weights landed in R1 (bulk copy), 1 / item
   __shared__ __align__(8) uint64_t bar_st;         // the item's SubStates landed (bulk copy), 1 / item
   __shared__ __align__(16) SubState s_state[kItem];
+  __shared__ __align__(8) uint64_t bar_tg;         // the items' next-target pc / address / flags prefetched
+  __shared__ uint64_t s_tidx[kItem], s_tpc[kItem], s_taddr[kItem];
+  __shared__ uint32_t s_tfl[kItem];
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[3][kC];
   __shared__ float s_zero[kSlots], s_one[kSlots];
@@ -254,6 +257,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     mbar_init(&bar_m2, 1);
     mbar_init(&bar_w2, 1);
     mbar_init(&bar_st, 1);
+    mbar_init(&bar_tg, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -312,6 +316,31 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
                 "l"(p.state + s0), "r"(bytes), "r"(su32(&bar_st))
                 : "memory");
           }
+          // Each sub-trace's next gather target is pos (+1 when this round
+          // first applies a step): prefetch its pc / address / flags for the
+          // column table while the compute warps run the decode.
+          mbar_wait(&bar_st, it & 1);
+          uint64_t idx[kItem], tpc[kItem], tad[kItem];
+          uint32_t tfl[kItem];
+#pragma unroll
+          for (int w = 0; w < kItem; ++w) {
+            const SubState& ss = s_state[w];
+            const uint32_t pos = ss.pos + ((ss.awaiting || ss.has_pend) ? 1u : 0u);
+            const bool ok = w < static_cast<int>(cnt) && ss.status == kOk && pos < ss.len;
+            idx[w] = ok ? ss.begin + pos : ~0ull;
+            const uint64_t at = ok ? idx[w] : 0ull;
+            tpc[w] = ok ? p.pc[at] : 0ull;
+            tad[w] = ok ? p.addr[at] : 0ull;
+            tfl[w] = ok ? p.iflags[at] : 0u;
+          }
+#pragma unroll
+          for (int w = 0; w < kItem; ++w) {
+            s_tidx[w] = idx[w];
+            s_tpc[w] = tpc[w];
+            s_taddr[w] = tad[w];
+            s_tfl[w] = tfl[w];
+          }
+          mbar_arrive(&bar_tg);  // release: the smem stores above are visible to waiters
         }
         mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
         load_w(1, &tmW1, &tmW1lo, S::kKChunks);
@@ -440,8 +469,11 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           if (st.status == kOk && st.pos < st.len) {
             const uint64_t tgt = st.begin + st.pos;
             const uint32_t ncols = min(static_cast<uint32_t>(p.max_context), (st.pt - st.ph) + (st.wt - st.wh));
-            const uint64_t tpc = p.pc[tgt], taddr = p.addr[tgt];
-            const uint8_t tfl = p.iflags[tgt];
+            mbar_wait(&bar_tg, it & 1);
+            const bool pre = s_tidx[warp] == tgt;  // the producer's prediction of this round's target
+            const uint64_t tpc = pre ? s_tpc[warp] : p.pc[tgt];
+            const uint64_t taddr = pre ? s_taddr[warp] : p.addr[tgt];
+            const uint8_t tfl = pre ? static_cast<uint8_t>(s_tfl[warp]) : p.iflags[tgt];
             const bool tmemop = (tfl & kFlagMem) != 0;
             uint32_t* ti = tbl_inst + warp * kTblCols;
             float4* td = tbl_dyn + warp * kTblCols;
