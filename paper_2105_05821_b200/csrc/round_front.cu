@@ -134,6 +134,16 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 
+// Row order inside each sample's 16 rows of a tile.  Each restage lane pair
+// (positions 2j, 2j+1) lands in ONE next-layer row (K halves 0 and 64 share
+// banks), so a layer's rows are ordered so that every quarter-warp of the
+// restage (8 consecutive TMEM lanes) writes 8 distinct rows with distinct
+// swizzle phases: conflict-free 16-B stores.
+//   conv0: slot s holds position 2(s%8) + s/8 (evens in 0-7, odds in 8-15);
+//   conv1: position p sits in slot conv1_slot(p) (evens p/2, odds 8 + (p/2 ^ 4));
+//   conv2: natural (slot = position), so flat needs no reordering.
+__device__ __forceinline__ int conv1_slot(int p) { return (p & 1) ? 8 + ((p >> 1) ^ 4) : (p >> 1); }
+
 template <int kMode>
 __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float* accv, int ar, int k0,
                                             const float* bias) {
@@ -517,8 +527,11 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       // one context column) per thread per tile: 11 float4 static-slot loads in
       // flight, the 9 dynamic slots from the column table, 16-B stores.
       for (int t = 0; t < T; ++t) {
-        const int col = 32 * t + lane;
-        const int r = warp * kRowsT + (lane >> 1), h = lane & 1;
+        // lane -> (position q of the tile, K half h); row slot: even positions
+        // in slots 0-7, odd in 8-15 (see row_slot_c0 below)
+        const int q = 2 * ((lane >> 1) & 7) + (lane >> 4), h = lane & 1;
+        const int col = 32 * t + 2 * q + h;
+        const int r = warp * kRowsT + (lane >> 4) * 8 + ((lane >> 1) & 7);
         const bool live = col <= s_ncols[warp];
         float v[kSlots];
         {
@@ -569,7 +582,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           for (int k = 100; k < 100 + 2 * S::kPadUnits; k += 2) put2<kMode>(R1, S::kA0Lo, r, k, 0.0f, 0.0f);
         }
         if (p.dump) {
-          const int row = t * kRowsT + (lane >> 1);
+          const int row = t * kRowsT + q;
           const uint64_t smp = static_cast<uint64_t>(item) * kItem + warp;
           if (smp < samples && (row + 1) * 100 <= static_cast<int>(p.dump_stride)) {
             float* o = p.dump + smp * p.dump_stride + row * 100 + 50 * h;
@@ -592,11 +605,11 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           mbar_wait(&bar_m1, n_m1++ & 1);  // conv1 tile 0 consumed R1
           tc_fence_after();
         }
-        // conv0 tile t = 2u + half, row m = (sample m/16, position 16t + m%16)
-        //   -> conv1 tile u row (m/16)*16 + 8*half + (m%16)/2, K half (m%2)
+        // conv0 tile t = 2u + half, row m = (sample m/16, slot m%16 = position
+        // 16t + 2(m%8) + (m%16)/8) -> conv1 tile u, position 8*half + m%8, K half (m%16)/8
         const int t = 2 * u + half;
         restage_row<kMode>(R1, tmem + lane_off + t * kC, t >= T ? s_zacc : nullptr,
-                           (m >> 4) * 16 + 8 * half + ((m & 15) >> 1), (m & 1) * kC, sbias[0]);
+                           (m >> 4) * 16 + conv1_slot(8 * half + (m & 7)), ((m >> 3) & 1) * kC, sbias[0]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&bar_a1);
@@ -613,10 +626,14 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         if (lane == 0)
           for (int c = 0; c < kC; ++c) p.c1acc_out[c] = __uint_as_float(raw[c]);
       }
-      // conv1 tile `half`, row m = (sample m/16, position 16*half + m%16)
-      //   -> conv2 row (m/16)*16 + 8*half + (m%16)/2, K half (m%2)
-      restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, (half == 1 && n_c1 == 1) ? s_c1 : nullptr,
-                         (m >> 4) * 16 + 8 * half + ((m & 15) >> 1), (m & 1) * kC, sbias[1]);
+      // conv1 tile `half`, row m = (sample m/16, slot m%16 holding position
+      // 16*half + p, conv1_slot(p) = m%16) -> conv2 row (m/16)*16 + 8*half + p/2, K half p%2
+      {
+        const int sl = m & 15;
+        const int pair = sl < 8 ? sl : ((sl & 7) ^ 4);  // p / 2
+        restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, (half == 1 && n_c1 == 1) ? s_c1 : nullptr,
+                           (m >> 4) * 16 + 8 * half + pair, (sl >> 3) * kC, sbias[1]);
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&bar_a2);
