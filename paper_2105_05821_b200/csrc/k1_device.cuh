@@ -179,15 +179,25 @@ __device__ inline void apply_step(SubState& st, const Rings& r, const ApplyArgs&
 
 // memory_dependency_flags (dataset.cpp:47-60) of context entry e against the
 // target (tpc, taddr, tmem): bit b = flag b.
+// a / d == b / d (dataset.cpp:51-58 divides by line / page size); a power-of-two
+// d (the usual 64 / 4096) is a shift instead of a 64-bit division subroutine.
+__device__ __forceinline__ bool same_block(uint64_t a, uint64_t b, uint32_t d) {
+  if (d != 0u && (d & (d - 1u)) == 0u) {
+    const int sh = __ffs(static_cast<int>(d)) - 1;
+    return (a >> sh) == (b >> sh);
+  }
+  return a / d == b / d;
+}
+
 __device__ __forceinline__ uint32_t dep_flags(uint64_t tpc, uint64_t taddr, bool tmem, const RingEntry& e,
                                               uint32_t line, uint32_t page) {
-  uint32_t f = (tpc / line) == (e.pc / line) ? 1u : 0u;
+  uint32_t f = same_block(tpc, e.pc, line) ? 1u : 0u;
   if (tmem && (e.flags & kFlagMem)) {
     f |= (taddr == e.addr) ? 2u : 0u;
-    f |= (taddr / line) == (e.addr / line) ? 4u : 0u;
-    f |= (taddr / page) == (e.addr / page) ? 8u : 0u;
+    f |= same_block(taddr, e.addr, line) ? 4u : 0u;
+    f |= same_block(taddr, e.addr, page) ? 8u : 0u;
   }
-  f |= (tpc / page) == (e.pc / page) ? 16u : 0u;
+  f |= same_block(tpc, e.pc, page) ? 16u : 0u;
   return f;
 }
 

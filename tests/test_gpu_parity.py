@@ -313,19 +313,23 @@ def test_fused_front_matches_unfused(gpu, port, golden, precision):
         assert np.array_equal(a.predicted_fetch, b.predicted_fetch), (t.n, k)
 
 
-@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
-def test_fused_front_inputs_bit_exact(gpu, port, golden, precision):
+@pytest.mark.parametrize("precision,geom", [("tf32x3", (64, 4096)), ("bf16", (64, 4096)), ("tf32x3", (48, 3000))])
+def test_fused_front_inputs_bit_exact(gpu, port, golden, precision, geom):
     """Inputs gathered by the fused kernel (captured from its shared-memory
     operand as exact f32) equal the reference's next_request tensors for every
-    round up to the first decode divergence from the CPU oracle."""
+    round up to the first decode divergence from the CPU oracle.  geom: line /
+    page size of the dependency flags (dataset.cpp:48-58); 48 / 3000 takes the
+    division path, powers of two the shift path."""
     g = gpu(precision)
     m = c3_model(port, golden)
     g.load_model(m)
+    line, page = geom
     for t, k in ((read_trace(GOLD / "mix_3000_s4.trace"), 5), (store_heavy(31, 1500), 3)):
         pc = pcfg(k)
+        pc.sim.line_size, pc.sim.page_size = line, page
         g.load_trace(t, pc)
         got = g.run(pc)
-        want = port.simulate(t, m, k=k, capture=t.n, capture_inputs=True)
+        want = port.simulate(t, m, k=k, capture=t.n, capture_inputs=True, line_size=line, page_size=page)
         # rounds before the first differing fetch latency see identical queues
         diff = np.nonzero(got.predicted_fetch != want["predicted_fetch"])[0]
         idx = want["cap_index"]
