@@ -11,6 +11,7 @@
 #pragma once
 #include "common.cuh"
 #include "decode.cuh"
+#include "tc_common.cuh"
 
 namespace simnet {
 
@@ -63,8 +64,10 @@ __device__ __forceinline__ void warp_decode_triple(const float* y, const double*
 //   an fma chain over those units in order; the 32 lane partials of the 8
 //   samples are combined by a transpose reduction (xor 16, 8, 4) then a
 //   butterfly (xor 2, 1); y[s][o] = that + b2[o].
+// w2_bar: when non-null, W2 is still landing (bulk copy): wait on this
+// mbarrier phase parity right before FC2, after the partials are reduced.
 __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const float* w2s, float* hs, float* ys,
-                               long long* trace = nullptr) {
+                               long long* trace = nullptr, uint64_t* w2_bar = nullptr, uint32_t w2_parity = 0) {
   const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
   const int hid = a.hidden, c4 = hid >> 2;
   // biases fetched with the partials (no dependent global load later): lane j
@@ -104,6 +107,7 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
                       fmaxf(acc.w + b.w, 0.0f));
     }
   }
+  if (w2_bar) mbar_wait(w2_bar, w2_parity);
   fc_sync256();
   if (trace && threadIdx.x == 0) trace[0] = clock64();
   {  // FC2: warp w computes outputs o = w, w + 8, ... for all 8 samples

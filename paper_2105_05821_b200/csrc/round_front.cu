@@ -443,12 +443,11 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         const uint64_t s = p.first + static_cast<uint64_t>(item) * kItem + warp;
         const bool mine = s < p.last && !p.calibrate;
         // R1 is idle until the gather: W2 (bulk copy) | h [8][hidden] | y [8][64]
-        mbar_wait(&bar_w2, it & 1);
         if (tr && it == 0 && lane == 0 && warp == 0) tr[24] = clock64();
         float* hs = reinterpret_cast<float*>(R1) + kFcMaxOut * kFcMaxHidden;
         float* ys = hs + kItem * kFcMaxHidden;
         cta8_fc(p.fc, (mine ? s : p.first) - p.first, reinterpret_cast<const float*>(R1), hs, ys,
-                (tr && it == 0) ? tr + 28 : nullptr);
+                (tr && it == 0) ? tr + 28 : nullptr, &bar_w2, it & 1);
         if (tr && it == 0 && lane == 0 && warp == 0) tr[25] = clock64();
         int ncs = -1;
         if (mine) {
