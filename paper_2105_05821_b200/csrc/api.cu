@@ -365,17 +365,24 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     return do_ctx(f, l, true, off, st) + do_forward(f, l, off, fbs, st) + do_decode(f, l, fbs, st);
   };
 
+  constexpr uint32_t kGraphRounds = 16;
   auto launch_rounds = [&](uint32_t reps) -> uint64_t {
     uint64_t launches = 0;
-    for (uint32_t r = 0; r < reps; ++r)
+    for (uint32_t r = 0; r < reps; ++r) {
+      // SIMNET_CHAIN_TRACE: with a 16-round graph, only its middle round is
+      // traced, so the buffer ends up holding a typical round (not the last)
+      chain_trace_on() = rounds < kGraphRounds || (reps > 1 && (r == reps / 2 || r == reps / 2 + 1));
+      chain_trace_slot() = reps > 1 && r == reps / 2 + 1 ? 1 : 0;
       for (uint64_t f = 0; f < K; f += chunk) launches += run_span(f, std::min(K, f + chunk), 0, c->stream);
+    }
+    chain_trace_on() = true;
+    chain_trace_slot() = 0;
     return launches;
   };
 
   if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
   if (capture_mode && !fused && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
   const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs
-  constexpr uint32_t kGraphRounds = 16;
   cudaGraphExec_t g1 = nullptr, gN = nullptr;
   uint64_t launches_1 = 0, launches_n = 0;
   if (!capture_mode && !profile) {

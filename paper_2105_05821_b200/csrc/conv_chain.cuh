@@ -26,5 +26,20 @@ inline long long*& chain_trace_ptr() {
   static long long* p = nullptr;
   return p;
 }
+// Diagnostics: whether the launch being recorded writes the trace buffer (the
+// round loop traces one mid-graph round instead of the final one).
+inline bool& chain_trace_on() {
+  static bool on = true;
+  return on;
+}
+// Two consecutive rounds are traced into slots 0 and 1 (kChainTraceWords each).
+constexpr int kChainTraceWords = 148 * 32 + 256 * 16;
+inline int& chain_trace_slot() {
+  static int slot = 0;
+  return slot;
+}
+inline long long* chain_trace_active() {
+  return chain_trace_on() && chain_trace_ptr() ? chain_trace_ptr() + chain_trace_slot() * kChainTraceWords : nullptr;
+}
 
 }  // namespace simnet

@@ -65,12 +65,15 @@ struct TcGemmParams {
   uint64_t out_split_stride;  // elements between split-K partial planes
   long long* trace;           // diagnostics (SIMNET_CHAIN_TRACE): per-CTA event clocks, 16 per CTA
   int stages;                 // A ring depth (2..kStages; 0 = kStages)
+  int tma_out;                // f32 split-K partials through tmOut: CTAs owning one M tile stage the
+                              // accumulator in the idle A ring and TMA-store it (coalesced, async)
 };
 
 template <int kMode>
 __global__ void __launch_bounds__(kLayerThreads, 1)
 tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmBlo, TcGemmParams p) {
+                const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmOut,
+                TcGemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr bool kSplit = kMode == kTF32x3;
   uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
@@ -130,6 +133,34 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // A CTA that owns exactly one M tile has its split warps (2-5) idle once the
   // tile's chunks are split: they drain half of the accumulator columns.
   const bool solo = blockIdx.x < p.m_tiles && blockIdx.x + gridDim.x >= p.m_tiles && p.n % 32 == 0;
+  const bool tma_out = solo && p.tma_out;
+  // Solo CTA, TMA-stored partials: the tile's MMAs are done, so the A ring is
+  // free; column group g (32 floats) of the accumulator goes to sA + g * 16 KB
+  // as 128 rows x 128 B, SWIZZLE_128B (conflict-free 16-B stores), and each
+  // warp TMA-stores its 32 rows x 32 columns boxes.
+  auto epilogue_tma = [&](int t, int cb, int ce) {
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      float v[32];
+      tmem_ld16(tl + c0, v);
+      tmem_ld16(tl + c0 + 16, v + 16);
+      uint8_t* stg = sA + (c0 >> 5) * kAChunk + r * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(stg + ((q ^ (r & 7)) << 4)) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      for (int c0 = cb; c0 < ce; c0 += 32)
+        tma_store_3d(&tmOut, sA + (c0 >> 5) * kAChunk + quad * 32 * 128, ntile * p.n + c0, t * kBM + quad * 32, ks);
+      bulk_commit();
+      bulk_wait_all();  // complete before the CTA exits
+    }
+  };
   auto epilogue = [&](int t, int acc, int cb, int ce) {
     const int quad = warp & 3;
     const int row = t * kBM + quad * 32 + lane;
@@ -174,6 +205,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (kSplit) tma_load_2d(sWlo + c * bBytes, &tmBlo, &bar_w, (kc0 + c) * elems, ntile * p.n);
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (tr) tr[12] = global_ns();  // the previous kernel's results are visible
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
@@ -276,7 +308,10 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       asm volatile("griddepcontrol.wait;" ::: "memory");
       mbar_wait(&bar_acc_full[0], 0);
       tc_fence_after();
-      epilogue(blockIdx.x, 0, p.n / 2, p.n);
+      if (tma_out)
+        epilogue_tma(blockIdx.x, p.n / 2, p.n);
+      else
+        epilogue(blockIdx.x, 0, p.n / 2, p.n);
       tc_fence_before();
     }
   } else {
@@ -287,7 +322,10 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int acc = it & 1;
       mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
       tc_fence_after();
-      epilogue(t, acc, 0, solo ? p.n / 2 : p.n);
+      if (tma_out)
+        epilogue_tma(t, 0, p.n / 2);
+      else
+        epilogue(t, acc, 0, solo ? p.n / 2 : p.n);
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
       if (tr && warp == 6 && lane == 0 && it < 2) {
@@ -298,10 +336,13 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
   tc_fence_before();
   __syncthreads();
-  if (tr && threadIdx.x == 0) tr[9] = global_ns();
   if (warp == 1) {
+    // diagnostics: past the final barrier (thread 0, the producer lane, may
+    // leave it before the epilogue warps arrive, so warp 1 takes the stamp)
+    if (tr && lane == 0) tr[9] = global_ns();
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+    if (tr && lane == 0) tr[13] = global_ns();  // diagnostics: TMEM released, CTA about to exit
   }
 }
 
@@ -488,15 +529,18 @@ int num_sms() {
 }
 
 void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
-                 const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
+                 const CUtensorMap& out, const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
   num_sms();
   const int groups = ny * nz;
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
   const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages);
-  if (mode == kBF16) launch_pdl_tag("layer_bf16", tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
-  else if (mode == kTF32) launch_pdl_tag("layer", tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
-  else launch_pdl_tag("layer", tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, p);
+  if (mode == kBF16)
+    launch_pdl_tag("layer_bf16", tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
+  else if (mode == kTF32)
+    launch_pdl_tag("layer", tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
+  else
+    launch_pdl_tag("layer", tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
 }
 
 }  // namespace
@@ -524,7 +568,7 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   conv_chain_set_attributes();
   round_front_set_attributes();
   if (std::getenv("SIMNET_CHAIN_TRACE") && !chain_trace_ptr())  // diagnostics buffer, allocated outside capture
-    CUDA_OK(cudaMalloc(&chain_trace_ptr(), (148 * 32 + 256 * 16) * sizeof(long long)));
+    CUDA_OK(cudaMalloc(&chain_trace_ptr(), 2 * kChainTraceWords * sizeof(long long)));
   auto* t = new TcModel();
   t->mode = mode;
   t->chain = c.n_conv == 3 && c.conv[0] == 64 && c.conv[1] == 64 && c.conv[2] == 64 && c.input_channels == 50 &&
@@ -634,10 +678,20 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.ldo = c.fc_hidden;
     p.out_bf16 = 0;
     p.out_split_stride = plane;
-    p.trace = chain_trace_ptr();
+    p.trace = chain_trace_active();
     if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
-    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, p, t.fc1.npad / fc_tile, nsplit, s);
+    // partial planes as a 3-D tensor [nsplit][samples][hidden]: the TMA store
+    // clips rows past `samples` within each plane
+    const uint64_t odims[3] = {static_cast<uint64_t>(c.fc_hidden), samples, static_cast<uint64_t>(nsplit)};
+    const uint64_t ostr[2] = {static_cast<uint64_t>(c.fc_hidden) * 4, plane * 4};
+    const uint32_t obox[3] = {32, 32, 1};
+    const CUtensorMap omap = make_map(part, false, 3, odims, ostr, obox);
+    const size_t ring = static_cast<size_t>(p.stages) * kAChunk * (mode == kTF32x3 ? 2 : 1);
+    // each solo half must be whole 32-column groups
+    p.tma_out = fc_tile % 64 == 0 && ring >= static_cast<size_t>(fc_tile / 32) * kAChunk &&
+                !std::getenv("SIMNET_FC1_DIRECT_STORE");
+    launch_mode(mode, amap, t.fc1.map_hi, t.fc1.map_lo, omap, p, t.fc1.npad / fc_tile, nsplit, s);
     ++launches;
     if (!with_tail) return launches;  // the fused round front reduces the partials next round
     TailParams tp{};
@@ -709,7 +763,7 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   fp.out = fb.act[2];
   const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
                             t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
-  fp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
+  fp.trace = chain_trace_active();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
   if (!fp.calibrate) fp.c1acc = t.c1acc.as<float>();
   launch_round_front(t.mode, w, fp, num_sms(), s);
   return 1;
@@ -744,7 +798,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
                               t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
     ChainParams cp{static_cast<int>(samples), P + m.L.b[0], P + m.L.b[1], P + m.L.b[2], fb.act[2], nullptr};
-    cp.trace = chain_trace_ptr();  // SIMNET_CHAIN_TRACE diagnostics (null: off)
+    cp.trace = chain_trace_active();  // SIMNET_CHAIN_TRACE diagnostics (null: off)
     launch_conv_chain(mode, xmap, xlo, w, cp, num_sms(), s);
     ++launches;
     in = fb.act[2];
@@ -783,7 +837,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     p.out = fb.act[l];
     p.ldo = cout;
     p.out_bf16 = bf;
-    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, p, cout / bn, 1, s);
+    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, amap, p, cout / bn, 1, s);  // no TMA store
     ++launches;
     in = fb.act[l];
     cin = cout;

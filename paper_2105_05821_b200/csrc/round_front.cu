@@ -239,6 +239,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   // PDL: the FC kernels may launch now (their prologue only touches weights);
   // this kernel's prologue (barriers, TMEM, biases, W0) overlaps the previous
   // round's tail, and only the compute warps wait for its results.
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 30] = global_ns();  // diagnostics: CTA entry
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x < 3 * kC) {
     const int l = threadIdx.x / kC, c = threadIdx.x % kC;
@@ -276,6 +277,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
                  "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (p.trace && lane == 0) p.trace[blockIdx.x * 32 + 29] = global_ns();  // diagnostics: TMEM allocated
   }
   tc_fence_before();
   __syncthreads();
@@ -679,6 +681,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   if (warp == 9) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    if (p.trace && lane == 0) p.trace[blockIdx.x * 32 + 31] = global_ns();  // diagnostics: about to exit
   }
 }
 

@@ -349,6 +349,25 @@ def test_fused_front_inputs_bit_exact(gpu, port, golden, precision, geom):
 
 
 @pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_fc1_tma_store_matches_direct_store(gpu, port, golden, precision, monkeypatch):
+    """FC1's split-K partials staged in shared memory and TMA-stored (CTAs that
+    own one M tile) equal the per-thread direct stores bit for bit, including a
+    partial last M tile (rows clipped by the tensor map)."""
+    g = gpu(precision)
+    m, _ = _fused_cases(port, golden)
+    g.load_model(m)
+    t = read_trace(GOLD / "branchy_2000_s8.trace")
+    for k in (130, 300):
+        pc = pcfg(k)
+        g.load_trace(t, pc)
+        monkeypatch.delenv("SIMNET_FC1_DIRECT_STORE", raising=False)
+        a = g.run(pc)
+        monkeypatch.setenv("SIMNET_FC1_DIRECT_STORE", "1")
+        b = g.run(pc)
+        assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch), k
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
 def test_chunked_rounds_match(gpu, port, golden, precision, monkeypatch):
     """Batches larger than one chunk (65536 sub-traces in production; 24 here)
     run chunk after chunk each round; results must not change."""

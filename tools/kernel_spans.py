@@ -19,8 +19,11 @@ for prec in ("tf32x3", "bf16"):
     pc = ParallelConfig(k=1024)
     g.load_trace(t, pc)
     r = g.run(pc)
-    buf = np.zeros(148 * 32 + 256 * 16, np.int64)
-    _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
+    W = 148 * 32 + 256 * 16
+    buf2 = np.zeros(2 * W, np.int64)
+    _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf2.ctypes.data), C.c_int(buf2.size))
+    buf = buf2[:W]
+    nfr = buf2[W:W + 148 * 32].reshape(148, 32)[:128]  # the next round's front
     fr = buf[:148 * 32].reshape(148, 32)[:128]
     f1 = buf[148 * 32:].reshape(256, 16)[:128]
     fs, fe = fr[:, 13].min(), fr[:, 14].max()
@@ -37,5 +40,21 @@ for prec in ("tf32x3", "bf16"):
     cyc1 = (f1[:, 4] - f1[:, 0]).astype(np.float64)
     ns1 = (f1[:, 9] - f1[:, 8]).astype(np.float64)
     print(f"   fc1 per-CTA: clock64 {np.median(cyc1):.0f} cyc vs globaltimer {np.median(ns1):.0f} ns")
+    dw = f1[:, 12]
+    print(f"   timeline (ns from first front CTA start): front CTA ends median {np.median(fr[:, 14]) - fs:.0f} "
+          f"max {fe - fs:.0f} | fc1 dependency-wait exits min {dw.min() - fs:.0f} median {np.median(dw) - fs:.0f} | "
+          f"fc1 CTA ends median {np.median(f1[:, 9]) - fs:.0f} max {ce - fs:.0f} | next round starts ~{1000 * per_round:.0f}")
+    q = lambda a: " ".join(f"{v:.0f}" for v in np.percentile(a, [0, 10, 25, 50, 75, 90, 100]))
+    print(f"   front CTA entries                             : {q(fr[:, 30] - fs)}")
+    print(f"   front TMEM allocated                          : {q(fr[:, 29] - fs)}")
+    print(f"   front CTA starts (ns, pct 0/10/25/50/75/90/100): {q(fr[:, 13] - fs)}")
+    print(f"   front CTA ends                                : {q(fr[:, 14] - fs)}")
+    print(f"   fc1 CTA starts                                : {q(f1[:, 8] - fs)}")
+    print(f"   fc1 dependency-wait exits                     : {q(f1[:, 12] - fs)}")
+    print(f"   fc1 CTA ends                                  : {q(f1[:, 9] - fs)}")
+    print(f"   fc1 after TMEM dealloc                        : {q(f1[:, 13] - fs)}")
+    print(f"   front after TMEM dealloc                      : {q(fr[:, 31] - fs)}")
+    print(f"   next front CTA entries                        : {q(nfr[:, 30] - fs)}")
+    print(f"   next front CTA starts                         : {q(nfr[:, 13] - fs)}")
     print(f"   fc1 start->tile0 epilogue: globaltimer {np.median(f1[:, 10] - f1[:, 8]):.0f} ns, clock64 "
           f"{np.median(f1[:, 4] - f1[:, 0]):.0f} cyc; end-start {np.median(f1[:, 9] - f1[:, 8]):.0f} ns")
