@@ -761,8 +761,18 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   fp.b1 = P + m.L.b[1];
   fp.b2 = P + m.L.b[2];
   fp.out = fb.act[2];
-  const CUtensorMap w[6] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
-                            t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo};
+  CUtensorMap w[7] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
+                      t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo, t.conv[0].map_hi};
+  const uint64_t samples = fp.last - fp.first;
+  fp.out_tma = 0;
+  if (t.mode != kBF16 && samples > 0 && !std::getenv("SIMNET_FLAT_DIRECT_STORE")) {
+    // flat as [samples * 16 rows][64 f32]: the front TMA-stores 32 x 32 boxes
+    const uint64_t dims[2] = {64, samples * 16};
+    const uint64_t strides[1] = {64 * 4};
+    const uint32_t box[2] = {32, 32};
+    w[6] = make_map(fb.act[2], false, 2, dims, strides, box);
+    fp.out_tma = 1;
+  }
   fp.trace = chain_trace_active();  // SIMNET_CHAIN_TRACE: event clocks of the last launch (null: off)
   if (!fp.calibrate) fp.c1acc = t.c1acc.as<float>();
   launch_round_front(t.mode, w, fp, num_sms(), s);

@@ -47,6 +47,7 @@ constexpr int kTblCols = 128; // max columns (max_context + 1)
 constexpr uint32_t kR1 = 128 * 1024;
 constexpr uint32_t kR2 = 64 * 1024;
 constexpr uint32_t kTbl = kItem * kTblCols * (4 + 16);
+constexpr uint32_t kOutStage = 96 * 1024;  // flat staging in R1 (2 x 16 KB)
 constexpr int kThreadsRF = 320;
 constexpr int kCompute = 256;
 
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kThreadsRF, 1)
 round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW0lo,
                    const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW1lo,
                    const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW2lo,
-                   FrontParams p) {
+                   const __grid_constant__ CUtensorMap tmOut, FrontParams p) {
   using S = Shape<kMode>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* R1 = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
@@ -645,7 +646,30 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       tc_fence_after();
       mark(11);
       const uint64_t sample = static_cast<uint64_t>(item) * kItem + (m >> 4);
-      for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
+      const bool out_tma = kMode != kBF16 && p.out_tma;
+      if (out_tma) {
+        // stage the 32 columns of row m in R1 (idle after conv2: the next item's
+        // W2 lands below 64 KB) as 128 rows x 128 B per column half, SWIZZLE_128B;
+        // each warp TMA-stores its 32 x 32 box, rows past the batch clipped
+        uint8_t* stg = R1 + kOutStage + half * S::kStage;
+        float v[32];
+        tmem_ld16(tmem + lane_off + 384 + half * 32, v);
+        tmem_ld16(tmem + lane_off + 384 + half * 32 + 16, v + 16);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + m * 128 + ((q ^ (m & 7)) << 4)) =
+              make_float4(fmaxf(v[4 * q] + sbias[2][half * 32 + 4 * q], 0.0f),
+                          fmaxf(v[4 * q + 1] + sbias[2][half * 32 + 4 * q + 1], 0.0f),
+                          fmaxf(v[4 * q + 2] + sbias[2][half * 32 + 4 * q + 2], 0.0f),
+                          fmaxf(v[4 * q + 3] + sbias[2][half * 32 + 4 * q + 3], 0.0f));
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, stg + quad * 32 * 128, half * 32, item * (kItem * 16) + quad * 32);
+          bulk_commit();
+        }
+      }
+      for (int c0 = half * 32; c0 < half * 32 + 32 && !out_tma; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + lane_off + 384 + c0, v);
 #pragma unroll
@@ -671,10 +695,12 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         }
       }
       tc_fence_before();
+      if (out_tma && lane == 0) bulk_wait_read();  // staging is read: R1 reusable
       compute_sync();  // TMEM conv2 columns and the tables are free for the next item
       mark(12);
     }
   }
+  if (kMode != kBF16 && p.out_tma && warp < 8 && lane == 0) bulk_wait_all();  // flat stores complete
   tc_fence_before();
   __syncthreads();
   if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 32 + 14] = global_ns();
@@ -735,11 +761,11 @@ void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, in
   const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
   const size_t sm = front_smem_bytes();
   if (mode == kBF16)
-    launch_pdl_tag("front", round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    launch_pdl_tag("front", round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], p);
   else if (mode == kTF32)
-    launch_pdl_tag("front", round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    launch_pdl_tag("front", round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], p);
   else
-    launch_pdl_tag("front", round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], p);
+    launch_pdl_tag("front", round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], p);
 }
 
 void round_front_set_attributes() {

@@ -31,6 +31,7 @@ struct FrontParams {
   const float* b1;
   const float* b2;
   void* out;                 // flat [last-first][1024] (f32, or bf16 for the bf16 path)
+  int32_t out_tma;           // f32 flat: staged in shared memory and TMA-stored through w[6]
   // optional: write the gathered input (exact f32 values) in the standard
   // row layout [last-first][dump_stride] (rows of 100 floats) — input capture
   float* dump;
@@ -47,8 +48,8 @@ struct FrontParams {
   long long* trace;          // optional: per-CTA event clocks of the first item (diagnostics)
 };
 
-// w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
-// w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows)
+// w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows),
+//    w[6]: flat viewed as [(last-first)*16 rows][64 f32], box 32 x 32, SWIZZLE_128B (p.out_tma)
 void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s);
 void round_front_set_attributes();
 // After the last round: decode the outstanding predictions, apply them and

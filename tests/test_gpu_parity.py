@@ -350,9 +350,9 @@ def test_fused_front_inputs_bit_exact(gpu, port, golden, precision, geom):
 
 @pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
 def test_fc1_tma_store_matches_direct_store(gpu, port, golden, precision, monkeypatch):
-    """FC1's split-K partials staged in shared memory and TMA-stored (CTAs that
-    own one M tile) equal the per-thread direct stores bit for bit, including a
-    partial last M tile (rows clipped by the tensor map)."""
+    """FC1's split-K partials and the front's flat output, staged in shared
+    memory and TMA-stored, equal the per-thread direct stores bit for bit,
+    including a partial last M tile / item (rows clipped by the tensor map)."""
     g = gpu(precision)
     m, _ = _fused_cases(port, golden)
     g.load_model(m)
@@ -360,9 +360,11 @@ def test_fc1_tma_store_matches_direct_store(gpu, port, golden, precision, monkey
     for k in (130, 300):
         pc = pcfg(k)
         g.load_trace(t, pc)
-        monkeypatch.delenv("SIMNET_FC1_DIRECT_STORE", raising=False)
+        for v in ("SIMNET_FC1_DIRECT_STORE", "SIMNET_FLAT_DIRECT_STORE"):
+            monkeypatch.delenv(v, raising=False)
         a = g.run(pc)
-        monkeypatch.setenv("SIMNET_FC1_DIRECT_STORE", "1")
+        for v in ("SIMNET_FC1_DIRECT_STORE", "SIMNET_FLAT_DIRECT_STORE"):
+            monkeypatch.setenv(v, "1")
         b = g.run(pc)
         assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch), k
 
