@@ -240,7 +240,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t d = tmem + acc * p.n;
         for (int c = 0; c < p.chunks; ++c) {
           mbar_wait(kSplit ? &bar_split[stage] : &bar_full[stage], phase);
-          if (tr && it == 0 && c == 0) tr[2] = clock64();
+          if (tr && it == 0 && c < 4) tr[c == 0 ? 2 : 4 + c] = clock64();  // chunk c ready (5, 6, 7: chunks 1-3)
           tc_fence_after();
           const int steps = c == p.chunks - 1 ? p.ksteps_last : 4;
           for (int j = 0; j < steps; ++j) {
@@ -263,7 +263,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
         }
         mma_commit(&bar_acc_full[acc]);
-        if (tr && it < 2) tr[3 + 2 * it] = clock64();
+        if (tr && it < 1) tr[3] = clock64();
       }
     }
     __syncwarp();
@@ -322,15 +322,16 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int acc = it & 1;
       mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
       tc_fence_after();
+      if (tr && warp == 6 && lane == 0 && it == 0) tr[14] = clock64();  // accumulator complete
       if (tma_out)
         epilogue_tma(t, 0, p.n / 2);
       else
         epilogue(t, acc, 0, solo ? p.n / 2 : p.n);
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
-      if (tr && warp == 6 && lane == 0 && it < 2) {
-        tr[4 + 2 * it] = clock64();
-        tr[10 + it] = global_ns();
+      if (tr && warp == 6 && lane == 0 && it < 1) {
+        tr[4] = clock64();
+        tr[10] = global_ns();
       }
     }
   }

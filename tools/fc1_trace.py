@@ -21,13 +21,14 @@ for prec in ("tf32x3", "bf16"):
     g.run(pc)
     buf = np.zeros(148 * 32 + 256 * 16, np.int64)
     _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
-    tr = buf[148 * 32:].reshape(256, 16)[:144].astype(np.float64)
-    rel = tr[:, :8] - tr[:, :1]
-    names = ["start", "W landed", "A chunk0 ready", "tile0 MMAs issued", "tile0 epilogue done", "tile1 MMAs issued",
-             "tile1 epilogue done", "end (globaltimer ns)"]
-    tr[:, 7] = (tr[:, 9] - tr[:, 8]) * 1.87 + tr[:, 0]  # end, converted to cycles at ~1.87 cyc/ns
+    tr = buf[148 * 32:].reshape(256, 16)[:128].astype(np.float64)
+    rel = tr - tr[:, :1]
+    names = {0: "start", 1: "W landed", 2: "A chunk0 ready", 5: "A chunk1 ready", 6: "A chunk2 ready",
+             7: "A chunk3 ready", 3: "tile0 MMAs issued", 14: "accumulator done", 4: "tile0 epilogue done"}
     print(prec)
-    for i, n in enumerate(names):
+    dw = (tr[:, 12] - tr[:, 8]) * 1.87
+    print(f"  dependency wait exit median {np.median(dw):8.0f} cyc (globaltimer x 1.87)")
+    for i, n in names.items():
         col = rel[:, i][tr[:, i] > 0]
         if col.size:
             print(f"  {n:20s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
