@@ -33,7 +33,8 @@ inline bool& chain_trace_on() {
   return on;
 }
 // Two consecutive rounds are traced into slots 0 and 1 (kChainTraceWords each).
-constexpr int kChainTraceWords = 148 * 32 + 256 * 16;
+constexpr int kChainTraceFrontX = 148 * 32 + 256 * 32;  // front extras: 16 words per CTA
+constexpr int kChainTraceWords = kChainTraceFrontX + 148 * 16;
 inline int& chain_trace_slot() {
   static int slot = 0;
   return slot;

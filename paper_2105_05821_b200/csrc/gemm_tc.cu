@@ -120,8 +120,9 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const uint32_t tmem = tmem_slot;
   const int elems = kMode == kBF16 ? 64 : 32;  // elements per 128 B chunk
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  long long* tr = p.trace ? p.trace + 148 * 32 + cta * 16 : nullptr;
+  long long* tr = p.trace ? p.trace + 148 * 32 + cta * 32 : nullptr;  // 32 words per CTA
   if (tr && threadIdx.x == 0) {
+    tr[15] = 0;
     tr[0] = clock64();
     tr[8] = global_ns();
   }
@@ -142,23 +143,29 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    const bool stamp = tr && warp == 6 && lane == 0;
     for (int c0 = cb; c0 < ce; c0 += 32) {
       float v[32];
       tmem_ld16(tl + c0, v);
       tmem_ld16(tl + c0 + 16, v + 16);
+      if (stamp && c0 == cb) tr[16] = clock64();  // first TMEM columns in registers
       uint8_t* stg = sA + (c0 >> 5) * kAChunk + r * 128;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         *reinterpret_cast<float4*>(stg + ((q ^ (r & 7)) << 4)) =
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
+    if (stamp) tr[17] = clock64();  // staged
     fence_async_smem();
     __syncwarp();
+    if (stamp) tr[18] = clock64();  // fenced
     if (lane == 0) {
       for (int c0 = cb; c0 < ce; c0 += 32)
         tma_store_3d(&tmOut, sA + (c0 >> 5) * kAChunk + quad * 32 * 128, ntile * p.n + c0, t * kBM + quad * 32, ks);
       bulk_commit();
-      bulk_wait_all();  // complete before the CTA exits
+      if (stamp) tr[19] = clock64();  // stores issued
+      bulk_wait_read();  // staging read; the stores complete with the grid (dependents wait for it)
+      if (stamp) tr[20] = clock64();  // staging read back
     }
   };
   auto epilogue = [&](int t, int acc, int cb, int ce) {
@@ -243,6 +250,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (tr && it == 0 && c < 4) tr[c == 0 ? 2 : 4 + c] = clock64();  // chunk c ready (5, 6, 7: chunks 1-3)
           tc_fence_after();
           const int steps = c == p.chunks - 1 ? p.ksteps_last : 4;
+          const long long t_issue = tr ? clock64() : 0;
           for (int j = 0; j < steps; ++j) {
             const uint32_t aoff = stage * kAChunk + j * 32, boff = c * bBytes + j * 32;
             const uint64_t ad = smem_desc_sw128(su32(sA) + aoff);
@@ -257,6 +265,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
           }
           mma_commit(&bar_empty[stage]);  // the stage is free once these MMAs retire
+          if (tr && it == 0) tr[15] += clock64() - t_issue;  // diagnostics: cycles spent issuing
           if (++stage == ns) {
             stage = 0;
             phase ^= 1;

@@ -31,6 +31,7 @@
 
 #include <cstdlib>
 
+#include "conv_chain.cuh"
 #include "k1_device.cuh"
 #include "launch.cuh"
 #include "round_front.cuh"
@@ -428,6 +429,11 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     uint32_t n_t0 = 0, n_m1 = 0;
     int it = 0;
     long long* tr = p.trace ? p.trace + blockIdx.x * 32 : nullptr;
+    // extra per-warp-0 stamps of the first item (no barrier: warp 0's own progress)
+    long long* tx = p.trace ? p.trace + kChainTraceFrontX + blockIdx.x * 16 : nullptr;
+    auto stampx = [&](int i) {
+      if (tx && it == 0 && tid == 0) tx[i] = clock64();
+    };
     // diagnostics: phase-boundary clocks of the first item, taken after a
     // barrier of the compute warps so a mark means "all of them are done"
     auto mark = [&](int i) {
@@ -481,7 +487,9 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           if (st.status == kOk && st.pos < st.len) {
             const uint64_t tgt = st.begin + st.pos;
             const uint32_t ncols = min(static_cast<uint32_t>(p.max_context), (st.pt - st.ph) + (st.wt - st.wh));
+            stampx(5);
             mbar_wait(&bar_tg, it & 1);
+            stampx(6);
             const bool pre = s_tidx[warp] == tgt;  // the producer's prediction of this round's target
             const uint64_t tpc = pre ? s_tpc[warp] : p.pc[tgt];
             const uint64_t taddr = pre ? s_taddr[warp] : p.addr[tgt];
@@ -502,6 +510,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
               td[c] = make_float4(norm_slot(res, nc.mean[kSlotResidence], nc.sd[kSlotResidence]), e.nexec, e.nstore,
                                   __uint_as_float(f));
             }
+            stampx(7);
             if (lane == 0) {  // the next round's push carries these into the ring entry
               sp->awaiting = 1;
               sp->xcols = ncols + 1;
@@ -528,6 +537,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       // Thread = (sample `warp`, column 32t + lane): one A half-row (50 slots of
       // one context column) per thread per tile: 11 float4 static-slot loads in
       // flight, the 9 dynamic slots from the column table, 16-B stores.
+      const long long t_gather0 = tx ? clock64() : 0;
+      if (tx && it == 0 && tid == 0) tx[10] = t_gather0;
       for (int t = 0; t < T; ++t) {
         // lane -> (position q of the tile, K half h); row slot: even positions
         // in slots 0-7, odd in 8-15 (see row_slot_c0 below)
@@ -537,23 +548,23 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         const bool live = col <= s_ncols[warp];
         float v[kSlots];
         {
-          float4 q[11];
-          const float4* srow = reinterpret_cast<const float4*>(
-              p.stat + static_cast<uint64_t>(live ? tbl_inst[warp * kTblCols + col] : 0u) * kStatStride);
+          // the row's 41 static slots: six 32-B loads (one L2 sector each; rows
+          // are 192 B, sector aligned) instead of eleven 16-B ones
+          const float* srow =
+              p.stat + static_cast<uint64_t>(live ? tbl_inst[warp * kTblCols + col] : 0u) * kStatStride;
+          float w[48];
 #pragma unroll
-          for (int i = 0; i < 11; ++i) q[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          for (int i = 0; i < 48; ++i) w[i] = 0.0f;
           if (live) {
 #pragma unroll
-            for (int i = 0; i < 11; ++i) q[i] = __ldg(srow + i);
+            for (int i = 0; i < 6; ++i)
+              asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                           : "=f"(w[8 * i]), "=f"(w[8 * i + 1]), "=f"(w[8 * i + 2]), "=f"(w[8 * i + 3]),
+                             "=f"(w[8 * i + 4]), "=f"(w[8 * i + 5]), "=f"(w[8 * i + 6]), "=f"(w[8 * i + 7])
+                           : "l"(srow + 8 * i));
           }
 #pragma unroll
-          for (int i = 0; i < 10; ++i) {
-            v[4 * i] = q[i].x;
-            v[4 * i + 1] = q[i].y;
-            v[4 * i + 2] = q[i].z;
-            v[4 * i + 3] = q[i].w;
-          }
-          v[40] = q[10].x;
+          for (int i = 0; i <= 40; ++i) v[i] = w[i];
           const float4 d = tbl_dyn[warp * kTblCols + (live ? col : 0)];
           const uint32_t f = __float_as_uint(d.w);
           v[kSlotResidence] = d.x;
@@ -568,9 +579,27 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
             for (int k = 0; k < kSlots; ++k) v[k] = 0.0f;
           }
         }
+        if (tx && it == 0) {  // diagnostics: force the loads before the stamp
+          float sum = 0.0f;
+#pragma unroll
+          for (int k = 0; k < kSlots; ++k) sum += v[k];
+          if (sum == 12345.0f) tx[15] = 1;
+          stampx(t == 0 ? 0 : 2);
+          if (t == 0 && warp == 0) {  // per-lane completion spread of warp 0 (vs tx[10])
+            const uint32_t now = static_cast<uint32_t>(clock64() - t_gather0);
+            const uint32_t mn = __reduce_min_sync(0xffffffffu, now), mx = __reduce_max_sync(0xffffffffu, now);
+            const uint32_t l1 = __shfl_sync(0xffffffffu, now, 2);
+            if (lane == 0) {
+              tx[8] = t_gather0 + mn;
+              tx[9] = t_gather0 + mx;
+              tx[11] = t_gather0 + l1;
+            }
+          }
+        }
         // loads and values above overlap the previous tile's MMAs; only the
         // operand writes wait for them to finish reading R1
         if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);
+        if (t == 1) stampx(3);
         if (h == 0) {  // K 0..49
 #pragma unroll
           for (int i = 0; i < 12; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -592,6 +621,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
             for (int k = 0; k < kSlots; k += 2) *reinterpret_cast<float2*>(o + k) = make_float2(v[k], v[k + 1]);
           }
         }
+        stampx(t == 0 ? 1 : 4);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&bar_a0);
         mark(2 + t);

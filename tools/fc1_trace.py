@@ -19,14 +19,16 @@ for prec in ("tf32x3", "bf16"):
     pc = ParallelConfig(k=K)
     g.load_trace(t, pc)
     g.run(pc)
-    buf = np.zeros(148 * 32 + 256 * 16, np.int64)
+    buf = np.zeros(148 * 32 + 256 * 32, np.int64)
     _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
-    tr = buf[148 * 32:].reshape(256, 16)[:128].astype(np.float64)
+    tr = buf[148 * 32:].reshape(256, 32)[:128].astype(np.float64)
     rel = tr - tr[:, :1]
     names = {0: "start", 1: "W landed", 2: "A chunk0 ready", 5: "A chunk1 ready", 6: "A chunk2 ready",
-             7: "A chunk3 ready", 3: "tile0 MMAs issued", 14: "accumulator done", 4: "tile0 epilogue done"}
+             7: "A chunk3 ready", 3: "tile0 MMAs issued", 14: "accumulator done", 16: "epi: tmem ld", 17: "epi: staged",
+             18: "epi: fenced", 19: "epi: TMA issued", 20: "epi: staging read", 4: "tile0 epilogue done"}
     print(prec)
     dw = (tr[:, 12] - tr[:, 8]) * 1.87
+    print(f"  MMA issue total      median {np.median(tr[:, 15]):8.0f} cyc")
     print(f"  dependency wait exit median {np.median(dw):8.0f} cyc (globaltimer x 1.87)")
     for i, n in names.items():
         col = rel[:, i][tr[:, i] > 0]

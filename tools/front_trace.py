@@ -8,8 +8,11 @@ N = int(os.environ.get("N", "300000")); t = synthetic_trace(N, 101); m = synthet
 for prec in ("tf32x3", "bf16"):
     g = GpuSimulator(0, prec); g.load_model(m)
     pc = ParallelConfig(k=1024); g.load_trace(t, pc); g.run(pc)
-    buf = np.zeros(148 * 32, np.int64)
-    _lib.lib().simnet_debug_chain_trace(C.c_void_p(buf.ctypes.data))
+    W = 148 * 32 + 256 * 32 + 148 * 16
+    full = np.zeros(W, np.int64)
+    _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(full.ctypes.data), C.c_int(W))
+    buf = full[:148 * 32]
+    tx = full[148 * 32 + 256 * 32:].reshape(148, 16)[:128].astype(np.float64)
     tr = buf.reshape(148, 32)[:128].astype(np.float64)
     T = tr[:, 20]
     base = tr[:, :1]
@@ -26,3 +29,9 @@ for prec in ("tf32x3", "bf16"):
     for i in (0, 15, 16, 1, 2, 3, 6, 7, 8, 9, 10, 11, 12, 21, 22, 23, 31):
         col = (tr[:, i] - base[:, 0])[tr[:, i] > 0]
         if col.size: print(f"  {names[i]:18s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")
+    for i, n in ((5, "w0 table: before tg wait"), (6, "w0 table: tg ready"), (7, "w0 table: loop done"),
+                 (10, "w0 gather start"), (8, "w0 tile0 loads first lane"), (11, "w0 tile0 loads lane 2"),
+                 (9, "w0 tile0 loads last lane"), (0, "w0 tile0 loads done"), (1, "w0 tile0 stores done"), (2, "w0 tile1 loads done"),
+                 (3, "w0 tile1 t0 wait done"), (4, "w0 tile1 stores done")):
+        col = (tx[:, i] - base[:, 0])[tx[:, i] > 0]
+        if col.size: print(f"  {n:24s} median {np.median(col):8.0f} cyc   max {col.max():8.0f}")

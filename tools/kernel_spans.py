@@ -19,13 +19,13 @@ for prec in ("tf32x3", "bf16"):
     pc = ParallelConfig(k=1024)
     g.load_trace(t, pc)
     r = g.run(pc)
-    W = 148 * 32 + 256 * 16
+    W = 148 * 32 + 256 * 32
     buf2 = np.zeros(2 * W, np.int64)
     _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf2.ctypes.data), C.c_int(buf2.size))
     buf = buf2[:W]
     nfr = buf2[W:W + 148 * 32].reshape(148, 32)[:128]  # the next round's front
     fr = buf[:148 * 32].reshape(148, 32)[:128]
-    f1 = buf[148 * 32:].reshape(256, 16)[:128]
+    f1 = buf[148 * 32:].reshape(256, 32)[:128]
     fs, fe = fr[:, 13].min(), fr[:, 14].max()
     cs, ce = f1[:, 8].min(), f1[:, 9].max()
     per_round = 1000 * r.device_ms / r.rounds
