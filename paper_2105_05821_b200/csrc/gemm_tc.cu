@@ -65,11 +65,13 @@ struct TcGemmParams {
   uint64_t out_split_stride;  // elements between split-K partial planes
   long long* trace;           // diagnostics (SIMNET_CHAIN_TRACE): per-CTA event clocks, 16 per CTA
   int stages;                 // A ring depth (2..kStages; 0 = kStages)
+  int a_tmem;                 // 3xTF32: the split warps write A hi / lo into tensor memory (4-slot ring
+                              // next to the accumulators) and the MMAs read A from there (SMEM: W only)
   int tma_out;                // f32 split-K partials through tmOut: CTAs owning one M tile stage the
                               // accumulator in the idle A ring and TMA-store it (coalesced, async)
 };
 
-template <int kMode>
+template <int kMode, bool kAInTmem = false>
 __global__ void __launch_bounds__(kLayerThreads, 1)
 tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmOut,
@@ -87,12 +89,16 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   __shared__ __align__(8) uint64_t bar_w;
   __shared__ __align__(8) uint64_t bar_full[kStages], bar_split[kStages], bar_empty[kStages];
   __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
+  __shared__ __align__(8) uint64_t bar_sfree[kStages], bar_tfree[4];  // a_tmem: SMEM stage read / TMEM A slot free
   __shared__ uint32_t tmem_slot;
+  constexpr bool a_tmem = kSplit && kAInTmem;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntile = blockIdx.y, ks = blockIdx.z;
   const int kc0 = ks * p.chunks;  // first K chunk of this split
-  const uint32_t tcols = 2 * p.n <= 32 ? 32u : (2 * p.n <= 64 ? 64u : (2 * p.n <= 128 ? 128u : 256u));
+  const uint32_t tcols =
+      a_tmem ? 512u : (2 * p.n <= 32 ? 32u : (2 * p.n <= 64 ? 64u : (2 * p.n <= 128 ? 128u : 256u)));
+  constexpr uint32_t kATmem = 256;  // a_tmem: A ring columns [256, 512): slot g % 4 = hi 32 | lo 32
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_w, 1);
@@ -100,7 +106,9 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(&bar_full[i], 1);
       mbar_init(&bar_split[i], 128);
       mbar_init(&bar_empty[i], 1);
+      mbar_init(&bar_sfree[i], 128);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&bar_tfree[i], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_acc_full[i], 1);
       mbar_init(&bar_acc_empty[i], 128);
@@ -217,7 +225,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
         for (int c = 0; c < p.chunks; ++c) {
-          mbar_wait(&bar_empty[stage], phase ^ 1);
+          mbar_wait(a_tmem ? &bar_sfree[stage] : &bar_empty[stage], phase ^ 1);
           mbar_expect_tx(&bar_full[stage], kAChunk);
           const int kx = (kc0 + c) * elems;
           if (p.a3d)
@@ -239,6 +247,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      uint32_t g = 0;  // chunk counter (a_tmem: TMEM slot g % 4)
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
@@ -251,7 +260,19 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           tc_fence_after();
           const int steps = c == p.chunks - 1 ? p.ksteps_last : 4;
           const long long t_issue = tr ? clock64() : 0;
-          for (int j = 0; j < steps; ++j) {
+          if constexpr (a_tmem) {  // A hi / lo in TMEM slot g % 4 (columns: hi 32 | lo 32), W from SMEM
+            const uint32_t slot = tmem + kATmem + (g & 3u) * 64u;
+            for (int j = 0; j < steps; ++j) {
+              const uint32_t boff = c * bBytes + j * 32;
+              const uint64_t bd = smem_desc_sw128(su32(sW) + boff);
+              const uint32_t first = (c == 0 && j == 0) ? 0u : 1u;
+              mma_ts<kMode>(d, slot + 32 + j * 8, bd, idesc, first);  // small terms first
+              mma_ts<kMode>(d, slot + j * 8, smem_desc_sw128(su32(sWlo) + boff), idesc, 1);
+              mma_ts<kMode>(d, slot + j * 8, bd, idesc, 1);
+            }
+            mma_commit(&bar_tfree[g & 3u]);  // the TMEM slot is free once these MMAs retire
+          }
+          for (int j = 0; j < steps && !a_tmem; ++j) {
             const uint32_t aoff = stage * kAChunk + j * 32, boff = c * bBytes + j * 32;
             const uint64_t ad = smem_desc_sw128(su32(sA) + aoff);
             const uint64_t bd = smem_desc_sw128(su32(sW) + boff);
@@ -264,7 +285,8 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               mma<kMode>(d, ad, bd, idesc, first);
             }
           }
-          mma_commit(&bar_empty[stage]);  // the stage is free once these MMAs retire
+          if (!a_tmem) mma_commit(&bar_empty[stage]);  // the stage is free once these MMAs retire
+          ++g;
           if (tr && it == 0) tr[15] += clock64() - t_issue;  // diagnostics: cycles spent issuing
           if (++stage == ns) {
             stage = 0;
@@ -277,7 +299,45 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     __syncwarp();
   } else if (warp < 6) {
-    if (kSplit) {  // hi/lo split of each landed A chunk
+    if constexpr (a_tmem) {  // hi / lo split of each landed A chunk straight into TMEM: thread = A row
+      const int quad = warp & 3;
+      const int r = quad * 32 + lane;
+      const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
+        for (int c = 0; c < p.chunks; ++c, ++g) {
+          mbar_wait(&bar_full[stage], phase);
+          if (g >= 4) mbar_wait(&bar_tfree[g & 3u], ((g >> 2) - 1) & 1u);  // chunk g-4's MMAs done
+          tc_fence_after();
+          const uint8_t* row = sA + stage * kAChunk + r * 128;
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4 u = *reinterpret_cast<const uint4*>(row + ((q ^ (r & 7)) << 4));
+            const uint32_t x[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              // hi = x rounded to tf32 (cvt.rna); lo = x - hi, exact in fp32, read at tf32
+              hi[4 * q + e] = (x[e] + 0x1000u) & 0xffffe000u;
+              lo[4 * q + e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(hi[4 * q + e]));
+            }
+          }
+          const uint32_t slot = tmem + lane_off + kATmem + (g & 3u) * 64u;
+          tmem_st32(slot, hi);
+          tmem_st32(slot + 32, lo);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bar_sfree[stage]);  // SMEM stage read
+          mbar_arrive(&bar_split[stage]);  // TMEM slot written
+          if (++stage == ns) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    } else if (kSplit) {  // hi/lo split of each landed A chunk
       const int t128 = threadIdx.x - 64;
       int stage = 0;
       uint32_t phase = 0;
@@ -522,9 +582,10 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
 }
 
-size_t smem_bytes(int mode, int n, int chunks, int stages) {
+size_t smem_bytes(int mode, int n, int chunks, int stages, bool a_tmem = false) {
   const size_t w = static_cast<size_t>(chunks) * n * 128 * (mode == kTF32x3 ? 2 : 1);
-  const size_t a = static_cast<size_t>(stages > 0 ? stages : kStages) * kAChunk * (mode == kTF32x3 ? 2 : 1);
+  const size_t a =
+      static_cast<size_t>(stages > 0 ? stages : kStages) * kAChunk * (mode == kTF32x3 && !a_tmem ? 2 : 1);
   return w + a + 1024;
 }
 
@@ -544,11 +605,13 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   const int groups = ny * nz;
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
-  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages);
+  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0);
   if (mode == kBF16)
     launch_pdl_tag("layer_bf16", tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
   else if (mode == kTF32)
     launch_pdl_tag("layer", tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
+  else if (p.a_tmem)
+    launch_pdl_tag("layer", tc_layer_kernel<kTF32x3, true>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
   else
     launch_pdl_tag("layer", tc_layer_kernel<kTF32x3>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
 }
@@ -574,6 +637,8 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(fc_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   conv_chain_set_attributes();
   round_front_set_attributes();
@@ -680,8 +745,14 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.chunks = per;
     p.ksteps_last = 4;
     // A ring depth that fits next to the resident W slice (226 KB dynamic smem)
+    // A in TMEM pays off when CTAs loop over several M tiles (the split runs a
+    // chunk ahead of the MMAs); with one tile per CTA the split sits on the
+    // critical path and A from shared memory is faster (measured at K = 1024 / 8192)
+    const int groups = (t.fc1.npad / fc_tile) * nsplit;
+    const int gx = std::max(1, std::min(p.m_tiles, std::max(1, num_sms() / groups)));
+    p.a_tmem = mode == kTF32x3 && p.n <= 128 && p.m_tiles > gx && !std::getenv("SIMNET_FC1_SS");
     p.stages = kStages;
-    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages) > 226 * 1024) --p.stages;
+    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0) > 226 * 1024) --p.stages;
     p.bias = nullptr;
     p.relu = 0;
     p.out = part;
@@ -697,7 +768,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     const uint64_t ostr[2] = {static_cast<uint64_t>(c.fc_hidden) * 4, plane * 4};
     const uint32_t obox[3] = {32, 32, 1};
     const CUtensorMap omap = make_map(part, false, 3, odims, ostr, obox);
-    const size_t ring = static_cast<size_t>(p.stages) * kAChunk * (mode == kTF32x3 ? 2 : 1);
+    const size_t ring = static_cast<size_t>(p.stages) * kAChunk * (mode == kTF32x3 && !p.a_tmem ? 2 : 1);
     // each solo half must be whole 32-column groups
     p.tma_out = fc_tile % 64 == 0 && ring >= static_cast<size_t>(fc_tile / 32) * kAChunk &&
                 !std::getenv("SIMNET_FC1_DIRECT_STORE");

@@ -352,7 +352,8 @@ def test_fused_front_inputs_bit_exact(gpu, port, golden, precision, geom):
 def test_fc1_tma_store_matches_direct_store(gpu, port, golden, precision, monkeypatch):
     """FC1's split-K partials and the front's flat output, staged in shared
     memory and TMA-stored, equal the per-thread direct stores bit for bit,
-    including a partial last M tile / item (rows clipped by the tensor map)."""
+    including a partial last M tile / item (rows clipped by the tensor map);
+    FC1 with A in tensor memory (3xTF32) equals A read from shared memory."""
     g = gpu(precision)
     m, _ = _fused_cases(port, golden)
     g.load_model(m)
@@ -360,13 +361,32 @@ def test_fc1_tma_store_matches_direct_store(gpu, port, golden, precision, monkey
     for k in (130, 300):
         pc = pcfg(k)
         g.load_trace(t, pc)
-        for v in ("SIMNET_FC1_DIRECT_STORE", "SIMNET_FLAT_DIRECT_STORE"):
+        toggles = ("SIMNET_FC1_DIRECT_STORE", "SIMNET_FLAT_DIRECT_STORE", "SIMNET_FC1_SS")
+        for v in toggles:
             monkeypatch.delenv(v, raising=False)
         a = g.run(pc)
-        for v in ("SIMNET_FC1_DIRECT_STORE", "SIMNET_FLAT_DIRECT_STORE"):
+        for v in toggles:
             monkeypatch.setenv(v, "1")
         b = g.run(pc)
         assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch), k
+
+
+def test_fc1_tmem_a_multi_tile(gpu, port, monkeypatch):
+    """FC1 CTAs looping over several M tiles (K > 9 x 128 sub-traces) take A
+    from tensor memory (3xTF32); results equal A read from shared memory, bit
+    for bit, and stay within 0.1% of the CPU oracle."""
+    g = gpu("tf32x3")
+    m, t = _bench_like("default", n=24_000)
+    g.load_model(m)
+    pc = pcfg(1500)
+    g.load_trace(t, pc)
+    monkeypatch.delenv("SIMNET_FC1_SS", raising=False)
+    a = g.run(pc)
+    monkeypatch.setenv("SIMNET_FC1_SS", "1")
+    b = g.run(pc)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    want = port.simulate(t, m, k=1500)
+    assert abs(a.total_cycles - want["total_cycles"]) <= 1e-3 * want["total_cycles"]
 
 
 @pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
