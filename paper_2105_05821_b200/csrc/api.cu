@@ -323,6 +323,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     fp.first = f;
     fp.last = l;
     fp.stat = c->stat.as<float>();
+    fp.stat_rows = c->g1 - c->g0;
     fp.pc = c->pc.as<uint64_t>();
     fp.addr = c->addr.as<uint64_t>();
     fp.iflags = c->iflags.as<uint8_t>();

@@ -480,6 +480,26 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// f32, no swizzle (byte-exact rows in shared memory)
+CUtensorMap make_map_plain(const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                           const uint32_t* box) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t gd[3];
+  cuuint64_t gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(ptr), gd, gs, bx, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ApiError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
 CUtensorMap make_map(const void* ptr, bool bf16, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                      const uint32_t* box) {
   CUtensorMap m;
@@ -842,8 +862,14 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   fp.b1 = P + m.L.b[1];
   fp.b2 = P + m.L.b[2];
   fp.out = fb.act[2];
-  CUtensorMap w[7] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi,
-                      t.conv[1].map_lo, t.conv[2].map_hi, t.conv[2].map_lo, t.conv[0].map_hi};
+  CUtensorMap w[8] = {t.conv[0].map_hi, t.conv[0].map_lo, t.conv[1].map_hi, t.conv[1].map_lo,
+                      t.conv[2].map_hi, t.conv[2].map_lo, t.conv[0].map_hi, t.conv[0].map_hi};
+  if (fp.stat && fp.stat_rows > 0) {  // tile-0 static rows, staged by the front's producer
+    const uint64_t dims[2] = {static_cast<uint64_t>(kStatStride), fp.stat_rows};
+    const uint64_t strides[1] = {static_cast<uint64_t>(kStatStride) * 4};
+    const uint32_t box[2] = {44, 32};
+    w[7] = make_map_plain(fp.stat, 2, dims, strides, box);
+  }
   const uint64_t samples = fp.last - fp.first;
   fp.out_tma = 0;
   if (t.mode != kBF16 && samples > 0 && !std::getenv("SIMNET_FLAT_DIRECT_STORE")) {

@@ -49,6 +49,13 @@ constexpr uint32_t kR1 = 128 * 1024;
 constexpr uint32_t kR2 = 64 * 1024;
 constexpr uint32_t kTbl = kItem * kTblCols * (4 + 16);
 constexpr uint32_t kOutStage = 96 * 1024;  // flat staging in R1 (2 x 16 KB)
+// Tile-0 static-slot staging in R1 during the decode (R1 holds W2 [0, 64 KB)
+// and h / y [64 KB, 74 KB) then): per sample one TMA box of 32 trace rows
+// [lo, lo + 32) ending at the predicted target, 176 B per row (11 x 16 B: an
+// odd pitch, so LDS.128 of 8 rows hit 8 distinct bank groups).
+constexpr uint32_t kStgOff = 74 * 1024;
+constexpr uint32_t kStgPitch = 176;
+constexpr uint32_t kStgBox = 32 * kStgPitch;  // 5632 B, 128-B aligned
 constexpr int kThreadsRF = 320;
 constexpr int kCompute = 256;
 
@@ -206,7 +213,8 @@ __global__ void __launch_bounds__(kThreadsRF, 1)
 round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW0lo,
                    const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW1lo,
                    const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW2lo,
-                   const __grid_constant__ CUtensorMap tmOut, FrontParams p) {
+                   const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmStat,
+                   FrontParams p) {
   using S = Shape<kMode>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* R1 = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
@@ -226,6 +234,9 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __shared__ __align__(8) uint64_t bar_tg;         // the items' next-target pc / address / flags prefetched
   __shared__ uint64_t s_tidx[kItem], s_tpc[kItem], s_taddr[kItem];
   __shared__ uint32_t s_tfl[kItem];
+  __shared__ __align__(8) uint64_t bar_stg;        // tile-0 static rows staged in R1 (bulk copies)
+  __shared__ __align__(8) uint64_t bar_fo;         // flat-output staging in R1 read back (8 warps), 1 / item
+  __shared__ uint32_t s_stg_lo[kItem], s_stg_hi[kItem];  // staged trace-row range per sample (hi - row = slot)
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[3][kC];
   __shared__ float s_zero[kSlots], s_one[kSlots];
@@ -271,6 +282,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     mbar_init(&bar_w2, 1);
     mbar_init(&bar_st, 1);
     mbar_init(&bar_tg, 1);
+    mbar_init(&bar_stg, 1);
+    mbar_init(&bar_fo, kCompute / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -336,6 +349,26 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           mbar_wait(&bar_st, it & 1);
           uint64_t idx[kItem], tpc[kItem], tad[kItem];
           uint32_t tfl[kItem];
+          {  // stage the tile-0 static rows: trace rows [max(begin, target - 31), target]
+            if (it > 0) mbar_wait(&bar_fo, (it - 1) & 1);  // previous item's flat staging (R1 96 KB+) read
+            uint32_t total = 0;
+#pragma unroll
+            for (int w = 0; w < kItem; ++w) {
+              const SubState& ss = s_state[w];
+              const uint32_t pos = ss.pos + ((ss.awaiting || ss.has_pend) ? 1u : 0u);
+              const bool ok = w < static_cast<int>(cnt) && ss.status == kOk && pos < ss.len;
+              const uint32_t hi = ok ? static_cast<uint32_t>(ss.begin + pos) : 0u;
+              const uint32_t lo = ok ? (pos >= 31u ? hi - 31u : static_cast<uint32_t>(ss.begin)) : 1u;
+              s_stg_lo[w] = lo;
+              s_stg_hi[w] = ok ? lo + 31u : 0u;  // the whole box (rows past the trace read as zeros)
+              total += ok ? kStgBox : 0u;
+            }
+            mbar_expect_tx(&bar_stg, total);  // arrives: the ranges above are released with it
+#pragma unroll 1
+            for (int w = 0; w < kItem; ++w)
+              if (s_stg_lo[w] <= s_stg_hi[w])
+                tma_load_2d(R1 + kStgOff + w * kStgBox, &tmStat, &bar_stg, 0, static_cast<int>(s_stg_lo[w]));
+          }
 #pragma unroll
           for (int w = 0; w < kItem; ++w) {
             const SubState& ss = s_state[w];
@@ -537,6 +570,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       // Thread = (sample `warp`, column 32t + lane): one A half-row (50 slots of
       // one context column) per thread per tile: 11 float4 static-slot loads in
       // flight, the 9 dynamic slots from the column table, 16-B stores.
+      mbar_wait(&bar_stg, it & 1);  // tile-0 staging landed (issued by the producer during the decode)
       const long long t_gather0 = tx ? clock64() : 0;
       if (tx && it == 0 && tid == 0) tx[10] = t_gather0;
       for (int t = 0; t < T; ++t) {
@@ -550,12 +584,24 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         {
           // the row's 41 static slots: six 32-B loads (one L2 sector each; rows
           // are 192 B, sector aligned) instead of eleven 16-B ones
-          const float* srow =
-              p.stat + static_cast<uint64_t>(live ? tbl_inst[warp * kTblCols + col] : 0u) * kStatStride;
+          const uint32_t row = live ? tbl_inst[warp * kTblCols + col] : 0u;
+          const float* srow = p.stat + static_cast<uint64_t>(row) * kStatStride;
+          const uint32_t slo = s_stg_lo[warp], shi = s_stg_hi[warp];
+          const bool staged = t == 0 && live && row >= slo && row <= shi;
           float w[48];
 #pragma unroll
           for (int i = 0; i < 48; ++i) w[i] = 0.0f;
-          if (live) {
+          if (staged) {  // from the R1 staging (landed during the decode)
+            const float4* sp = reinterpret_cast<const float4*>(R1 + kStgOff + warp * kStgBox + (row - slo) * kStgPitch);
+#pragma unroll
+            for (int i = 0; i < 11; ++i) {
+              const float4 x = sp[i];
+              w[4 * i] = x.x;
+              w[4 * i + 1] = x.y;
+              w[4 * i + 2] = x.z;
+              w[4 * i + 3] = x.w;
+            }
+          } else if (live) {
 #pragma unroll
             for (int i = 0; i < 6; ++i)
               asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -597,8 +643,10 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           }
         }
         // loads and values above overlap the previous tile's MMAs; only the
-        // operand writes wait for them to finish reading R1
+        // operand writes wait for them to finish reading R1 (tile 0: for every
+        // thread to finish reading the staging, which the operand overlaps)
         if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);
+        if (t == 0) compute_sync();
         if (t == 1) stampx(3);
         if (h == 0) {  // K 0..49
 #pragma unroll
@@ -725,7 +773,10 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         }
       }
       tc_fence_before();
-      if (out_tma && lane == 0) bulk_wait_read();  // staging is read: R1 reusable
+      if (lane == 0) {
+        if (out_tma) bulk_wait_read();  // staging is read: R1 reusable
+        mbar_arrive(&bar_fo);
+      }
       compute_sync();  // TMEM conv2 columns and the tables are free for the next item
       mark(12);
     }
@@ -791,11 +842,11 @@ void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, in
   const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
   const size_t sm = front_smem_bytes();
   if (mode == kBF16)
-    launch_pdl_tag("front", round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], p);
+    launch_pdl_tag("front", round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], p);
   else if (mode == kTF32)
-    launch_pdl_tag("front", round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], p);
+    launch_pdl_tag("front", round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], p);
   else
-    launch_pdl_tag("front", round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], p);
+    launch_pdl_tag("front", round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], p);
 }
 
 void round_front_set_attributes() {

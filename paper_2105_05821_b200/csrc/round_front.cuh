@@ -19,6 +19,7 @@ struct FrontParams {
   uint32_t pmask, wmask;
   uint64_t first, last;      // sub-trace range of this launch (chunk)
   const float* stat;         // [n][kStatStride] normalised static slots
+  uint64_t stat_rows;        // n (rows of the static table on the device)
   const uint64_t* pc;
   const uint64_t* addr;
   const uint8_t* iflags;
@@ -49,7 +50,8 @@ struct FrontParams {
 };
 
 // w: {W0 hi, W0 lo, W1 hi, W1 lo, W2 hi, W2 lo} tensor maps (box 1 chunk x 64 rows),
-//    w[6]: flat viewed as [(last-first)*16 rows][64 f32], box 32 x 32, SWIZZLE_128B (p.out_tma)
+//    w[6]: flat viewed as [(last-first)*16 rows][64 f32], box 32 x 32, SWIZZLE_128B (p.out_tma),
+//    w[7]: the static-slot table viewed as [trace rows][48 f32], box 44 x 32, no swizzle
 void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, int num_sms, cudaStream_t s);
 void round_front_set_attributes();
 // After the last round: decode the outstanding predictions, apply them and

@@ -86,6 +86,72 @@ __global__ void mma_probe(int n, int count, int ts, int nacc, long long* out) {
   }
 }
 
+// 3xTF32 k-step patterns, N = n output channels (SS):
+//   pattern 0: Alo*Whi, Ahi*Wlo, Ahi*Whi into one accumulator (3 MMAs of N)
+//   pattern 1: Ahi*[Whi;Wlo] (one MMA of 2N) + Alo*Whi into the cross half (N)
+__global__ void ksteps_probe(int n, int ksteps, int pattern, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t id1 = instr_desc(2, n), id2 = instr_desc(2, 2 * n);
+    const uint32_t ahi = su32(base), alo = su32(base + 16384), whi = su32(base + 32768), wlo = whi + n * 128;
+    long long t0 = clock64();
+    for (int s = 0; s < ksteps; ++s) {
+      const int j = s & 3;
+      const uint64_t dah = smem_desc_sw128(ahi + j * 32), dal = smem_desc_sw128(alo + j * 32);
+      const uint64_t dwh = smem_desc_sw128(whi + j * 32), dwl = smem_desc_sw128(wlo + j * 32);
+      if (pattern == 0) {
+        mma<kTF32>(tmem, dal, dwh, id1, s > 0);
+        mma<kTF32>(tmem, dah, dwl, id1, 1);
+        mma<kTF32>(tmem, dah, dwh, id1, 1);
+      } else {
+        mma<kTF32>(tmem, dah, dwh, id2, s > 0);       // [main | cross] = Ahi * [Whi ; Wlo]
+        mma<kTF32>(tmem + n, dal, dwh, id1, 1);       // cross += Alo * Whi
+      }
+    }
+    long long t1 = clock64();
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+extern "C" int probe_ksteps(int n, int ksteps, int pattern, long long* host) {
+  long long* d;
+  cudaMalloc(&d, 16 * sizeof(long long));
+  const size_t sm = 100 * 1024;
+  cudaFuncSetAttribute(ksteps_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  ksteps_probe<<<1, 128, sm>>>(n, ksteps, pattern, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(host, d, 2 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
 extern "C" int probe(int mode, int n, int count, int ts, int nacc, long long* host) {
   long long* d;
   cudaMalloc(&d, 16 * sizeof(long long));

@@ -22,3 +22,12 @@ for mode, name in ((1, "tf32"),):
                 per = (t2 - t1) / (c2 - c1)
                 print(f"{name} N={n:3d} {'TS' if ts else 'SS'} acc={nacc % 10}{' warp-wide' if nacc > 10 else ''}: {per:6.1f} cyc/MMA (issue {(i2 - i1) / (c2 - c1):5.1f}), "
                       f"floor {128 * n / 256:.0f}; err {e}")
+
+for n in (64, 128):
+    for pattern in (0, 1):
+        r = []
+        for ks in (16, 64):
+            e = L.probe_ksteps(n, ks, pattern, out.ctypes.data_as(C.c_void_p))
+            r.append((ks, out[1]))
+        per = (r[1][1] - r[0][1]) / (r[1][0] - r[0][0])
+        print(f"3xTF32 k-step N={n} pattern {'3 MMAs' if pattern == 0 else 'stacked 2N + N'}: {per:6.1f} cyc/k-step; err {e}")
