@@ -66,8 +66,13 @@ __device__ __forceinline__ void warp_decode_triple(const float* y, const double*
 //   butterfly (xor 2, 1); y[s][o] = that + b2[o].
 // w2_bar: when non-null, W2 is still landing (bulk copy): wait on this
 // mbarrier phase parity right before FC2, after the partials are reduced.
+// part_smem: the CTA's 8 partial rows per plane in shared memory,
+// [q][8][hidden] (landing on part_bar, phase parity part_parity); every
+// thread then arrives on read_bar once its partials are consumed.
 __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const float* w2s, float* hs, float* ys,
-                               long long* trace = nullptr, uint64_t* w2_bar = nullptr, uint32_t w2_parity = 0) {
+                               long long* trace = nullptr, uint64_t* w2_bar = nullptr, uint32_t w2_parity = 0,
+                               const float* part_smem = nullptr, uint64_t* part_bar = nullptr,
+                               uint64_t* read_bar = nullptr, uint32_t part_parity = 0) {
   const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
   const int hid = a.hidden, c4 = hid >> 2;
   // biases fetched with the partials (no dependent global load later): lane j
@@ -80,14 +85,26 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
                                 : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   {  // h of this warp's sample
     float4 pv[2][kFcMaxSplit];
+    if (part_smem) {
+      mbar_wait(part_bar, part_parity);
+      const float4* ps = reinterpret_cast<const float4*>(part_smem + warp * hid);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int c = lane + 32 * u;
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
 #pragma unroll
-      for (int q = 0; q < kFcMaxSplit; ++q)
-        pv[u][q] = (c < c4 && q < a.nsplit)
-                       ? __ldg(reinterpret_cast<const float4*>(a.part + q * a.split_stride + s_local * hid) + c)
-                       : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        for (int q = 0; q < kFcMaxSplit; ++q)
+          pv[u][q] = (c < c4 && q < a.nsplit) ? ps[q * 2 * hid + c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
+#pragma unroll
+        for (int q = 0; q < kFcMaxSplit; ++q)
+          pv[u][q] = (c < c4 && q < a.nsplit)
+                         ? __ldg(reinterpret_cast<const float4*>(a.part + q * a.split_stride + s_local * hid) + c)
+                         : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -107,6 +124,7 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
                       fmaxf(acc.w + b.w, 0.0f));
     }
   }
+  if (part_smem) mbar_arrive(read_bar);  // partials consumed (they fed the h stores above)
   if (w2_bar) mbar_wait(w2_bar, w2_parity);
   fc_sync256();
   if (trace && threadIdx.x == 0) trace[0] = clock64();

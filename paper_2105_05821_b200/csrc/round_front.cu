@@ -208,7 +208,10 @@ __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float
 
 }  // namespace
 
-template <int kMode>
+// kMulti: the launch gives CTAs several items (K > 8 x SMs); later items get
+// their FC1 partial rows bulk-copied into R2 during the previous item's tail.
+// A separate instantiation, so the single-item kernel's code is untouched.
+template <int kMode, bool kMulti>
 __global__ void __launch_bounds__(kThreadsRF, 1)
 round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW0lo,
                    const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW1lo,
@@ -236,6 +239,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   __shared__ uint32_t s_tfl[kItem];
   __shared__ __align__(8) uint64_t bar_stg;        // tile-0 static rows staged in R1 (bulk copies)
   __shared__ __align__(8) uint64_t bar_fo;         // flat-output staging in R1 read back (8 warps), 1 / item
+  __shared__ __align__(8) uint64_t bar_part;       // the item's FC1 split-K partial rows landed in R2, 1 / item
+  __shared__ __align__(8) uint64_t bar_pread;      // ... and were read by the decode (256): R2 free for W0
   __shared__ uint32_t s_stg_lo[kItem], s_stg_hi[kItem];  // staged trace-row range per sample (hi - row = slot)
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[3][kC];
@@ -284,6 +289,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     mbar_init(&bar_tg, 1);
     mbar_init(&bar_stg, 1);
     mbar_init(&bar_fo, kCompute / 32);
+    mbar_init(&bar_part, 1);
+    mbar_init(&bar_pread, kCompute);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -327,11 +334,27 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
                 : "memory");
           }
         }
-        load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
+        if (it == 0) load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);  // a constant: ahead of the dependency wait
         {  // the item's sub-trace states, contiguous in HBM: one bulk copy, ahead of the decode
           if (it == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round final (PDL)
           const uint64_t s0 = p.first + static_cast<uint64_t>(item) * kItem;
           const uint64_t cnt = p.calibrate ? 0 : (p.last - s0 < kItem ? p.last - s0 : kItem);
+          if (kMulti && it > 0) {
+            // later items: the item's rows of the FC1 split-K partial planes -> R2
+            // [q][8][hidden] right after the previous item's conv2 (W0 comes after
+            // the decode has read them).  The first item reads them with direct
+            // loads: at kernel start the TMA unit is busy with W2, W0 and the staging.
+            const uint32_t row_bytes = static_cast<uint32_t>(p.fc.hidden) * 4u;
+            const uint32_t bytes = static_cast<uint32_t>(cnt) * row_bytes;
+            mbar_expect_tx(&bar_part, bytes * static_cast<uint32_t>(p.fc.nsplit));
+            for (int q = 0; q < p.fc.nsplit && bytes > 0; ++q)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      su32(R2 + q * kItem * row_bytes)),
+                  "l"(p.fc.part + q * p.fc.split_stride + (s0 - p.first) * p.fc.hidden), "r"(bytes),
+                  "r"(su32(&bar_part))
+                  : "memory");
+          }
           const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(SubState));
           if (bytes == 0) {
             mbar_arrive(&bar_st);
@@ -388,6 +411,10 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
             s_tfl[w] = tfl[w];
           }
           mbar_arrive(&bar_tg);  // release: the smem stores above are visible to waiters
+        }
+        if (kMulti && it > 0) {
+          mbar_wait(&bar_pread, (it - 1) & 1);  // the decode has read the partials: R2 takes W0
+          load_w(0, &tmW0, &tmW0lo, S::kK0Chunks);
         }
         mbar_wait(&bar_c0, it & 1);  // conv0 MMAs done: W0 no longer read
         load_w(1, &tmW1, &tmW1lo, S::kKChunks);
@@ -489,7 +516,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         float* hs = reinterpret_cast<float*>(R1) + kFcMaxOut * kFcMaxHidden;
         float* ys = hs + kItem * kFcMaxHidden;
         cta8_fc(p.fc, (mine ? s : p.first) - p.first, reinterpret_cast<const float*>(R1), hs, ys,
-                (tr && it == 0) ? tr + 28 : nullptr, &bar_w2, it & 1);
+                (tr && it == 0) ? tr + 28 : nullptr, &bar_w2, it & 1,
+                kMulti && it > 0 ? reinterpret_cast<const float*>(R2) : nullptr, &bar_part, &bar_pread, (it - 1) & 1);
         if (tr && it == 0 && lane == 0 && warp == 0) tr[25] = clock64();
         int ncs = -1;
         if (mine) {
@@ -841,19 +869,27 @@ void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, in
   const uint64_t items = (samples + kItem - 1) / kItem;
   const dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(num_sms) ? items : num_sms));
   const size_t sm = front_smem_bytes();
+  const bool multi = items > grid.x;
+#define SIMNET_FRONT(M, MU) \
+  launch_pdl_tag("front", round_front_kernel<M, MU>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], \
+                 w[5], w[6], w[7], p)
   if (mode == kBF16)
-    launch_pdl_tag("front", round_front_kernel<kBF16>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], p);
+    multi ? SIMNET_FRONT(kBF16, true) : SIMNET_FRONT(kBF16, false);
   else if (mode == kTF32)
-    launch_pdl_tag("front", round_front_kernel<kTF32>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], p);
+    multi ? SIMNET_FRONT(kTF32, true) : SIMNET_FRONT(kTF32, false);
   else
-    launch_pdl_tag("front", round_front_kernel<kTF32x3>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], p);
+    multi ? SIMNET_FRONT(kTF32x3, true) : SIMNET_FRONT(kTF32x3, false);
+#undef SIMNET_FRONT
 }
 
 void round_front_set_attributes() {
   const int sm = static_cast<int>(front_smem_bytes());
-  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kBF16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32x3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kBF16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32x3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
 }
 
 }  // namespace simnet
