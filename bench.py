@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--precision", default=os.environ.get("SIMNET_PRECISION", "tf32x3"),
-                   choices=["fp32", "tf32x3", "tf32", "bf16"])
+                   choices=["fp32", "tf32x3", "tf32", "bf16", "fp8"])
     p.add_argument("--instructions", dest="n", type=int, default=N_INSTR)
     p.add_argument("--k", type=int, default=K_SUB)
     p.add_argument("--regime", default="default", choices=["default", "memory"])
@@ -281,9 +281,10 @@ def main():
     launch_ms = dom_ms / rounds
     pk = peaks()
     if tc:
-        div = 1.0 if args.precision == "bf16" else 2.0
+        div = {"bf16": 1.0, "fp8": 0.5}.get(args.precision, 2.0)
         peak_val = pk.get("bf16_tflops_sustained", 1365.8) / div
-        peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" + ("" if div == 1.0 else " / 2 (tf32 rate)")
+        peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" + {1.0: "", 0.5: " x 2 (fp8 e4m3 rate)"}.get(
+            div, " / 2 (tf32 rate)")
         if args.precision == "tf32x3":
             peak_src += "; 3xTF32 issues 3 tensor ops per algorithmic op"
     else:
@@ -326,7 +327,7 @@ def main():
     line = {
         "metric": "simulated MIPS", "value": value, "unit": "MIPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if args.precision in ("fp32", "tf32x3") else args.precision,
+        "vs_baseline": None, "dtype": "f32" if args.precision in ("fp32", "tf32x3") else ("e4m3" if args.precision == "fp8" else args.precision),
         "data": "synthetic trace + random-init C3 weights (reference init rule), resident in HBM",
         "config": {"workload": f"c2: C3 CNN predictor, {args.n} instructions x {world} GPU(s), {args.k} sub-traces per GPU",
                    "precision": args.precision, "regime": args.regime, "sub_traces": args.k * world,

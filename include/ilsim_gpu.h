@@ -32,12 +32,17 @@ typedef struct ilsim_gpu_ctx ilsim_gpu_ctx;
  * FP32   : SIMT fp32 FFMA (exact fp32 products, order differs from Eigen).
  * TF32X3 : tcgen05 kind::tf32 with the 3-term hi/lo split (fp32-faithful).
  * TF32   : tcgen05 kind::tf32, one pass.
- * BF16   : tcgen05 kind::f16 with bf16 operands, fp32 accumulate.          */
+ * BF16   : tcgen05 kind::f16 with bf16 operands, fp32 accumulate.
+ * FP8    : tcgen05 kind::f8f6f4, e4m3 activations and weights (per-layer
+ *          power-of-two weight scale), fp32 accumulate and fp32 FC tail.
+ *          Fused simulate path only (no teacher-forced predict, no unfused
+ *          rounds); its CPI error is reported, not bounded.                 */
 enum {
   ILSIM_PREC_FP32 = 0,
   ILSIM_PREC_TF32X3 = 1,
   ILSIM_PREC_TF32 = 2,
-  ILSIM_PREC_BF16 = 3
+  ILSIM_PREC_BF16 = 3,
+  ILSIM_PREC_FP8 = 4
 };
 
 typedef struct ilsim_gpu_options {

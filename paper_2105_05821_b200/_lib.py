@@ -13,7 +13,7 @@ from .errors import IlsimError
 
 LIB_PATH = Path(__file__).resolve().parent / "libilsim_gpu.so"
 
-PREC = {"fp32": 0, "tf32x3": 1, "tf32": 2, "bf16": 3}
+PREC = {"fp32": 0, "tf32x3": 1, "tf32": 2, "bf16": 3, "fp8": 4}
 
 
 class Options(C.Structure):

@@ -109,7 +109,7 @@ def main(argv=None) -> int:
     s.add_argument("--phase-report", default="", help="phase CPI csv (default: <report>.phase.csv)")
     s.add_argument("--throughput", default="", help="throughput csv")
     s.add_argument("--device", type=int, default=0, help="CUDA device")
-    s.add_argument("--precision", default="tf32x3", choices=["fp32", "tf32x3", "tf32", "bf16"])
+    s.add_argument("--precision", default="tf32x3", choices=["fp32", "tf32x3", "tf32", "bf16", "fp8"])
     s.add_argument("--warmup", type=int, default=0, help="extension: warm-up instructions per sub-trace")
     s.add_argument("--drain-trim", action="store_true", help="extension: count only the last sub-trace's drain")
     a = p.parse_args(argv)

@@ -233,6 +233,8 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   // kernel, the gathered input stays in shared memory.  reserved[2] = 1 forces
   // the unfused path (ctx_kernel + TMA conv chain), e.g. for A/B checks.
   const bool fused = !oracle && c->model.tc != nullptr && tc_fused_front(c->model.tc) && cfg.reserved[2] == 0;
+  if (!oracle && c->precision == ILSIM_PREC_FP8 && !fused)
+    throw ApiError("fp8 precision runs only the fused rounds (C3 shape, reserved[2] = 0)");
   const bool capture_mode = c->cap_round != UINT32_MAX;
   const uint32_t dump_stride = input_stride(mc, ILSIM_PREC_FP32);  // fused capture: f32 rows of 100
   // gathered inputs: f32 rows of 100, or (bf16 inference) bf16 rows of 104
@@ -594,7 +596,7 @@ int ilsim_gpu_create(const ilsim_gpu_options* o, ilsim_gpu_ctx** out, char* err,
     auto c = std::make_unique<ilsim_gpu_ctx>();
     c->device = o ? o->device : 0;
     c->precision = o ? o->precision : ILSIM_PREC_FP32;
-    if (c->precision < ILSIM_PREC_FP32 || c->precision > ILSIM_PREC_BF16)
+    if (c->precision < ILSIM_PREC_FP32 || c->precision > ILSIM_PREC_FP8)
       throw ApiError("unknown precision");
     int count = 0;
     CUDA_OK(cudaGetDeviceCount(&count));

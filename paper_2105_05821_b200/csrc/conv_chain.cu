@@ -207,7 +207,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, kC);
+      const uint32_t idesc = instr_desc(mode_fmt(kMode), kC);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;

@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -65,6 +66,7 @@ struct TcGemmParams {
   uint64_t out_split_stride;  // elements between split-K partial planes
   long long* trace;           // diagnostics (SIMNET_CHAIN_TRACE): per-CTA event clocks, 16 per CTA
   int stages;                 // A ring depth (2..kStages; 0 = kStages)
+  float out_scale;            // fp8: 1 / (power-of-two weight scale), applied to the accumulator
   int a_tmem;                 // 3xTF32: the split warps write A hi / lo into tensor memory (4-slot ring
                               // next to the accumulators) and the MMAs read A from there (SMEM: W only)
   int tma_out;                // f32 split-K partials through tmOut: CTAs owning one M tile stage the
@@ -126,7 +128,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const int elems = kMode == kBF16 ? 64 : 32;  // elements per 128 B chunk
+  const int elems = mode_chunk_elems(kMode);  // elements per 128 B chunk
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   long long* tr = p.trace ? p.trace + 148 * 32 + cta * 32 : nullptr;  // 32 words per CTA
   if (tr && threadIdx.x == 0) {
@@ -156,6 +158,10 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       float v[32];
       tmem_ld16(tl + c0, v);
       tmem_ld16(tl + c0 + 16, v + 16);
+      if constexpr (kMode == kFP8) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= p.out_scale;
+      }
       if (stamp && c0 == cb) tr[16] = clock64();  // first TMEM columns in registers
       uint8_t* stg = sA + (c0 >> 5) * kAChunk + r * 128;
 #pragma unroll
@@ -183,6 +189,10 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     for (int c0 = cb; c0 < ce; c0 += 16) {
       float v[16];
       tmem_ld16(tl + c0, v);
+      if constexpr (kMode == kFP8) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= p.out_scale;
+      }
       if (row < p.m) {
         const int col = ntile * p.n + c0;
 #pragma unroll
@@ -243,7 +253,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {
       mbar_wait(&bar_w, 0);
       if (tr) tr[1] = clock64();
-      const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, p.n);
+      const uint32_t idesc = instr_desc(mode_fmt(kMode), p.n);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -500,6 +510,28 @@ CUtensorMap make_map_plain(const void* ptr, int rank, const uint64_t* dims, cons
   return m;
 }
 
+// element size -> tensor-map data type (1: fp8 e4m3 as bytes, 2: bf16, 4: f32)
+CUtensorMap make_map_e(const void* ptr, int esz, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t gd[3];
+  cuuint64_t gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  const CUtensorMapDataType dt = esz == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                          : (esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  const CUresult r = encode_fn()(&m, dt, rank, const_cast<void*>(ptr), gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ApiError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
 CUtensorMap make_map(const void* ptr, bool bf16, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                      const uint32_t* box) {
   CUtensorMap m;
@@ -531,6 +563,34 @@ float tf32_round_host(float x) {  // cvt.rna.tf32.f32: round half away from zero
   return r;
 }
 
+// float -> fp8 e4m3 (round to nearest even, saturate to +-448; NaN -> 0x7f)
+uint8_t fp8_e4m3_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  const uint8_t sign = static_cast<uint8_t>((u >> 24) & 0x80u);
+  const float a = std::fabs(x);
+  if (std::isnan(x)) return 0x7f;
+  if (a >= 448.0f) return sign | 0x7e;  // max finite (satfinite)
+  if (a < std::ldexp(1.0f, -10)) return sign;  // below half the smallest subnormal (2^-9): 0
+  int e;
+  std::frexp(a, &e);  // a = f * 2^e, f in [0.5, 1)
+  int exp = e - 1;    // a = 1.xxx * 2^exp
+  if (exp < -6) {     // subnormal: multiples of 2^-9
+    const float q = std::nearbyint(std::ldexp(a, 9));  // round half even (default mode)
+    const int m = static_cast<int>(q);
+    if (m >= 8) return sign | 0x08;  // rounds up to the smallest normal
+    return sign | static_cast<uint8_t>(m);
+  }
+  float mant = std::ldexp(a, -exp) - 1.0f;                       // [0, 1)
+  int m = static_cast<int>(std::nearbyint(std::ldexp(mant, 3)));  // 3 bits, round half even
+  if (m == 8) {
+    m = 0;
+    ++exp;
+  }
+  if (exp > 8 || (exp == 8 && m == 7)) return sign | 0x7e;
+  return sign | static_cast<uint8_t>(((exp + 7) << 3) | m);
+}
+
 uint16_t bf16_rn_host(float x) {
   uint32_t u;
   std::memcpy(&u, &x, 4);
@@ -540,12 +600,14 @@ uint16_t bf16_rn_host(float x) {
 }
 
 struct TcWeights {
-  DevBuf hi, lo;  // K-major [npad][kpad] (f32 or bf16)
+  DevBuf hi, lo;  // K-major [npad][kpad] (f32, bf16 or fp8 e4m3)
   int n = 0, npad = 0, k = 0, kpad = 0, n_tile = 0;
+  float inv_scale = 1.0f;  // fp8: weights are stored x 2^e; accumulators are multiplied back by 2^-e
   CUtensorMap map_hi{}, map_lo{};  // box: one 128-B K chunk x n_tile rows
 };
 
 int mode_of(int precision) {
+  if (precision == ILSIM_PREC_FP8) return kFP8;
   return precision == ILSIM_PREC_BF16 ? kBF16 : (precision == ILSIM_PREC_TF32 ? kTF32 : kTF32x3);
 }
 
@@ -566,13 +628,31 @@ namespace {
 
 // Reference column-major W[o + k*N] -> K-major [npad][kpad], split per mode.
 void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int n_tile, cudaStream_t s) {
-  const int elem_per_chunk = mode == kBF16 ? 64 : 32;
+  const int elem_per_chunk = mode_chunk_elems(mode);
   w.n = n;
   w.k = k;
   w.npad = ((n + n_tile - 1) / n_tile) * n_tile;
   w.kpad = ((k + elem_per_chunk - 1) / elem_per_chunk) * elem_per_chunk;
   const size_t cnt = static_cast<size_t>(w.npad) * w.kpad;
-  if (mode == kBF16) {
+  if (mode == kFP8) {
+    // e4m3 (max 448): a per-tensor power-of-two scale keeps the largest weight
+    // near the top of the range (small weights stay out of the subnormals)
+    float amax = 0.0f;
+    for (int o = 0; o < n; ++o)
+      for (int q = 0; q < k; ++q) amax = std::max(amax, std::fabs(src[o + static_cast<size_t>(q) * n]));
+    int e = 0;
+    if (amax > 0.0f) e = static_cast<int>(std::floor(std::log2(448.0f / amax)));
+    e = std::max(-20, std::min(20, e));
+    const float sc = std::ldexp(1.0f, e);
+    w.inv_scale = std::ldexp(1.0f, -e);
+    std::vector<uint8_t> h(cnt, 0);
+    for (int o = 0; o < n; ++o)
+      for (int q = 0; q < k; ++q)
+        h[static_cast<size_t>(o) * w.kpad + q] = fp8_e4m3_host(src[o + static_cast<size_t>(q) * n] * sc);
+    w.hi.need(cnt);
+    CUDA_OK(cudaMemcpyAsync(w.hi.p, h.data(), cnt, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+  } else if (mode == kBF16) {
     std::vector<uint16_t> h(cnt, 0);
     for (int o = 0; o < n; ++o)
       for (int q = 0; q < k; ++q) h[static_cast<size_t>(o) * w.kpad + q] = bf16_rn_host(src[o + static_cast<size_t>(q) * n]);
@@ -595,10 +675,10 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
     CUDA_OK(cudaStreamSynchronize(s));
   }
   const uint64_t dims[2] = {static_cast<uint64_t>(w.kpad), static_cast<uint64_t>(w.npad)};
-  const uint64_t strides[1] = {static_cast<uint64_t>(w.kpad) * (mode == kBF16 ? 2 : 4)};
+  const uint64_t strides[1] = {static_cast<uint64_t>(w.kpad) * mode_esz(mode)};
   const uint32_t box[2] = {static_cast<uint32_t>(elem_per_chunk), static_cast<uint32_t>(n_tile)};
   w.n_tile = n_tile;
-  w.map_hi = make_map(w.hi.p, mode == kBF16, 2, dims, strides, box);
+  w.map_hi = make_map_e(w.hi.p, mode_esz(mode), 2, dims, strides, box);
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
 }
 
@@ -626,7 +706,9 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
   const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0);
-  if (mode == kBF16)
+  if (mode == kFP8)
+    launch_pdl_tag("layer_bf16", tc_layer_kernel<kFP8>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
+  else if (mode == kBF16)
     launch_pdl_tag("layer_bf16", tc_layer_kernel<kBF16>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
   else if (mode == kTF32)
     launch_pdl_tag("layer", tc_layer_kernel<kTF32>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
@@ -655,6 +737,7 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
   if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
   if (c.fc_hidden % 16 != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 16");
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kFP8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
   CUDA_OK(cudaFuncSetAttribute(tc_layer_kernel<kTF32x3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -686,7 +769,8 @@ TcModel* tc_model_create(const DevModel& m, const float* host_params, int precis
     // FC1 N tile: 128 hidden units for the f32 modes (one M tile per CTA at
     // K = 1024: 8 M x 2 N x 8 split planes = 128 CTAs), 64 for bf16 (4 planes),
     // else the whole (small) layer
-    const int fc_tile = (c.fc_hidden % 128 == 0 && mode != kBF16) ? 128 : (c.fc_hidden >= 64 ? 64 : c.fc_hidden);
+    const int fc_tile =
+        (c.fc_hidden % 128 == 0 && mode_esz(mode) == 4) ? 128 : (c.fc_hidden >= 64 ? 64 : c.fc_hidden);
     if (c.fc_hidden % fc_tile != 0) throw ApiError("tensor-core path: fc_hidden must be a multiple of 64 (or <= 64)");
     upload_weights(t->fc1, host_params + m.L.fc1_w, c.fc_hidden, m.L.flat, mode, fc_tile, s);
     // fc2 (reference column-major [od x hidden]) -> [od][hidden]
@@ -712,14 +796,13 @@ void tc_model_destroy(TcModel* t) { delete t; }
 // 2-stage A ring fits next to the 128 KB 3xTF32 W slice) measured slower:
 // the A loads are TMA-latency-bound and need the 4-stage ring.
 int fc1_cps(int mode) {
-  (void)mode;
-  return kMaxChunks;
+  return mode == kFP8 ? 2 : kMaxChunks;  // fp8: flat is 8 chunks -> 4 planes of 2
 }
 
 // Allocations the forward needs, done before any graph capture.
 void tc_prepare(const DevModel& m, uint64_t samples) {
   TcModel& t = *m.tc;
-  const int esz = t.mode == kBF16 ? 2 : 4;
+  const int esz = mode_esz(t.mode);
   const int total_chunks = (m.L.flat * esz + 127) / 128;
   const int nsplit = (total_chunks + fc1_cps(t.mode) - 1) / fc1_cps(t.mode);
   t.part.need(samples * static_cast<uint64_t>(m.cfg.fc_hidden) * nsplit * sizeof(float));
@@ -727,7 +810,7 @@ void tc_prepare(const DevModel& m, uint64_t samples) {
 
 bool tc_split_input(const TcModel* t) { return t->chain && t->mode == kTF32x3; }
 
-uint32_t tc_act_bytes(const TcModel* t) { return t->mode == kBF16 ? 2u : 4u; }
+uint32_t tc_act_bytes(const TcModel* t) { return static_cast<uint32_t>(mode_esz(t->mode)); }
 
 // FC1 (split-K tcgen05 partials) and the FC tail (FC2 + fused K3) on the
 // flat conv output `in`.
@@ -737,9 +820,8 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
   TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
   const int mode = t.mode;
-  const bool bf = mode == kBF16;
-  const int esz = bf ? 2 : 4;
-  const int chunk_elems = bf ? 64 : 32;
+  const int esz = mode_esz(mode);
+  const int chunk_elems = mode_chunk_elems(mode);
   const float* P = m.params.as<float>();
   uint64_t launches = 0;
   // FC1 split-K partials
@@ -752,7 +834,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     const uint64_t dims[2] = {static_cast<uint64_t>(flat), samples};
     const uint64_t strides[1] = {static_cast<uint64_t>(flat) * esz};
     const uint32_t box[2] = {static_cast<uint32_t>(chunk_elems), kBM};
-    const CUtensorMap amap = make_map(in, bf, 2, dims, strides, box);
+    const CUtensorMap amap = make_map_e(in, esz, 2, dims, strides, box);
     const uint64_t plane = samples * static_cast<uint64_t>(c.fc_hidden);
     // this slice's own [nsplit][samples][hidden] block (slices run concurrently)
     const uint64_t base = fb.part_off * nsplit * static_cast<uint64_t>(c.fc_hidden);
@@ -779,6 +861,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.ldo = c.fc_hidden;
     p.out_bf16 = 0;
     p.out_split_stride = plane;
+    p.out_scale = t.fc1.inv_scale;
     p.trace = chain_trace_active();
     if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
@@ -832,7 +915,7 @@ void tc_calibrate(const DevModel& m, cudaStream_t s) {
 FcDecodeArgs tc_fc_decode_args(const DevModel& m, uint64_t samples, const ForwardBuffers& fb) {
   const TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
-  const int esz = t.mode == kBF16 ? 2 : 4;
+  const int esz = mode_esz(t.mode);
   const int total_chunks = (m.L.flat * esz + 127) / 128;
   const int nsplit = (total_chunks + fc1_cps(t.mode) - 1) / fc1_cps(t.mode);
   if (m.L.out_dim > 64 || c.fc_hidden % 4 != 0) throw ApiError("tensor-core path: FC tail supports fc_hidden multiple of 4 and <= 64 outputs");
@@ -872,7 +955,8 @@ uint64_t tc_front(const DevModel& m, FrontParams fp, const ForwardBuffers& fb, c
   }
   const uint64_t samples = fp.last - fp.first;
   fp.out_tma = 0;
-  if (t.mode != kBF16 && samples > 0 && !std::getenv("SIMNET_FLAT_DIRECT_STORE")) {
+  for (int l = 0; l < 3; ++l) fp.wscale[l] = t.conv[l].inv_scale;
+  if (mode_esz(t.mode) == 4 && samples > 0 && !std::getenv("SIMNET_FLAT_DIRECT_STORE")) {
     // flat as [samples * 16 rows][64 f32]: the front TMA-stores 32 x 32 boxes
     const uint64_t dims[2] = {64, samples * 16};
     const uint64_t strides[1] = {64 * 4};
@@ -892,6 +976,7 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
   TcModel& t = *m.tc;
   const ilsim_cnn_config& c = m.cfg;
   const int mode = t.mode;
+  if (mode == kFP8) throw ApiError("fp8 precision runs only the fused simulate path (no unfused forward / predict)");
   const bool bf = mode == kBF16;
   const int esz = bf ? 2 : 4;
   const int chunk_elems = bf ? 64 : 32;

@@ -28,6 +28,7 @@
 //   warp 9      TMEM allocator + tcgen05.mma issuer
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 
 #include <cstdlib>
 
@@ -74,14 +75,23 @@ __device__ __forceinline__ uint32_t sw128_bf16(int r, int k) {
   return chunk * (128 * 128) + r * 128 + ((((kk >> 3) ^ (r & 7)) << 4) | ((kk & 7) << 1));
 }
 
+// fp8 e4m3 element (row r, k), 128 elements per chunk
+__device__ __forceinline__ uint32_t sw128_fp8(int r, int k) {
+  const int chunk = k >> 7, kk = k & 127;
+  return chunk * (128 * 128) + r * 128 + ((((kk >> 4) ^ (r & 7)) << 4) | (kk & 15));
+}
+__device__ __forceinline__ uint16_t fp8x2(float v0, float v1) {
+  return static_cast<uint16_t>(__nv_cvt_float2_to_fp8x2(make_float2(v0, v1), __NV_SATFINITE, __NV_E4M3));
+}
+
 template <int kMode>
 struct Shape {
   static constexpr bool kSplit = kMode == kTF32x3;
-  static constexpr int kElems = kMode == kBF16 ? 64 : 32;   // elements per 128 B chunk
-  static constexpr int kK0Chunks = kMode == kBF16 ? 2 : 4;  // conv0 K = 100 (+pad)
-  static constexpr int kK0Steps = kMode == kBF16 ? 7 : 13;  // 32 B k-steps covering K = 100
-  static constexpr int kPadUnits = kMode == kBF16 ? 6 : 2;  // float2 units of zeros after K = 100
-  static constexpr int kKChunks = kMode == kBF16 ? 2 : 4;   // conv1/2 K = 128
+  static constexpr int kElems = mode_chunk_elems(kMode);                           // elements per 128 B chunk
+  static constexpr int kK0Chunks = kMode == kFP8 ? 1 : (kMode == kBF16 ? 2 : 4);   // conv0 K = 100 (+pad)
+  static constexpr int kK0Steps = kMode == kFP8 ? 4 : (kMode == kBF16 ? 7 : 13);   // 32 B k-steps covering K = 100
+  static constexpr int kPadUnits = kMode == kFP8 ? 14 : (kMode == kBF16 ? 6 : 2);  // pairs of zeros after K = 100
+  static constexpr int kKChunks = kMode == kFP8 ? 1 : (kMode == kBF16 ? 2 : 4);    // conv1/2 K = 128
   static constexpr uint32_t kWBytes = kC * 128 * kKChunks;  // one weight copy (hi or lo)
   static constexpr uint32_t kStage = 128 * 128;             // one A chunk (128 rows x 128 B)
   static constexpr uint32_t kALo = kKChunks * kStage;       // lo plane of a restaged A
@@ -92,7 +102,9 @@ struct Shape {
 // operand planes: 3xTF32 hi = cvt.rna, lo = v - hi (exact); tf32 plain; bf16 rn.
 template <int kMode>
 __device__ __forceinline__ void put2(uint8_t* a, uint32_t lo_off, int r, int k, float v0, float v1) {
-  if constexpr (kMode == kBF16) {
+  if constexpr (kMode == kFP8) {
+    *reinterpret_cast<uint16_t*>(a + sw128_fp8(r, k)) = fp8x2(v0, v1);
+  } else if constexpr (kMode == kBF16) {
     __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
     *reinterpret_cast<__nv_bfloat162*>(a + sw128_bf16(r, k)) = b;
   } else {
@@ -112,7 +124,10 @@ __device__ __forceinline__ void put2(uint8_t* a, uint32_t lo_off, int r, int k, 
 template <int kMode>
 __device__ __forceinline__ void put4(uint8_t* a, uint32_t lo_off, int r, int k, float v0, float v1, float v2,
                                      float v3) {
-  if constexpr (kMode == kBF16) {
+  if constexpr (kMode == kFP8) {
+    *reinterpret_cast<uint32_t*>(a + sw128_fp8(r, k)) =
+        static_cast<uint32_t>(fp8x2(v0, v1)) | (static_cast<uint32_t>(fp8x2(v2, v3)) << 16);
+  } else if constexpr (kMode == kBF16) {
     put2<kMode>(a, lo_off, r, k, v0, v1);
     put2<kMode>(a, lo_off, r, k + 2, v2, v3);
   } else {
@@ -155,7 +170,7 @@ __device__ __forceinline__ int conv1_slot(int p) { return (p & 1) ? 8 + ((p >> 1
 
 template <int kMode>
 __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float* accv, int ar, int k0,
-                                            const float* bias) {
+                                            const float* bias, float scale) {
   using S = Shape<kMode>;
   uint32_t raw[kC];
   if (accv) {  // accumulator row known in advance (shared memory), no TMEM read
@@ -170,8 +185,20 @@ __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float
   for (int c0 = 0; c0 < kC; c0 += 16) {
     float v[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = fmaxf(__uint_as_float(raw[c0 + i]) + bias[c0 + i], 0.0f);
-    if constexpr (kMode == kBF16) {
+    for (int i = 0; i < 16; ++i) {
+      float x = __uint_as_float(raw[c0 + i]);
+      if constexpr (kMode == kFP8) x *= scale;  // undo the weight scale
+      v[i] = fmaxf(x + bias[c0 + i], 0.0f);
+    }
+    if constexpr (kMode == kFP8) {  // 16 e4m3 values: one 16-B unit of row ar
+      uint4 pk;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        w[i] = static_cast<uint32_t>(fp8x2(v[4 * i], v[4 * i + 1])) |
+               (static_cast<uint32_t>(fp8x2(v[4 * i + 2], v[4 * i + 3])) << 16);
+      *reinterpret_cast<uint4*>(a + ar * 128 + ((((k0 + c0) >> 4) ^ (ar & 7)) << 4)) = pk;
+    } else if constexpr (kMode == kBF16) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint4 pk;
@@ -425,7 +452,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   } else if (warp == 9) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t idesc = instr_desc(kMode == kBF16 ? 1 : 2, kC);
+      const uint32_t idesc = instr_desc(mode_fmt(kMode), kC);
       const uint32_t r1 = su32(R1), r2 = su32(R2);
       uint32_t n_a0 = 0, n_a1 = 0;
       int it = 0;
@@ -717,7 +744,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         // 16t + 2(m%8) + (m%16)/8) -> conv1 tile u, position 8*half + m%8, K half (m%16)/8
         const int t = 2 * u + half;
         restage_row<kMode>(R1, tmem + lane_off + t * kC, t >= T ? s_zacc : nullptr,
-                           (m >> 4) * 16 + conv1_slot(8 * half + (m & 7)), ((m >> 3) & 1) * kC, sbias[0]);
+                           (m >> 4) * 16 + conv1_slot(8 * half + (m & 7)), ((m >> 3) & 1) * kC, sbias[0],
+                           p.wscale[0]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&bar_a1);
@@ -740,7 +768,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         const int sl = m & 15;
         const int pair = sl < 8 ? sl : ((sl & 7) ^ 4);  // p / 2
         restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, (half == 1 && n_c1 == 1) ? s_c1 : nullptr,
-                           (m >> 4) * 16 + 8 * half + pair, (sl >> 3) * kC, sbias[1]);
+                           (m >> 4) * 16 + 8 * half + pair, (sl >> 3) * kC, sbias[1], p.wscale[1]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
@@ -779,10 +807,21 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         float v[16];
         tmem_ld16(tmem + lane_off + 384 + c0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
+        for (int i = 0; i < 16; ++i) {
+          if constexpr (kMode == kFP8) v[i] *= p.wscale[2];
+          v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
+        }
         if (sample < samples) {
           const uint64_t off = static_cast<uint64_t>(item) * (kItem * 16 * kC) + m * kC + c0;
-          if (kMode == kBF16) {
+          if constexpr (kMode == kFP8) {
+            uint4 pk;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              w[i] = static_cast<uint32_t>(fp8x2(v[4 * i], v[4 * i + 1])) |
+                     (static_cast<uint32_t>(fp8x2(v[4 * i + 2], v[4 * i + 3])) << 16);
+            *reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.out) + off) = pk;
+          } else if (kMode == kBF16) {
             uint4 pk[2];
             uint32_t* w = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
@@ -873,7 +912,9 @@ void launch_round_front(int mode, const CUtensorMap* w, const FrontParams& p, in
 #define SIMNET_FRONT(M, MU) \
   launch_pdl_tag("front", round_front_kernel<M, MU>, grid, dim3(kThreadsRF), sm, s, w[0], w[1], w[2], w[3], w[4], \
                  w[5], w[6], w[7], p)
-  if (mode == kBF16)
+  if (mode == kFP8)
+    multi ? SIMNET_FRONT(kFP8, true) : SIMNET_FRONT(kFP8, false);
+  else if (mode == kBF16)
     multi ? SIMNET_FRONT(kBF16, true) : SIMNET_FRONT(kBF16, false);
   else if (mode == kTF32)
     multi ? SIMNET_FRONT(kTF32, true) : SIMNET_FRONT(kTF32, false);
@@ -888,6 +929,8 @@ void round_front_set_attributes() {
   CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32x3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kBF16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kFP8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kFP8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   CUDA_OK(cudaFuncSetAttribute(round_front_kernel<kTF32x3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
 }

@@ -31,6 +31,7 @@ struct FrontParams {
   const float* b0;
   const float* b1;
   const float* b2;
+  float wscale[3];           // fp8: per-layer accumulator scale (1 / weight scale); 1 otherwise
   void* out;                 // flat [last-first][1024] (f32, or bf16 for the bf16 path)
   int32_t out_tma;           // f32 flat: staged in shared memory and TMA-stored through w[6]
   // optional: write the gathered input (exact f32 values) in the standard

@@ -6,7 +6,15 @@
 
 namespace simnet {
 
-enum TcMode : int { kBF16 = 0, kTF32 = 1, kTF32x3 = 2 };
+enum TcMode : int { kBF16 = 0, kTF32 = 1, kTF32x3 = 2, kFP8 = 3 };
+
+// Operand element bytes and elements per 128-B SWIZZLE_128B chunk per mode.
+// Every mode's MMA consumes 32 B of K per row per instruction: K = 8 (tf32),
+// 16 (bf16), 32 (fp8 e4m3).
+constexpr int mode_esz(int mode) { return mode == kBF16 ? 2 : (mode == kFP8 ? 1 : 4); }
+constexpr int mode_chunk_elems(int mode) { return 128 / mode_esz(mode); }
+// instruction-descriptor operand format: kind::f16 bf16 = 1, kind::tf32 = 2, kind::f8f6f4 E4M3 = 0
+constexpr int mode_fmt(int mode) { return mode == kBF16 ? 1 : (mode == kFP8 ? 0 : 2); }
 
 constexpr int kMaxChunks = 4;    // K chunks (128 B each) resident per CTA
 constexpr int kBM = 128;
@@ -96,7 +104,12 @@ __device__ __forceinline__ uint32_t instr_desc(int fmt, int n) {
 
 template <int kMode>
 __device__ __forceinline__ void mma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  if constexpr (kMode == kBF16) {
+  if constexpr (kMode == kFP8) {  // e4m3 x e4m3 -> f32 (idesc formats 0 = E4M3)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  } else if constexpr (kMode == kBF16) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),

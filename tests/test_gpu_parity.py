@@ -481,3 +481,25 @@ def test_gpu_trace_ingest_matches_host_path(gpu, port, golden, oracle):
         g.load_trace_file(str(path), pcfg(7), oracle=oracle, shard=shard)
         b = g.run(pcfg(7), oracle=oracle, shard=shard)
         assert np.array_equal(gpu_subs(a), gpu_subs(b))
+
+
+def test_fp8_fused_rounds(gpu, port):
+    """fp8 (e4m3 operands, tcgen05 kind::f8f6f4) runs the fused rounds; its CPI
+    error against the CPU oracle is reported (printed) and loosely bounded.
+    Teacher-forced predict and unfused rounds refuse fp8 with an error."""
+    g = gpu("fp8")
+    m, t = _bench_like("default", n=12_000)
+    g.load_model(m)
+    pc = pcfg(48)
+    g.load_trace(t, pc)
+    r = g.run(pc)
+    want = port.simulate(t, m, k=48)
+    err = (r.total_cycles - want["total_cycles"]) / want["total_cycles"]
+    same = float(np.mean(r.predicted_fetch == want["predicted_fetch"]))
+    print(f"fp8: total cycles {r.total_cycles} vs oracle {want['total_cycles']} ({100 * err:+.2f}%), "
+          f"{100 * same:.1f}% fetch latencies identical")
+    assert abs(err) < 0.25 and r.instructions == t.n
+    with pytest.raises(IlsimError):
+        g.run(pc, fused=False)
+    with pytest.raises(IlsimError):
+        g.predict(np.zeros((1, 50 * 111), np.float32), np.zeros(1, np.uint8))
