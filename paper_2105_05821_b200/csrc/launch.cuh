@@ -13,14 +13,16 @@
 namespace simnet {
 
 // Programmatic dependent launch per launch tag.  Default: the fused round's
-// front ("front") and its f32 FC1 ("layer") -- measured A/B on B200 at K=1024:
-// tf32x3 35.9 -> 34.2 us per round (both), bf16 24.0 -> 23.4 (front only; PDL
-// on the bf16 FC1, "layer_bf16", measured slower).  SIMNET_PDL overrides:
-// "0" = none, "1" / "all" = every launch, else a comma list of tags.
+// front ("front") and its FC1 ("layer": f32 modes, "layer_bf16": bf16 / fp8)
+// -- measured A/B on B200 at K=1024: tf32x3 35.9 -> 34.2 us per round (front +
+// layer); bf16 19.8 -> 18.9 and fp8 18.2 -> 17.3 with layer_bf16 (early in the
+// round it measured slower, before the FC1 epilogue became a TMA store).
+// SIMNET_PDL overrides: "0" = none, "1" / "all" = every launch, else a comma
+// list of tags.
 inline bool pdl_enabled(const char* tag) {
   static const char* env = std::getenv("SIMNET_PDL");
   const std::string t = tag ? tag : "";
-  if (!env) return t == "front" || t == "layer";
+  if (!env) return t == "front" || t == "layer" || t == "layer_bf16";
   const std::string e(env);
   if (e.empty() || e == "0") return false;
   if (e == "1" || e == "all") return true;

@@ -13,7 +13,7 @@ from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace  # noqa
 K = int(os.environ.get("K", "1024"))
 t = synthetic_trace(max(300_000, 300 * K), 101)
 m = synthetic_model(synthetic_trace(200_000, 101), 1)
-for prec in ("tf32x3", "bf16"):
+for prec in os.environ.get("PRECS", "tf32x3,bf16").split(","):
     g = GpuSimulator(0, prec)
     g.load_model(m)
     pc = ParallelConfig(k=K)

@@ -5,7 +5,7 @@ sys.path.insert(0, '/root/repo')
 from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, _lib
 from paper_2105_05821_b200.synth import synthetic_trace, synthetic_model
 N = int(os.environ.get("N", "300000")); t = synthetic_trace(N, 101); m = synthetic_model(synthetic_trace(200_000, 101), 1)
-for prec in ("tf32x3", "bf16"):
+for prec in os.environ.get("PRECS", "tf32x3,bf16").split(","):
     g = GpuSimulator(0, prec); g.load_model(m)
     pc = ParallelConfig(k=1024); g.load_trace(t, pc); g.run(pc)
     W = 148 * 32 + 256 * 32 + 148 * 16
