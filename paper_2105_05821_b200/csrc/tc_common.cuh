@@ -11,10 +11,10 @@ enum TcMode : int { kBF16 = 0, kTF32 = 1, kTF32x3 = 2, kFP8 = 3 };
 // Operand element bytes and elements per 128-B SWIZZLE_128B chunk per mode.
 // Every mode's MMA consumes 32 B of K per row per instruction: K = 8 (tf32),
 // 16 (bf16), 32 (fp8 e4m3).
-constexpr int mode_esz(int mode) { return mode == kBF16 ? 2 : (mode == kFP8 ? 1 : 4); }
-constexpr int mode_chunk_elems(int mode) { return 128 / mode_esz(mode); }
+__host__ __device__ constexpr int mode_esz(int mode) { return mode == kBF16 ? 2 : (mode == kFP8 ? 1 : 4); }
+__host__ __device__ constexpr int mode_chunk_elems(int mode) { return 128 / mode_esz(mode); }
 // instruction-descriptor operand format: kind::f16 bf16 = 1, kind::tf32 = 2, kind::f8f6f4 E4M3 = 0
-constexpr int mode_fmt(int mode) { return mode == kBF16 ? 1 : (mode == kFP8 ? 0 : 2); }
+__host__ __device__ constexpr int mode_fmt(int mode) { return mode == kBF16 ? 1 : (mode == kFP8 ? 0 : 2); }
 
 constexpr int kMaxChunks = 4;    // K chunks (128 B each) resident per CTA
 constexpr int kBM = 128;
