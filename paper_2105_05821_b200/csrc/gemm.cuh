@@ -21,8 +21,19 @@ struct LayerGemm {
   float* c;                // [m][ldc]
   int n, ldc;
   int relu;
+  float* splitk;           // scratch for the small-batch split-K path ([m][chunks][n] floats), or null
 };
 
+// K is accumulated in chunks of kSgemmChunk: each chunk's fma chain starts at
+// 0 (k ascending), and the chunk sums are added in order.  Every batch size
+// and both kernels below use this order, so results stay batch-independent.
+constexpr int kSgemmChunk = 512;
+constexpr uint64_t kSgemvMaxM = 8;  // batches up to this many rows take the split-K GEMV
+inline uint64_t sgemm_splitk_floats(uint64_t m, int kdim, int n) {
+  return m * static_cast<uint64_t>((kdim + kSgemmChunk - 1) / kSgemmChunk) * static_cast<uint64_t>(n);
+}
+
 void launch_sgemm(const LayerGemm& g, cudaStream_t stream);
+bool sgemm_two_launches(const LayerGemm& g);  // the split-K GEMV path (2 kernels)
 
 }  // namespace simnet

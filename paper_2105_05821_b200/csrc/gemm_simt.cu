@@ -33,7 +33,20 @@ __global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
 
   float acc[4][4] = {};
   float acp[4][4] = {};
+  float tot[4][4] = {};  // sum of the finished kSgemmChunk chunks (see gemm.cuh)
+  float tpp[4][4] = {};
   for (int k0 = 0; k0 < g.kdim; k0 += BK) {
+    if (k0 > 0 && k0 % kSgemmChunk == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          tot[i][j] += acc[i][j];
+          tpp[i][j] += acp[i][j];
+          acc[i][j] = 0.0f;
+          acp[i][j] = 0.0f;
+        }
+    }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int k = k0 + lk + t;
@@ -77,20 +90,66 @@ __global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
     for (int j = 0; j < 4; ++j) {
       const int n = col0 + tx + 16 * j;
       if (n >= g.n) continue;
-      float v = acc[i][j];
-      if (g.w2) v += acp[i][j];
+      float v = tot[i][j] + acc[i][j];
+      if (g.w2) v += tpp[i][j] + acp[i][j];
       v += g.bias[n];
       if (g.relu) v = fmaxf(v, 0.0f);
       g.c[r * g.ldc + n] = v;
     }
   }
 }
+// Small batches (the sequential / FC-only configurations): one thread per
+// (row, output), one CTA per (128 outputs, K chunk, row); the chunk's fma
+// chain as in sgemm_kernel, written to the scratch, then summed in chunk order.
+constexpr int kGv = 128;
+__global__ void __launch_bounds__(kGv) sgemv_chunk_kernel(LayerGemm g) {
+  __shared__ float as[kSgemmChunk];
+  const int n = blockIdx.x * kGv + threadIdx.x;
+  const int c = blockIdx.y;
+  const uint64_t r = blockIdx.z;
+  const int k0 = c * kSgemmChunk, k1 = min(g.kdim, k0 + kSgemmChunk);
+  const float* arow = g.a + r * g.sample_stride;
+  for (int k = k0 + threadIdx.x; k < k1; k += kGv) as[k - k0] = arow[k];
+  __syncthreads();
+  if (n >= g.n) return;
+  const float* w = g.w + static_cast<uint64_t>(k0) * g.n + n;
+  float acc = 0.0f;
+  int k = k0;
+#pragma unroll 8
+  for (; k < k1; ++k, w += g.n) acc = fmaf(as[k - k0], __ldg(w), acc);
+  const int chunks = gridDim.y;
+  g.splitk[(r * chunks + c) * g.n + n] = acc;
+}
+
+__global__ void __launch_bounds__(kGv) sgemv_reduce_kernel(LayerGemm g, int chunks) {
+  const int n = blockIdx.x * kGv + threadIdx.x;
+  const uint64_t r = blockIdx.y;
+  if (n >= g.n) return;
+  float tot = 0.0f;
+  for (int c = 0; c < chunks; ++c) tot += g.splitk[(r * chunks + c) * g.n + n];
+  float v = tot + g.bias[n];
+  if (g.relu) v = fmaxf(v, 0.0f);
+  g.c[r * g.ldc + n] = v;
+}
 }  // namespace
 
 void launch_sgemm(const LayerGemm& g, cudaStream_t stream) {
   if (g.m == 0) return;
+  if (g.splitk && g.m <= kSgemvMaxM && g.rows_per_sample == 1 && g.valid_rows == 1 && !g.w2 &&
+      g.kdim > kSgemmChunk) {
+    const int chunks = (g.kdim + kSgemmChunk - 1) / kSgemmChunk;
+    const unsigned gx = static_cast<unsigned>((g.n + kGv - 1) / kGv);
+    sgemv_chunk_kernel<<<dim3(gx, chunks, static_cast<unsigned>(g.m)), kGv, 0, stream>>>(g);
+    sgemv_reduce_kernel<<<dim3(gx, static_cast<unsigned>(g.m)), kGv, 0, stream>>>(g, chunks);
+    return;
+  }
   dim3 grid(static_cast<unsigned>((g.m + BM - 1) / BM), (g.n + BN - 1) / BN);
   sgemm_kernel<<<grid, 256, 0, stream>>>(g);
+}
+
+bool sgemm_two_launches(const LayerGemm& g) {
+  return g.splitk && g.m <= kSgemvMaxM && g.rows_per_sample == 1 && g.valid_rows == 1 && !g.w2 &&
+         g.kdim > kSgemmChunk;
 }
 
 }  // namespace simnet

@@ -159,8 +159,15 @@ ForwardBuffers forward_buffers(const DevModel& m, uint64_t chunk, DevBuf& act, D
   }
   off.push_back(floats);
   floats += chunk * static_cast<uint64_t>(c.fc_hidden);
+  floats = (floats + 63) & ~63ull;
+  const uint64_t sk_off = floats;
+  const bool sk = chunk <= kSgemvMaxM;  // sequential / tiny batches: split-K GEMV for the FC layers
+  if (sk)
+    floats += std::max(sgemm_splitk_floats(chunk, m.L.flat, c.fc_hidden),
+                       sgemm_splitk_floats(chunk, c.fc_hidden, m.L.out_dim));
   float* base = static_cast<float*>(act.need(floats * sizeof(float)));
   for (size_t i = 0; i < off.size(); ++i) fb.act[i] = base + off[i];
+  fb.splitk = sk ? base + sk_off : nullptr;
   fb.y_stride = static_cast<uint32_t>(m.L.out_dim);
   fb.y = static_cast<float*>(y.need(chunk * fb.y_stride * sizeof(float)));
   if (m.tc) tc_prepare(m, chunk);
@@ -181,6 +188,7 @@ ForwardBuffers fb_slice(const DevModel& m, const ForwardBuffers& fb, uint64_t of
   s.act[c.n_conv] = fb.act[c.n_conv] + off * static_cast<uint64_t>(c.fc_hidden);
   s.y = fb.y + off * fb.y_stride;
   s.part_off = fb.part_off + off;
+  if (off > 0) s.splitk = nullptr;  // one scratch: only the first slice may use it
   return s;
 }
 
@@ -237,6 +245,7 @@ uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32
   f1.n = c.fc_hidden;
   f1.ldc = c.fc_hidden;
   f1.relu = 1;
+  f1.splitk = fb.splitk;
   launch_sgemm(f1, s);
   LayerGemm f2{};
   f2.a = fb.act[c.n_conv];
@@ -251,8 +260,9 @@ uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32
   f2.n = m.L.out_dim;
   f2.ldc = static_cast<int>(fb.y_stride);
   f2.relu = 0;
+  f2.splitk = fb.splitk;
   launch_sgemm(f2, s);
-  return launches + 2;
+  return launches + (sgemm_two_launches(f1) ? 2 : 1) + (sgemm_two_launches(f2) ? 2 : 1);
 }
 
 }  // namespace simnet

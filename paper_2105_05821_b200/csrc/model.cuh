@@ -57,6 +57,7 @@ struct ForwardBuffers {
   uint32_t y_stride;
   uint32_t act_esz;    // bytes per conv activation element (2: bf16 tensor-core path)
   uint64_t part_off;   // first sample of this slice in the split-K partial buffer
+  float* splitk;       // fp32 SIMT small-batch split-K scratch (null: tiled kernel only)
 };
 
 void model_upload(DevModel& m, const ilsim_cnn_config& c, const float* params, int precision,
