@@ -5,6 +5,7 @@ timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_tf32x3.log 2>&1; tail -1 gpurun_out/bench_tf32x3.log
 timeout 600 python bench.py --precision bf16 --no-cpu-baseline > gpurun_out/bench_bf16.log 2>&1; tail -1 gpurun_out/bench_bf16.log
+timeout 600 python bench.py --precision fp8 --no-cpu-baseline > gpurun_out/bench_fp8.log 2>&1; tail -1 gpurun_out/bench_fp8.log
 timeout 600 python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1; tail -1 gpurun_out/bench_reference.log
 for P in tf32x3 bf16; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 200 --csv \
