@@ -62,6 +62,27 @@ def test_struct_layouts_match_header(tmp_path):
             assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)
 
 
+def test_precision_enum_matches_header(tmp_path):
+    """_lib.PREC (the Python names) mirrors the header's ILSIM_PREC_* values."""
+    import shutil
+    import subprocess
+
+    from paper_2105_05821_b200._lib import PREC
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc unavailable")
+    names = {"fp32": "ILSIM_PREC_FP32", "tf32x3": "ILSIM_PREC_TF32X3", "tf32": "ILSIM_PREC_TF32",
+             "bf16": "ILSIM_PREC_BF16", "fp8": "ILSIM_PREC_FP8"}
+    assert set(PREC) == set(names)
+    src = tmp_path / "prec.c"
+    src.write_text('#include <stdio.h>\n#include "ilsim_gpu.h"\nint main(void){' +
+                   "".join(f'printf("{k} %d\\n", {v});' for k, v in names.items()) + "return 0;}")
+    exe = tmp_path / "prec"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    assert {k: int(v) for k, v in got.items()} == PREC
+
+
 def test_host_helpers_without_gpu(L, port):
     from paper_2105_05821_b200 import api
 
