@@ -263,11 +263,15 @@ class GpuSimulator:
         return n
 
     def run(self, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None, profile=False,
-            truth_inputs=False, n_total: int | None = None, fused=True) -> ParallelResult:
+            truth_inputs=False, n_total: int | None = None, fused=True,
+            fetch_out: np.ndarray | None = None) -> ParallelResult:
         """Round loop over the loaded trace.  ``truth_inputs``: test hook, truth
         latencies with the input tensor still gathered (for input capture).
         ``fused=False`` forces the unfused tensor-core round (separate K1
-        kernel + TMA conv chain) instead of the fused round front (A/B checks)."""
+        kernel + TMA conv chain) instead of the fused round front (A/B checks).
+        ``fetch_out``: caller-owned uint32 buffer (at least the owned
+        instruction count) for the predicted fetch series, as the C-ABI's
+        caller-allocated output; the result's series are views into it."""
         cfg = self._sim_cfg(pc, sequential=sequential, oracle=oracle or truth_inputs, shard=shard,
                             profile=profile, truth_inputs=truth_inputs, fused=fused)
         n = self._trace_n if n_total is None else n_total
@@ -280,7 +284,14 @@ class GpuSimulator:
         starts = partition_starts(n, k) if n > 0 else [0]
         own0 = starts[sb] if n > 0 else 0
         own1 = (starts[se] if se < k else n) if n > 0 else 0
-        pf = np.zeros(max(own1 - own0, 1), dtype=np.uint32) if pc.sim.record_fetch else None
+        if not pc.sim.record_fetch:
+            pf = None
+        elif fetch_out is not None:
+            if fetch_out.dtype != np.uint32 or not fetch_out.flags.c_contiguous or fetch_out.size < own1 - own0:
+                raise IlsimError("fetch_out must be a contiguous uint32 array of at least the owned instruction count")
+            pf = fetch_out
+        else:
+            pf = np.zeros(max(own1 - own0, 1), dtype=np.uint32)
         tot = _lib.Totals()
         self._check(self.L.ilsim_gpu_run(self._h, C.byref(cfg), subs, nsub,
                                          pf.ctypes.data if pf is not None else None, C.byref(tot)))
@@ -319,11 +330,11 @@ class GpuSimulator:
                               float(tot.device_ms), tuple(tot.kernel_ms), int(tot.launches), int(tot.rounds))
 
     def simulate_parallel(self, trace: Trace, pc: ParallelConfig | None = None, *, oracle=False,
-                          shard=None) -> ParallelResult:
+                          shard=None, fetch_out: np.ndarray | None = None) -> ParallelResult:
         """``simulate_parallel`` (parallel.cpp:26-93)."""
         pc = pc or ParallelConfig()
         self.load_trace(trace, pc, oracle=oracle, shard=shard, truth=oracle)
-        return self.run(pc, oracle=oracle, shard=shard)
+        return self.run(pc, oracle=oracle, shard=shard, fetch_out=fetch_out)
 
     def simulate_trace(self, trace: Trace, sim: SimConfig | None = None, *, oracle=False) -> SimResult:
         """``simulate_trace`` (simcore.cpp:185-196)."""

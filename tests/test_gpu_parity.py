@@ -503,3 +503,21 @@ def test_fp8_fused_rounds(gpu, port):
         g.run(pc, fused=False)
     with pytest.raises(IlsimError):
         g.predict(np.zeros((1, 50 * 111), np.float32), np.zeros(1, np.uint8))
+
+
+def test_run_into_caller_fetch_buffer(gpu, port, golden):
+    """run(fetch_out=...) writes the predicted fetch series into a caller-owned
+    buffer (the C-ABI contract), with the same values as a fresh array."""
+    g = gpu("tf32x3")
+    m, _ = _fused_cases(port, golden)
+    g.load_model(m)
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    pc = pcfg(5)
+    g.load_trace(t, pc)
+    a = g.run(pc)
+    buf = np.full(t.n + 7, 0xDEADBEEF, np.uint32)
+    b = g.run(pc, fetch_out=buf)
+    assert np.array_equal(a.predicted_fetch, b.predicted_fetch) and np.array_equal(buf[:t.n], a.predicted_fetch)
+    assert np.all(buf[t.n:] == 0xDEADBEEF)
+    with pytest.raises(IlsimError):
+        g.run(pc, fetch_out=np.zeros(t.n, np.int64))
