@@ -264,7 +264,7 @@ class GpuSimulator:
 
     def run(self, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None, profile=False,
             truth_inputs=False, n_total: int | None = None, fused=True,
-            fetch_out: np.ndarray | None = None) -> ParallelResult:
+            fetch_out: np.ndarray | None = None, _view=None) -> ParallelResult:
         """Round loop over the loaded trace.  ``truth_inputs``: test hook, truth
         latencies with the input tensor still gathered (for input capture).
         ``fused=False`` forces the unfused tensor-core round (separate K1
@@ -293,8 +293,13 @@ class GpuSimulator:
         else:
             pf = np.zeros(max(own1 - own0, 1), dtype=np.uint32)
         tot = _lib.Totals()
-        self._check(self.L.ilsim_gpu_run(self._h, C.byref(cfg), subs, nsub,
-                                         pf.ctypes.data if pf is not None else None, C.byref(tot)))
+        if _view is not None:  # one C call: upload (overlapped with the rounds when large) + rounds
+            self._check(self.L.ilsim_gpu_simulate_parallel(self._h, C.byref(_view), C.byref(cfg), subs, nsub,
+                                                           pf.ctypes.data if pf is not None else None,
+                                                           C.byref(tot)))
+        else:
+            self._check(self.L.ilsim_gpu_run(self._h, C.byref(cfg), subs, nsub,
+                                             pf.ctypes.data if pf is not None else None, C.byref(tot)))
         return self._collect(subs, int(tot.sub_traces), pf, own1 - own0, tot, starts, sb, pc)
 
     @staticmethod
@@ -331,10 +336,14 @@ class GpuSimulator:
 
     def simulate_parallel(self, trace: Trace, pc: ParallelConfig | None = None, *, oracle=False,
                           shard=None, fetch_out: np.ndarray | None = None) -> ParallelResult:
-        """``simulate_parallel`` (parallel.cpp:26-93)."""
+        """``simulate_parallel`` (parallel.cpp:26-93): one ``ilsim_gpu_simulate_parallel``
+        call, which overlaps the trace upload with the rounds on large traces."""
         pc = pc or ParallelConfig()
-        self.load_trace(trace, pc, oracle=oracle, shard=shard, truth=oracle)
-        return self.run(pc, oracle=oracle, shard=shard, fetch_out=fetch_out)
+        view, keep = trace_view(trace, with_truth=oracle)
+        self._trace_n = trace.n
+        r = self.run(pc, oracle=oracle, shard=shard, fetch_out=fetch_out, _view=view)
+        del keep
+        return r
 
     def simulate_trace(self, trace: Trace, sim: SimConfig | None = None, *, oracle=False) -> SimResult:
         """``simulate_trace`` (simcore.cpp:185-196)."""

@@ -114,6 +114,12 @@ struct ilsim_gpu_ctx {
   DevBuf state, proc, wq, x, y, act, pred_fetch;
   DevBuf rec_stage;  // SNT1 record staging for the GPU trace ingest
 
+  // simulate_parallel with the trace upload overlapped with the rounds: the
+  // borrowed host view, uploaded window by window on copy_stream
+  const ilsim_trace_view* deferred = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> win_ev;
+
   // capture hook
   uint32_t cap_round = UINT32_MAX;
   float* cap_host = nullptr;
@@ -215,8 +221,81 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     st.count_drain = (cfg.drain_trim && i + 1 < P.k) ? 0u : 1u;
     rounds = std::max(rounds, st.len);
   }
-  if (needs_input) pack_if_needed(c, true);
-  else if (c->packed_gen == ~0ull || c->iflags.bytes < (P.g1 - P.g0)) pack_if_needed(c, false);
+  // Overlapped upload (simulate_parallel): round r reads trace position r of
+  // every sub-trace (and older ones), so the trace goes up in windows of
+  // positions, each copied (2-D copies over runs of equal-length sub-traces)
+  // and packed on copy_stream while earlier windows' rounds run.
+  uint32_t win_rounds = 0, n_win = 0;
+  if (c->deferred) {
+    win_rounds = std::max<uint32_t>(16, ((rounds + 15) / 16 + 15) / 16 * 16);
+    n_win = (rounds + win_rounds - 1) / win_rounds;
+    struct Group { uint64_t first_begin, stride, count; uint32_t len; };
+    std::vector<Group> groups;
+    for (uint64_t j = 0; j < K; ++j) {
+      const SubState& st = hs[j];
+      if (!groups.empty()) {
+        Group& g = groups.back();
+        const uint64_t stride = g.count == 1 ? st.begin - g.first_begin : g.stride;
+        if (st.len == g.len && st.begin == g.first_begin + g.count * stride && stride >= win_rounds) {
+          g.stride = stride;
+          ++g.count;
+          continue;
+        }
+      }
+      groups.push_back(Group{st.begin, static_cast<uint64_t>(win_rounds), 1, st.len});
+    }
+    while (c->win_ev.size() < n_win) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->win_ev.push_back(e);
+    }
+    const ilsim_trace_view* t = c->deferred;
+    auto copy2d = [&](void* dev, const void* host, size_t esz, const Group& g, uint64_t p0, uint64_t len) {
+      const size_t pitch = g.stride * esz, width = len * esz;
+      CUDA_OK(cudaMemcpy2DAsync(static_cast<char*>(dev) + (g.first_begin + p0) * esz, pitch,
+                                static_cast<const char*>(host) + (P.g0 + g.first_begin + p0) * esz, pitch, width,
+                                g.count, cudaMemcpyHostToDevice, c->copy_stream));
+    };
+    CUDA_OK(cudaEventRecord(c->ev[6], c->stream));  // buffers free of earlier users
+    CUDA_OK(cudaStreamWaitEvent(c->copy_stream, c->ev[6], 0));
+    for (uint32_t w = 0; w < n_win; ++w) {
+      const uint64_t p0 = static_cast<uint64_t>(w) * win_rounds;
+      for (const Group& g : groups) {
+        if (g.len <= p0) continue;
+        const uint64_t len = std::min<uint64_t>(win_rounds, g.len - p0);
+        copy2d(c->pc.p, t->pc, 8, g, p0, len);
+        copy2d(c->addr.p, t->data_addr, 8, g, p0, len);
+        copy2d(c->op.p, t->op, 13, g, p0, len);
+        copy2d(c->src.p, t->src, 16, g, p0, len);
+        copy2d(c->dst.p, t->dst, 12, g, p0, len);
+        copy2d(c->hist.p, t->hist, 28, g, p0, len);
+        PackParams pp{};
+        pp.n = g.count * len;
+        pp.op = c->op.as<uint8_t>();
+        pp.src = c->src.as<uint16_t>();
+        pp.dst = c->dst.as<uint16_t>();
+        pp.hist = c->hist.as<uint16_t>();
+        pp.nc = c->nc_dev.as<NormConsts>();
+        pp.stat = c->stat.as<float>();
+        pp.iflags = c->iflags.as<uint8_t>();
+        pp.seg_first = g.first_begin + p0;
+        pp.seg_stride = g.stride;
+        pp.seg_len = len;
+        launch_pack(pp, c->copy_stream);
+      }
+      CUDA_OK(cudaEventRecord(c->win_ev[w], c->copy_stream));
+    }
+    CUDA_OK(cudaGetLastError());
+  } else if (needs_input) {
+    pack_if_needed(c, true);
+  } else if (c->packed_gen == ~0ull || c->iflags.bytes < (P.g1 - P.g0)) {
+    pack_if_needed(c, false);
+  }
+  uint32_t win_waited = 0;
+  auto wait_windows = [&](uint32_t upto_round) {  // windows holding positions < upto_round
+    while (win_waited < n_win && static_cast<uint64_t>(win_waited) * win_rounds < upto_round)
+      CUDA_OK(cudaStreamWaitEvent(c->stream, c->win_ev[win_waited++], 0));
+  };
 
   SubState* d_state = static_cast<SubState*>(c->state.need(K * sizeof(SubState)));
   CUDA_OK(cudaMemcpyAsync(d_state, hs.data(), K * sizeof(SubState), cudaMemcpyHostToDevice, c->stream));
@@ -455,15 +534,18 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   } else {
     uint32_t r = 0;
     while (gN && r + kGraphRounds <= rounds) {
+      wait_windows(r + kGraphRounds);
       CUDA_OK(cudaGraphLaunch(gN, c->stream));
       launches += launches_n;
       r += kGraphRounds;
     }
     for (; r < rounds; ++r) {
+      wait_windows(r + 1);
       CUDA_OK(cudaGraphLaunch(g1, c->stream));
       launches += launches_1;
     }
   }
+  wait_windows(UINT32_MAX);
   for (uint64_t f = 0; f < K; f += chunk) {  // apply final step, drain
     const uint64_t l = std::min(K, f + chunk);
     if (fused) {
@@ -623,6 +705,11 @@ void ilsim_gpu_destroy(ilsim_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->win_ev) cudaEventDestroy(e);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -714,8 +801,47 @@ int ilsim_gpu_run(ilsim_gpu_ctx* c, const ilsim_sim_config* cfg, ilsim_sub_resul
 int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, const ilsim_sim_config* cfg,
                                 ilsim_sub_result* subs, uint64_t sub_cap, uint32_t* predicted_fetch,
                                 ilsim_totals* totals) {
-  if (ilsim_gpu_load_trace(c, t, cfg) != 0) return 1;
-  return ilsim_gpu_run(c, cfg, subs, sub_cap, predicted_fetch, totals);
+  // Large model-driven runs upload the trace window by window, overlapped
+  // with the rounds (one call borrows the view for its whole duration).
+  const bool overlap = c && t && cfg && c->has_model && cfg->oracle == 0 && t->truth == nullptr &&
+                       cfg->reserved[0] == 0 && cfg->reserved[1] == 0 && c->cap_round == UINT32_MAX &&
+                       cfg->shard_begin == 0 && (cfg->shard_end == 0) && t->n >= (1ull << 20) &&
+                       !std::getenv("SIMNET_NO_UPLOAD_OVERLAP");
+  if (!overlap) {
+    if (ilsim_gpu_load_trace(c, t, cfg) != 0) return 1;
+    return ilsim_gpu_run(c, cfg, subs, sub_cap, predicted_fetch, totals);
+  }
+  const int rc = guard(c, [&] {
+    const Plan P = make_plan(*cfg, t->n);
+    c->has_trace = false;
+    c->t_total = t->n;
+    c->g0 = P.g0;
+    c->g1 = P.g1;
+    const uint64_t m = P.g1 - P.g0;
+    c->pc.need(m * 8);
+    c->addr.need(m * 8);
+    c->op.need(m * 13);
+    c->src.need(m * 16);
+    c->dst.need(m * 12);
+    c->hist.need(m * 28);
+    c->has_truth = false;
+    c->iflags.need(m);
+    c->stat.need(m * kStatStride * sizeof(float));
+    c->packed_gen = c->model_gen;  // packed window by window in run_impl
+    c->has_trace = true;
+    if (!c->copy_stream) CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    c->deferred = t;
+    try {
+      run_impl(c, *cfg, subs, sub_cap, predicted_fetch, totals);
+    } catch (...) {
+      c->deferred = nullptr;
+      c->packed_gen = ~0ull;  // the static table may be partial
+      cudaStreamSynchronize(c->copy_stream);
+      throw;
+    }
+    c->deferred = nullptr;
+  });
+  return rc;
 }
 
 int ilsim_gpu_predict(ilsim_gpu_ctx* c, const float* inputs, uint64_t n, const uint8_t* is_store,

@@ -192,8 +192,9 @@ __global__ void decode_only_kernel(const float* y, int y_stride, uint64_t n, con
 // Pack: normalise the 41 static slots once per instruction and derive flags.
 // ---------------------------------------------------------------------------
 __global__ void pack_kernel(PackParams p) {
-  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
-  if (i >= p.n) return;
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  if (t >= p.n) return;
+  const uint64_t i = p.seg_len ? p.seg_first + (t / p.seg_len) * p.seg_stride + t % p.seg_len : t;
   const uint32_t k = threadIdx.x;  // 0..63
   if (k < kStatic && p.stat) {
     int32_t raw;

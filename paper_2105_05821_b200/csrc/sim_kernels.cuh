@@ -55,6 +55,9 @@ struct PackParams {
   const NormConsts* nc;
   float* stat;               // may be null (oracle mode)
   uint8_t* iflags;
+  // segmented mode (seg_len > 0): instructions seg_first + s * seg_stride + o,
+  // s < n / seg_len, o < seg_len (one window of equal-length sub-traces)
+  uint64_t seg_first, seg_stride, seg_len;
 };
 
 void launch_ctx(const CtxParams& p, cudaStream_t stream);

@@ -521,3 +521,20 @@ def test_run_into_caller_fetch_buffer(gpu, port, golden):
     assert np.all(buf[t.n:] == 0xDEADBEEF)
     with pytest.raises(IlsimError):
         g.run(pc, fetch_out=np.zeros(t.n, np.int64))
+
+
+@pytest.mark.parametrize("extra", [dict(), dict(warmup=200, drain_trim=True), dict(k=3000)])
+def test_overlapped_upload_matches_load_then_run(gpu, extra):
+    """simulate_parallel on a large trace uploads it window by window (2-D
+    copies over runs of equal-length sub-traces, packed per window) while the
+    rounds run; results equal a full upload followed by the rounds, bit for bit."""
+    from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace
+    g = gpu("tf32x3")
+    m = synthetic_model(synthetic_trace(20_000, 101), 1)
+    g.load_model(m)
+    t = synthetic_trace(1_100_000, 7)
+    pc = pcfg(extra.get("k", 1024), warmup=extra.get("warmup", 0), drain_trim=extra.get("drain_trim", False))
+    a = g.simulate_parallel(t, pc)
+    g.load_trace(t, pc)
+    b = g.run(pc)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)

@@ -26,3 +26,11 @@ for rep in range(6):
     t2 = time.perf_counter()
     print(f"load_trace {1e3 * (t1 - t0):7.1f} ms | run {1e3 * (t2 - t1):7.1f} ms (device {r.device_ms:7.1f} ms) | "
           f"total {1e3 * (t2 - t0):7.1f} ms -> {n / (t2 - t0) / 1e6:.2f} MIPS {'(pinned fetch_out)' if out is not None else ''}")
+
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = g.simulate_parallel(pt, pc, fetch_out=fetch)
+    t1 = time.perf_counter()
+    print(f"simulate_parallel (overlapped upload) {1e3 * (t1 - t0):7.1f} ms -> {n / (t1 - t0) / 1e6:.2f} MIPS, "
+          f"cycles {r.total_cycles}")
