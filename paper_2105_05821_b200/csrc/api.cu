@@ -805,7 +805,7 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, con
   // with the rounds (one call borrows the view for its whole duration).
   const bool overlap = c && t && cfg && c->has_model && cfg->oracle == 0 && t->truth == nullptr &&
                        cfg->reserved[0] == 0 && cfg->reserved[1] == 0 && c->cap_round == UINT32_MAX &&
-                       cfg->shard_begin == 0 && (cfg->shard_end == 0) && t->n >= (1ull << 20) &&
+                       t->n >= (1ull << 20) &&
                        !std::getenv("SIMNET_NO_UPLOAD_OVERLAP");
   if (!overlap) {
     if (ilsim_gpu_load_trace(c, t, cfg) != 0) return 1;

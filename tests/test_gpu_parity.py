@@ -523,7 +523,8 @@ def test_run_into_caller_fetch_buffer(gpu, port, golden):
         g.run(pc, fetch_out=np.zeros(t.n, np.int64))
 
 
-@pytest.mark.parametrize("extra", [dict(), dict(warmup=200, drain_trim=True), dict(k=3000)])
+@pytest.mark.parametrize("extra", [dict(), dict(warmup=200, drain_trim=True), dict(k=3000),
+                                   dict(shard=(300, 900), warmup=50)])
 def test_overlapped_upload_matches_load_then_run(gpu, extra):
     """simulate_parallel on a large trace uploads it window by window (2-D
     copies over runs of equal-length sub-traces, packed per window) while the
@@ -534,7 +535,8 @@ def test_overlapped_upload_matches_load_then_run(gpu, extra):
     g.load_model(m)
     t = synthetic_trace(1_100_000, 7)
     pc = pcfg(extra.get("k", 1024), warmup=extra.get("warmup", 0), drain_trim=extra.get("drain_trim", False))
-    a = g.simulate_parallel(t, pc)
-    g.load_trace(t, pc)
-    b = g.run(pc)
+    shard = extra.get("shard")
+    a = g.simulate_parallel(t, pc, shard=shard)
+    g.load_trace(t, pc, shard=shard, truth=False)
+    b = g.run(pc, shard=shard)
     assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
