@@ -835,7 +835,8 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, con
       run_impl(c, *cfg, subs, sub_cap, predicted_fetch, totals);
     } catch (...) {
       c->deferred = nullptr;
-      c->packed_gen = ~0ull;  // the static table may be partial
+      c->packed_gen = ~0ull;  // the device trace may be partial: it must be loaded again
+      c->has_trace = false;
       cudaStreamSynchronize(c->copy_stream);
       throw;
     }
