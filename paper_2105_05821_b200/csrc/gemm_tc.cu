@@ -168,14 +168,15 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int q = 0; q < 8; ++q)
         *reinterpret_cast<float4*>(stg + ((q ^ (r & 7)) << 4)) =
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      // this column group's box goes out while the next group is staged
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0)
+        tma_store_3d(&tmOut, sA + (c0 >> 5) * kAChunk + quad * 32 * 128, ntile * p.n + c0, t * kBM + quad * 32, ks);
     }
     if (stamp) tr[17] = clock64();  // staged
-    fence_async_smem();
-    __syncwarp();
     if (stamp) tr[18] = clock64();  // fenced
     if (lane == 0) {
-      for (int c0 = cb; c0 < ce; c0 += 32)
-        tma_store_3d(&tmOut, sA + (c0 >> 5) * kAChunk + quad * 32 * 128, ntile * p.n + c0, t * kBM + quad * 32, ks);
       bulk_commit();
       if (stamp) tr[19] = clock64();  // stores issued
       bulk_wait_read();  // staging read; the stores complete with the grid (dependents wait for it)
