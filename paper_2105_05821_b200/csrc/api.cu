@@ -447,13 +447,20 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     return do_ctx(f, l, true, off, st) + do_forward(f, l, off, fbs, st) + do_decode(f, l, fbs, st);
   };
 
-  constexpr uint32_t kGraphRounds = 16;
+  // rounds per CUDA graph: consecutive graph launches are not PDL-chained, so
+  // longer graphs amortise that gap (SIMNET_GRAPH_ROUNDS overrides, tests / A/B)
+  const uint32_t kGraphRounds = [] {
+    const char* e = std::getenv("SIMNET_GRAPH_ROUNDS");
+    const long v = e ? std::atol(e) : 16;
+    return static_cast<uint32_t>(v >= 2 && v <= 1024 ? v : 16);
+  }();
   auto launch_rounds = [&](uint32_t reps) -> uint64_t {
     uint64_t launches = 0;
     for (uint32_t r = 0; r < reps; ++r) {
       // SIMNET_CHAIN_TRACE: with a 16-round graph, only its middle round is
       // traced, so the buffer ends up holding a typical round (not the last)
-      chain_trace_on() = rounds < kGraphRounds || (reps > 1 && (r == reps / 2 || r == reps / 2 + 1));
+      const bool traced_graph = rounds < kGraphRounds || reps == kGraphRounds;  // not the tail graph
+      chain_trace_on() = traced_graph && (reps == 1 || r == reps / 2 || r == reps / 2 + 1);
       chain_trace_slot() = reps > 1 && r == reps / 2 + 1 ? 1 : 0;
       for (uint64_t f = 0; f < K; f += chunk) launches += run_span(f, std::min(K, f + chunk), 0, c->stream);
     }
@@ -465,12 +472,15 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
   if (capture_mode && !fused && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
   const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs
+  // graphs: gN = kGraphRounds rounds (replayed), g1 = the remaining
+  // rounds % kGraphRounds in one launch (graph boundaries are not PDL-chained)
   cudaGraphExec_t g1 = nullptr, gN = nullptr;
   uint64_t launches_1 = 0, launches_n = 0;
+  const uint32_t tail_rounds = rounds % kGraphRounds;
   if (!capture_mode && !profile) {
     for (int which = 0; which < 2; ++which) {
-      const uint32_t reps = which == 0 ? 1 : kGraphRounds;
-      if (which == 1 && rounds < kGraphRounds) break;
+      const uint32_t reps = which == 0 ? tail_rounds : kGraphRounds;
+      if (reps == 0 || (which == 1 && rounds < kGraphRounds)) continue;
       cudaGraph_t g = nullptr;
       CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       try {
@@ -539,10 +549,11 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
       launches += launches_n;
       r += kGraphRounds;
     }
-    for (; r < rounds; ++r) {
-      wait_windows(r + 1);
+    if (r < rounds) {  // the tail, one launch
+      wait_windows(rounds);
       CUDA_OK(cudaGraphLaunch(g1, c->stream));
       launches += launches_1;
+      r = rounds;
     }
   }
   wait_windows(UINT32_MAX);
