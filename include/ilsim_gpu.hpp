@@ -9,6 +9,7 @@
 // rethrown as ilsim::Error with the library's message.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <span>
 #include <string>
@@ -16,6 +17,7 @@
 
 #include "ilsim/cnn.hpp"
 #include "ilsim/parallel.hpp"
+#include "ilsim/predictor.hpp"
 #include "ilsim_gpu.h"
 
 namespace ilsim::gpu {
@@ -105,6 +107,22 @@ public:
     return out;
   }
 
+  // CnnPredictor::predict (predictor.cpp:13-29) on the GPU: inference + hybrid
+  // decode of the requests' inputs (PredictRequest::input layout).
+  void predict(std::span<const PredictRequest> requests, std::span<LatencyTriple> out) {
+    if (out.size() != requests.size()) throw Error("predict: output span size differs from the requests");
+    const size_t width = static_cast<size_t>(FeatureLayout::kSlots) * static_cast<size_t>(max_context_ + 1);
+    std::vector<float> in(requests.size() * width);
+    std::vector<uint8_t> st(requests.size());
+    for (size_t i = 0; i < requests.size(); ++i) {
+      std::copy(requests[i].input, requests[i].input + width, in.begin() + static_cast<std::ptrdiff_t>(i * width));
+      st[i] = requests[i].target_is_store ? 1 : 0;
+    }
+    std::vector<uint32_t> tri(requests.size() * 3);
+    if (!requests.empty()) check(ilsim_gpu_predict(ctx_, in.data(), requests.size(), st.data(), nullptr, tri.data()));
+    for (size_t i = 0; i < requests.size(); ++i) out[i] = LatencyTriple{tri[3 * i], tri[3 * i + 1], tri[3 * i + 2]};
+  }
+
 private:
   struct Soa {  // AnnotatedInstruction (trace.hpp:98-109) -> structure of arrays
     std::vector<uint64_t> pc, addr;
@@ -156,5 +174,26 @@ inline ParallelResult simulate_parallel_gpu(std::span<const AnnotatedInstruction
   ctx.load_model(w);
   return ctx.simulate_parallel(trace, config);
 }
+
+// Secondary drop-in behind the reference's plugin interface
+// (LatencyPredictor, predictor.hpp:19-29): CnnPredictor with K2 + decode on
+// the GPU, for callers that keep the reference's host round loop
+// (teacher-forced use, simcore.cpp:185-196 with a GPU predictor).
+class CudaCnnPredictor final : public LatencyPredictor {
+public:
+  explicit CudaCnnPredictor(ModelWeights weights, int device = 0, int precision = ILSIM_PREC_TF32X3)
+      : weights_(std::move(weights)), ctx_(device, precision) {
+    ctx_.load_model(weights_);
+  }
+  int max_context() const override { return weights_.config.max_context; }
+  const NormStats* norm_stats() const override { return &weights_.norm; }
+  void predict(std::span<const PredictRequest> requests, std::span<LatencyTriple> out) override {
+    ctx_.predict(requests, out);
+  }
+
+private:
+  ModelWeights weights_;
+  Context ctx_;
+};
 
 }  // namespace ilsim::gpu

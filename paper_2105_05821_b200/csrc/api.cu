@@ -814,7 +814,8 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, con
                                 ilsim_totals* totals) {
   // Large model-driven runs upload the trace window by window, overlapped
   // with the rounds (one call borrows the view for its whole duration).
-  const bool overlap = c && t && cfg && c->has_model && cfg->oracle == 0 && t->truth == nullptr &&
+  // (truth latencies, if present in the view, are not needed by a model-driven run)
+  const bool overlap = c && t && cfg && c->has_model && cfg->oracle == 0 &&
                        cfg->reserved[0] == 0 && cfg->reserved[1] == 0 && c->cap_round == UINT32_MAX &&
                        t->n >= (1ull << 20) &&
                        !std::getenv("SIMNET_NO_UPLOAD_OVERLAP");
