@@ -254,6 +254,10 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   // One barrier per event kind; each waiter consumes every completion in order.
   __shared__ __align__(8) uint64_t bar_w[3];       // layer weights landed (TMA tx), 1 / item
   __shared__ __align__(8) uint64_t bar_a0, bar_t0; // conv0 tile gathered (256) / its MMAs done: T / item
+  // f32 modes: conv0 tile K chunk c (32 floats) written; the MMAs of a chunk
+  // start while later chunks are still being stored.  Writers: chunk 0 the
+  // even-column threads (K 0-49), 1 both, 2-3 the odd-column threads (K 50-103)
+  __shared__ __align__(8) uint64_t bar_a0c[4];
   __shared__ __align__(8) uint64_t bar_c0;         // all conv0 MMAs done (W0 + conv0 A free), 1 / item
   __shared__ __align__(8) uint64_t bar_a1, bar_m1; // conv1 A restaged / its MMAs done: 2 / item
   __shared__ __align__(8) uint64_t bar_w1f;        // conv1 MMAs done (W1 free), 1 / item
@@ -304,6 +308,10 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
   if (threadIdx.x == 0) {
     for (int i = 0; i < 3; ++i) mbar_init(&bar_w[i], 1);
     mbar_init(&bar_a0, kCompute);
+    mbar_init(&bar_a0c[0], kCompute / 2);
+    mbar_init(&bar_a0c[1], kCompute);
+    mbar_init(&bar_a0c[2], kCompute / 2);
+    mbar_init(&bar_a0c[3], kCompute / 2);
     mbar_init(&bar_t0, 1);
     mbar_init(&bar_c0, 1);
     mbar_init(&bar_a1, kCompute);
@@ -472,17 +480,46 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       };
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         // conv0: T tiles of 128 rows (8 samples x 16 rows), gathered by the compute warps
-        mbar_wait(&bar_a0, n_a0++ & 1);
-        const int T = s_T;  // written before the first bar_a0 arrival of this item
-        mbar_wait(&bar_w[0], it & 1);
-        tc_fence_after();
-        for (int t = 0; t < T; ++t) {
-          if (t > 0) {
-            mbar_wait(&bar_a0, n_a0++ & 1);
-            tc_fence_after();
+        int T;
+        if constexpr (S::kK0Chunks == 4) {  // f32 modes: per-K-chunk readiness
+          mbar_wait(&bar_a0c[0], n_a0 & 1);
+          T = s_T;  // written before the first chunk-0 arrival of this item
+          mbar_wait(&bar_w[0], it & 1);
+          tc_fence_after();
+          for (int t = 0; t < T; ++t, ++n_a0) {
+            for (int c = 0; c < 4; ++c) {
+              if (t > 0 || c > 0) {
+                mbar_wait(&bar_a0c[c], n_a0 & 1);
+                tc_fence_after();
+              }
+              for (int s = 4 * c; s < 4 * c + 4 && s < S::kK0Steps; ++s) {
+                const uint32_t ao = c * S::kStage + (s & 3) * 32, wo = c * (kC * 128) + (s & 3) * 32;
+                const uint64_t ad = smem_desc_sw128(r1 + ao), bd = smem_desc_sw128(r2 + wo);
+                const uint32_t d = tmem + t * kC;
+                if (S::kSplit) {
+                  mma<kMode>(d, smem_desc_sw128(r1 + S::kA0Lo + ao), bd, idesc, s > 0);
+                  mma<kMode>(d, ad, smem_desc_sw128(r2 + S::kWBytes + wo), idesc, 1);
+                  mma<kMode>(d, ad, bd, idesc, 1);
+                } else {
+                  mma<kMode>(d, ad, bd, idesc, s > 0);
+                }
+              }
+            }
+            mma_commit(&bar_t0);
           }
-          gemm(tmem + t * kC, S::kA0Lo, S::kK0Steps);
-          mma_commit(&bar_t0);
+        } else {
+          mbar_wait(&bar_a0, n_a0++ & 1);
+          T = s_T;  // written before the first bar_a0 arrival of this item
+          mbar_wait(&bar_w[0], it & 1);
+          tc_fence_after();
+          for (int t = 0; t < T; ++t) {
+            if (t > 0) {
+              mbar_wait(&bar_a0, n_a0++ & 1);
+              tc_fence_after();
+            }
+            gemm(tmem + t * kC, S::kA0Lo, S::kK0Steps);
+            mma_commit(&bar_t0);
+          }
         }
         mma_commit(&bar_c0);
         // conv1: two tiles (16 positions x 8 samples each), A restaged by the
@@ -703,7 +740,35 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);
         if (t == 0) compute_sync();
         if (t == 1) stampx(3);
-        if (h == 0) {  // K 0..49
+        auto chunk_done = [&](int c) {  // f32 modes: this thread's part of K chunk c is written
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&bar_a0c[c]);
+        };
+        if constexpr (S::kK0Chunks == 4) {
+          if (h == 0) {  // K 0..49: chunk 0 (K 0-31), then its part of chunk 1
+#pragma unroll
+            for (int i = 0; i < 8; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            chunk_done(0);
+#pragma unroll
+            for (int i = 8; i < 12; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            put2<kMode>(R1, S::kA0Lo, r, 48, v[48], v[49]);
+            chunk_done(1);
+          } else {  // K 50..99 + pad: its part of chunk 1 (K 50-63), chunk 2 (64-95), chunk 3 (96-103)
+            put2<kMode>(R1, S::kA0Lo, r, 50, v[0], v[1]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+              put4<kMode>(R1, S::kA0Lo, r, 52 + 4 * i, v[2 + 4 * i], v[3 + 4 * i], v[4 + 4 * i], v[5 + 4 * i]);
+            chunk_done(1);
+#pragma unroll
+            for (int i = 3; i < 11; ++i)
+              put4<kMode>(R1, S::kA0Lo, r, 52 + 4 * i, v[2 + 4 * i], v[3 + 4 * i], v[4 + 4 * i], v[5 + 4 * i]);
+            chunk_done(2);
+            put4<kMode>(R1, S::kA0Lo, r, 96, v[46], v[47], v[48], v[49]);
+#pragma unroll
+            for (int k = 100; k < 100 + 2 * S::kPadUnits; k += 2) put2<kMode>(R1, S::kA0Lo, r, k, 0.0f, 0.0f);
+            chunk_done(3);
+          }
+        } else if (h == 0) {  // K 0..49
 #pragma unroll
           for (int i = 0; i < 12; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           put2<kMode>(R1, S::kA0Lo, r, 48, v[48], v[49]);
@@ -725,8 +790,10 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           }
         }
         stampx(t == 0 ? 1 : 4);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&bar_a0);
+        if constexpr (S::kK0Chunks != 4) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&bar_a0);
+        }
         mark(2 + t);
       }
       if (tr && it == 0 && tid == 0) tr[20] = T;
