@@ -78,6 +78,8 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
   // biases fetched with the partials (no dependent global load later): lane j
   // holds b2 of this warp's j-th output, b1 of its own hidden units
   const float b2v = (lane < 8 && warp + 8 * lane < a.od) ? __ldg(a.b2 + warp + 8 * lane) : 0.0f;
+  // and lane i < od % 8 holds b2 of remainder output (od & ~7) + i
+  const float b2r = lane < (a.od & 7) ? __ldg(a.b2 + (a.od & ~7) + lane) : 0.0f;
   float4 b1v[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u)
@@ -128,7 +130,8 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
   if (w2_bar) mbar_wait(w2_bar, w2_parity);
   fc_sync256();
   if (trace && threadIdx.x == 0) trace[0] = clock64();
-  {  // FC2: warp w computes outputs o = w, w + 8, ... for all 8 samples
+  {  // FC2: warp w computes outputs o = w, w + 8, ... for all 8 samples; the
+     // od % 8 remainder outputs are spread one sample per warp
     float4 hr[8][2];
 #pragma unroll
     for (int sm = 0; sm < 8; ++sm)
@@ -137,27 +140,27 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
         const int c = lane + 32 * u;
         hr[sm][u] = c < c4 ? reinterpret_cast<const float4*>(hs + sm * hid)[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
-    for (int j = 0, o = warp; o < a.od; ++j, o += 8) {
-      const float b2o = __shfl_sync(0xffffffffu, b2v, j);
-      float4 wv[2];
+    auto row = [&](int o, float4 (&wv)[2]) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int c = lane + 32 * u;
         wv[u] = c < c4 ? reinterpret_cast<const float4*>(w2s + o * hid)[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
-      float v[8];
+    };
+    auto dot = [&](const float4 (&wv)[2], const float4 (&hv)[2]) {  // this lane's 8 hidden units
+      float p = 0.0f;
 #pragma unroll
-      for (int sm = 0; sm < 8; ++sm) {
-        float p = 0.0f;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          p = fmaf(wv[u].x, hr[sm][u].x, p);
-          p = fmaf(wv[u].y, hr[sm][u].y, p);
-          p = fmaf(wv[u].z, hr[sm][u].z, p);
-          p = fmaf(wv[u].w, hr[sm][u].w, p);
-        }
-        v[sm] = p;
+      for (int u = 0; u < 2; ++u) {
+        p = fmaf(wv[u].x, hv[u].x, p);
+        p = fmaf(wv[u].y, hv[u].y, p);
+        p = fmaf(wv[u].z, hv[u].z, p);
+        p = fmaf(wv[u].w, hv[u].w, p);
       }
+      return p;
+    };
+    // lane sums over xor 16, 8, 4, 2, 1 (the butterfly below pairs lanes the
+    // same way, and fp addition is commutative: every output rounds identically)
+    auto transpose_store = [&](float (&v)[8], int o, float b2o) {
 #pragma unroll
       for (int m = 16, n = 4; m >= 4; m >>= 1, n >>= 1) {  // transpose: 8 -> 4 -> 2 -> 1 values per lane
         const bool upper = (lane & m) != 0;
@@ -173,6 +176,37 @@ __device__ inline void cta8_fc(const FcDecodeArgs& a, uint64_t s_local, const fl
       if ((lane & 3) == 0) {
         const int sm = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
         ys[sm * kFcMaxOut + o] = v[0] + b2o;
+      }
+    };
+    const int full = a.od >> 3;
+    for (int j = 0; j < full; ++j) {
+      const int o = warp + 8 * j;
+      const float b2o = __shfl_sync(0xffffffffu, b2v, j);
+      float4 wv[2];
+      row(o, wv);
+      float v[8];
+#pragma unroll
+      for (int sm = 0; sm < 8; ++sm) v[sm] = dot(wv, hr[sm]);
+      transpose_store(v, o, b2o);
+    }
+    // remainder outputs 8 * full + i: warp w takes sample w (its h re-read from smem)
+    const int rem = a.od & 7;
+    if (rem) {
+      float4 hv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
+        hv[u] = c < c4 ? reinterpret_cast<const float4*>(hs + warp * hid)[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+      for (int i = 0; i < rem; ++i) {
+        const int o = 8 * full + i;
+        float4 wv[2];
+        row(o, wv);
+        float p = dot(wv, hv);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) p += __shfl_xor_sync(0xffffffffu, p, m);
+        const float b2o = __shfl_sync(0xffffffffu, b2r, i);
+        if (lane == 0) ys[warp * kFcMaxOut + o] = p + b2o;
       }
     }
   }
