@@ -540,3 +540,30 @@ def test_overlapped_upload_matches_load_then_run(gpu, extra):
     g.load_trace(t, pc, shard=shard, truth=False)
     b = g.run(pc, shard=shard)
     assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+
+
+@pytest.mark.parametrize("heads", [(6, 9, 12), (4, 4, 5)])
+def test_fc2_head_sizes(gpu, port, golden, heads):
+    """Head sizes other than 10/10/10 (output_dim 30 and 16: FC2's od % 8
+    remainder is 6 and 0, spread over the warps): teacher-forced outputs vs the
+    port, the fused round bit-identical to the unfused one and within 0.1% of
+    the CPU oracle."""
+    g = gpu("tf32x3")
+    cfg = CnnConfig.preset_c3()
+    cfg.class_fetch, cfg.class_exec, cfg.class_store = heads
+    gm = golden["models"]["c3_mix_seed1"]
+    m = Model(cfg, np.array(gm["norm"]), port.init_params(cfg, 5))
+    g.load_model(m)
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    want = port.simulate(t, m, k=16, capture=600, capture_inputs=True, capture_outputs=True)
+    out, _ = g.predict(want["cap_inputs"], want["cap_is_store"])
+    assert out.shape[1] == cfg.output_dim
+    err = np.abs(out - want["cap_outputs"]) / np.maximum(1.0, np.abs(want["cap_outputs"]))
+    assert err.max() <= 1e-4, err.max()
+    pc = pcfg(16)
+    g.load_trace(t, pc)
+    a = g.run(pc)
+    b = g.run(pc, fused=False)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    full = port.simulate(t, m, k=16)
+    assert abs(a.total_cycles - full["total_cycles"]) <= 1e-3 * full["total_cycles"]
