@@ -53,8 +53,11 @@ constexpr uint32_t kOutStage = 96 * 1024;  // flat staging in R1 (2 x 16 KB)
 // Tile-0 static-slot staging in R1 during the decode (R1 holds W2 [0, 64 KB)
 // and h / y [64 KB, 74 KB) then): per sample one TMA box of 32 trace rows
 // [lo, lo + 32) ending at the predicted target, 176 B per row (11 x 16 B: an
-// odd pitch, so LDS.128 of 8 rows hit 8 distinct bank groups).
-constexpr uint32_t kStgOff = 74 * 1024;
+// odd pitch, so LDS.128 of 8 rows hit 8 distinct bank groups).  It starts past
+// conv0's K chunk 0 (hi [0, 16 KB), lo [64, 80 KB)), so tile 0's chunk-0
+// stores need not wait for the other threads' staging reads.
+constexpr uint32_t kStgOff = 80 * 1024;
+static_assert(kStgOff + kItem * 32 * 176 <= kR1, "tile-0 staging must fit in R1");
 constexpr uint32_t kStgPitch = 176;
 constexpr uint32_t kStgBox = 32 * kStgPitch;  // 5632 B, 128-B aligned
 constexpr int kThreadsRF = 320;
@@ -738,17 +741,24 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         // operand writes wait for them to finish reading R1 (tile 0: for every
         // thread to finish reading the staging, which the operand overlaps)
         if (t > 0) mbar_wait(&bar_t0, n_t0++ & 1);
-        if (t == 0) compute_sync();
-        if (t == 1) stampx(3);
-        auto chunk_done = [&](int c) {  // f32 modes: this thread's part of K chunk c is written
+        auto chunk_done = [&](int c) {  // this thread's part of K range [32c, 32c + 32) is written
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_arrive(&bar_a0c[c]);
         };
         if constexpr (S::kK0Chunks == 4) {
-          if (h == 0) {  // K 0..49: chunk 0 (K 0-31), then its part of chunk 1
+          if (h == 0) {  // K 0-31 (chunk 0) first: it does not overlap the tile-0 staging
 #pragma unroll
             for (int i = 0; i < 8; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             chunk_done(0);
+          }
+        }
+        // 3xTF32: the lo planes of chunks 1-3 overlap the staging, so tile 0
+        // waits for every thread to have read its staged rows (bf16 / fp8
+        // operands end below the staging: no wait)
+        if (S::kSplit && t == 0) compute_sync();
+        if (t == 1) stampx(3);
+        if constexpr (S::kK0Chunks == 4) {
+          if (h == 0) {  // the rest of K 0..49: its part of chunk 1
 #pragma unroll
             for (int i = 8; i < 12; ++i) put4<kMode>(R1, S::kA0Lo, r, 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             put2<kMode>(R1, S::kA0Lo, r, 48, v[48], v[49]);
