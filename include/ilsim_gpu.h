@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define ILSIM_GPU_ABI_VERSION 1
+#define ILSIM_GPU_ABI_VERSION 2
 
 typedef struct ilsim_gpu_ctx ilsim_gpu_ctx;
 
@@ -53,7 +53,12 @@ typedef struct ilsim_gpu_options {
 
 /* Structure-of-arrays view of an annotated trace: the AnnotatedInstruction
  * fields the simulate path reads (trace.hpp:49-109).  truth is only needed
- * in oracle mode (OraclePredictor, predictor.hpp:45-59).                   */
+ * in oracle mode (OraclePredictor, predictor.hpp:45-59).
+ * n is the GLOBAL trace length (the partition is computed over it); the
+ * arrays hold instructions [base, base + rows) of that trace, so a process
+ * simulating one shard of a large trace passes only its slice (rows must
+ * cover the shard's instructions plus its warm-up prefix).  base = 0: the
+ * arrays hold the whole trace.  (ABI v2 added base.)                      */
 typedef struct ilsim_trace_view {
   uint64_t n;
   const uint64_t* pc;        /* [n]                                  */
@@ -64,6 +69,7 @@ typedef struct ilsim_trace_view {
   const uint64_t* data_addr; /* [n]                                  */
   const uint16_t* hist;      /* [n][14] HistoryFeatures::v           */
   const uint32_t* truth;     /* [n][3] fetch, execution, store       */
+  uint64_t base;             /* global index of the arrays' row 0    */
 } ilsim_trace_view;
 
 /* CnnConfig (cnn.hpp:17-40).                                                 */
@@ -155,6 +161,16 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* ctx, const ilsim_trace_view* trac
  * NULL); triples: n x {fetch, execution, store}.                              */
 int ilsim_gpu_predict(ilsim_gpu_ctx* ctx, const float* inputs, uint64_t n, const uint8_t* is_store,
                       float* outputs, uint32_t* triples);
+
+/* Test hook: hybrid decode (decode_hybrid, cnn.cpp:388-417) of caller head
+ * outputs (n x output_dim floats, the ilsim_gpu_predict output layout) with
+ * the loaded model's NormStats label statistics and head sizes.  path 0: the
+ * per-thread decode of the unfused / teacher-forced path (decode.cuh);
+ * path 1: the warp-cooperative decode of the fused round (fc_decode.cuh).
+ * Lets the reference's decode goldens (test_cnn.cpp:183-224) run on the
+ * device functions themselves.                                              */
+int ilsim_gpu_decode_outputs(ilsim_gpu_ctx* ctx, const float* outputs, uint64_t n, const uint8_t* is_store,
+                             uint32_t* triples, int32_t path);
 
 /* Test hook: capture the gathered input tensor of round `round` of the next
  * run (k x 50*(max_context+1) floats in sub-trace order; rows of inactive

@@ -31,6 +31,7 @@ class TraceView(C.Structure):
         ("data_addr", C.c_void_p),
         ("hist", C.c_void_p),
         ("truth", C.c_void_p),
+        ("base", C.c_uint64),
     ]
 
 
@@ -100,6 +101,8 @@ class Totals(C.Structure):
     ]
 
 
+ABI_VERSION = 2  # ILSIM_GPU_ABI_VERSION in include/ilsim_gpu.h
+
 # Every symbol include/ilsim_gpu.h declares (checked by the CPU test suite).
 EXPORTS = [
     "ilsim_gpu_abi_version",
@@ -113,6 +116,7 @@ EXPORTS = [
     "ilsim_gpu_simulate_parallel",
     "ilsim_gpu_predict",
     "ilsim_gpu_set_capture",
+    "ilsim_gpu_decode_outputs",
     "ilsim_gpu_partition",
     "ilsim_gpu_model_flops",
     "ilsim_gpu_param_count",
@@ -132,6 +136,9 @@ def lib() -> C.CDLL:
     L = C.CDLL(str(LIB_PATH))
     vp, u64, i32 = C.c_void_p, C.c_uint64, C.c_int32
     L.ilsim_gpu_abi_version.restype = C.c_int
+    if L.ilsim_gpu_abi_version() != ABI_VERSION:
+        raise IlsimError(f"{LIB_PATH} has ABI version {L.ilsim_gpu_abi_version()}, this binding expects "
+                         f"{ABI_VERSION} (rebuild: paper_2105_05821_b200/build.py)")
     L.ilsim_gpu_create.argtypes = [C.POINTER(Options), C.POINTER(vp), C.c_char_p, C.c_int]
     L.ilsim_gpu_destroy.argtypes = [vp]
     L.ilsim_gpu_destroy.restype = None
@@ -145,6 +152,7 @@ def lib() -> C.CDLL:
                                               C.POINTER(Totals)]
     L.ilsim_gpu_predict.argtypes = [vp, vp, u64, vp, vp, vp]
     L.ilsim_gpu_set_capture.argtypes = [vp, C.c_uint32, vp, u64]
+    L.ilsim_gpu_decode_outputs.argtypes = [vp, vp, u64, vp, vp, i32]
     L.ilsim_gpu_partition.argtypes = [u64, u64, vp, C.c_char_p, C.c_int]
     L.ilsim_gpu_model_flops.argtypes = [C.POINTER(CnnCfg)]
     L.ilsim_gpu_model_flops.restype = u64
@@ -154,7 +162,7 @@ def lib() -> C.CDLL:
     for f in (L.ilsim_gpu_create, L.ilsim_gpu_load_model, L.ilsim_gpu_load_trace, L.ilsim_gpu_load_trace_records,
               L.ilsim_gpu_run,
               L.ilsim_gpu_simulate_parallel, L.ilsim_gpu_predict, L.ilsim_gpu_set_capture,
-              L.ilsim_gpu_partition, L.ilsim_gpu_init_weights):
+              L.ilsim_gpu_partition, L.ilsim_gpu_init_weights, L.ilsim_gpu_decode_outputs):
         f.restype = i32
     _lib = L
     return L

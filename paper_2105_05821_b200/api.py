@@ -142,11 +142,15 @@ def init_weights(cfg: CnnConfig, norm: np.ndarray, seed: int) -> Model:
                  np.zeros(n, np.float32), 0)
 
 
-def trace_view(t: Trace, with_truth: bool = True) -> tuple[_lib.TraceView, list]:
-    """C view of a trace (keeps the arrays alive via the returned list)."""
+def trace_view(t: Trace, with_truth: bool = True, n_total: int | None = None, base: int = 0
+               ) -> tuple[_lib.TraceView, list]:
+    """C view of a trace (keeps the arrays alive via the returned list).
+    ``n_total``/``base``: ``t`` holds only instructions [base, base + t.n) of
+    a global trace of n_total instructions (a shard's slice)."""
     keep = [np.ascontiguousarray(a) for a in (t.pc, t.op, t.src, t.dst, t.has_data, t.data_addr, t.hist, t.truth)]
     v = _lib.TraceView()
-    v.n = t.n
+    v.n = t.n if n_total is None else n_total
+    v.base = base
     v.pc, v.op, v.src, v.dst, v.has_data, v.data_addr, v.hist = (a.ctypes.data for a in keep[:7])
     v.truth = keep[7].ctypes.data if with_truth else None
     return v, keep
@@ -215,6 +219,20 @@ class GpuSimulator:
                                              tri.ctypes.data))
         return out, tri
 
+    def decode(self, outputs: np.ndarray, is_store: np.ndarray, path: int = 0) -> np.ndarray:
+        """Test hook: ``decode_hybrid`` (cnn.cpp:388-417) of caller head outputs
+        on the device decode functions (path 0: per-thread, 1: the fused
+        round's warp-cooperative form)."""
+        if self.model is None:
+            raise IlsimError("no model loaded")
+        y = np.ascontiguousarray(outputs, dtype=np.float32)
+        n = y.shape[0]
+        st = np.ascontiguousarray(is_store, dtype=np.uint8)
+        tri = np.zeros((n, 3), dtype=np.uint32)
+        self._check(self.L.ilsim_gpu_decode_outputs(self._h, y.ctypes.data, n, st.ctypes.data, tri.ctypes.data,
+                                                    path))
+        return tri
+
     # -- simulation ---------------------------------------------------------
     def _sim_cfg(self, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None,
                  profile=False, truth_inputs=False, fused=True) -> _lib.SimCfg:
@@ -239,13 +257,15 @@ class GpuSimulator:
         return c
 
     def load_trace(self, trace: Trace, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None,
-                   truth: bool = True):
+                   truth: bool = True, n_total: int | None = None, base: int = 0):
         """Upload this configuration's trace slice.  ``truth``: also upload the
-        recorded latencies (needed for oracle runs; the CNN path skips them)."""
+        recorded latencies (needed for oracle runs; the CNN path skips them).
+        ``n_total``/``base``: ``trace`` is the slice [base, base + trace.n) of a
+        global trace of n_total instructions (see :func:`trace_view`)."""
         cfg = self._sim_cfg(pc, sequential=sequential, oracle=oracle, shard=shard)
-        view, keep = trace_view(trace, with_truth=oracle or truth)
+        view, keep = trace_view(trace, with_truth=oracle or truth, n_total=n_total, base=base)
         self._check(self.L.ilsim_gpu_load_trace(self._h, C.byref(view), C.byref(cfg)))
-        self._trace_n = trace.n
+        self._trace_n = int(view.n)
         del keep
 
     def load_trace_file(self, path: str, pc: ParallelConfig, *, sequential=False, oracle=False, shard=None,
@@ -335,19 +355,23 @@ class GpuSimulator:
                               float(tot.device_ms), tuple(tot.kernel_ms), int(tot.launches), int(tot.rounds))
 
     def simulate_parallel(self, trace: Trace, pc: ParallelConfig | None = None, *, oracle=False,
-                          shard=None, fetch_out: np.ndarray | None = None) -> ParallelResult:
+                          shard=None, fetch_out: np.ndarray | None = None, n_total: int | None = None,
+                          base: int = 0) -> ParallelResult:
         """``simulate_parallel`` (parallel.cpp:26-93): one ``ilsim_gpu_simulate_parallel``
-        call, which overlaps the trace upload with the rounds on large traces."""
+        call, which overlaps the trace upload with the rounds on large traces.
+        ``n_total``/``base``: ``trace`` holds only a slice of the global trace."""
         pc = pc or ParallelConfig()
-        view, keep = trace_view(trace, with_truth=oracle)
-        self._trace_n = trace.n
+        view, keep = trace_view(trace, with_truth=oracle, n_total=n_total, base=base)
+        self._trace_n = int(view.n)
         r = self.run(pc, oracle=oracle, shard=shard, fetch_out=fetch_out, _view=view)
         del keep
         return r
 
-    def simulate_trace(self, trace: Trace, sim: SimConfig | None = None, *, oracle=False) -> SimResult:
-        """``simulate_trace`` (simcore.cpp:185-196)."""
-        pc = ParallelConfig(k=1, sim=sim or SimConfig())
+    def simulate_trace(self, trace: Trace, sim: SimConfig | None = None, *, oracle=False,
+                       write_ring: int = 0) -> SimResult:
+        """``simulate_trace`` (simcore.cpp:185-196).  ``write_ring``: device
+        write-queue ring entries (0 = auto, grows on overflow)."""
+        pc = ParallelConfig(k=1, sim=sim or SimConfig(), write_ring=write_ring)
         self.load_trace(trace, pc, sequential=True, oracle=oracle, truth=oracle)
         r = self.run(pc, sequential=True, oracle=oracle)
         return r.sub_results[0]
@@ -376,7 +400,7 @@ def throughput_csv(rows: list[tuple[int, int, float]]) -> str:
 
 def simulate(trace_path: str, model_path: str = "", oracle: bool = False, parallel: int = 1,
              subtrace_size: int = 0, batch_max: int = 4096, *, precision: str = "tf32x3", device: int = 0,
-             warmup: int = 0, drain_trim: bool = False) -> dict:
+             warmup: int = 0, drain_trim: bool = False, write_ring: int = 0) -> dict:
     """``ilsim.simulate`` (bindings/module.cpp:117-156) on the GPU; the trace
     file's records are unpacked on the device (GPU trace ingest)."""
     from .formats import trace_records
@@ -391,13 +415,14 @@ def simulate(trace_path: str, model_path: str = "", oracle: bool = False, parall
             sim.max_context = g.model.config.max_context
         if parallel > 1 or subtrace_size > 0:
             pc = ParallelConfig(k=parallel, subtrace_size=subtrace_size, batch_max=batch_max, sim=sim,
-                                warmup=warmup, drain_trim=drain_trim)
+                                warmup=warmup, drain_trim=drain_trim, write_ring=write_ring)
             g.load_trace_file(trace_path, pc, oracle=oracle)
             pr = g.run(pc, oracle=oracle)
-            d = _agg_dict(pr.sub_results, pr.instructions, pr.total_cycles, pr.cpi, n_trace == 0)
+            # module.cpp:131-150 leaves agg.empty false in the parallel branch
+            d = _agg_dict(pr.sub_results, pr.instructions, pr.total_cycles, pr.cpi, False)
             d["sub_traces"] = len(pr.sub_results)
             return d
-        pc = ParallelConfig(k=1, sim=sim)
+        pc = ParallelConfig(k=1, sim=sim, write_ring=write_ring)
         g.load_trace_file(trace_path, pc, sequential=True, oracle=oracle)
         r = g.run(pc, sequential=True, oracle=oracle).sub_results[0]
         return _agg_dict([r], r.instructions, r.total_cycles, r.cpi, r.empty)

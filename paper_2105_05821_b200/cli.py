@@ -66,12 +66,12 @@ def cmd_simulate(a) -> int:
         t0 = time.perf_counter()
         if a.parallel > 1 or a.subtrace_size > 0:
             pc = ParallelConfig(k=a.parallel, subtrace_size=a.subtrace_size, batch_max=a.batch_max, sim=sim,
-                                warmup=a.warmup, drain_trim=a.drain_trim)
+                                warmup=a.warmup, drain_trim=a.drain_trim, write_ring=a.write_ring)
             g.load_trace_file(a.trace, pc, oracle=a.oracle)
             pr = g.run(pc, oracle=a.oracle)
             subs, n, total, cpi, fetch = pr.sub_results, pr.instructions, pr.total_cycles, pr.cpi, pr.predicted_fetch
         else:
-            pc = ParallelConfig(k=1, sim=sim)
+            pc = ParallelConfig(k=1, sim=sim, write_ring=a.write_ring)
             g.load_trace_file(a.trace, pc, sequential=True, oracle=a.oracle)
             r = g.run(pc, sequential=True, oracle=a.oracle).sub_results[0]
             subs, n, total, cpi, fetch = [r], r.instructions, r.total_cycles, r.cpi, r.predicted_fetch
@@ -112,6 +112,8 @@ def main(argv=None) -> int:
     s.add_argument("--precision", default="tf32x3", choices=["fp32", "tf32x3", "tf32", "bf16", "fp8"])
     s.add_argument("--warmup", type=int, default=0, help="extension: warm-up instructions per sub-trace")
     s.add_argument("--drain-trim", action="store_true", help="extension: count only the last sub-trace's drain")
+    s.add_argument("--write-ring", type=int, default=0,
+                   help="write-queue ring entries per sub-trace (0 = auto: grows on overflow)")
     a = p.parse_args(argv)
     try:
         return cmd_simulate(a)

@@ -85,6 +85,15 @@ Plan make_plan(const ilsim_sim_config& c, uint64_t n) {
   return p;
 }
 
+// Row of the view's arrays that holds global instruction P.g0 (the view may
+// hold only a slice [base, ...) of the global trace, ilsim_trace_view.base).
+uint64_t view_row(const ilsim_trace_view* t, const Plan& P) {
+  if (t->base > P.g0 || t->base > t->n)
+    throw ApiError("trace view (base " + std::to_string(t->base) + ") does not cover the shard's first instruction " +
+                   std::to_string(P.g0));
+  return P.g0 - t->base;
+}
+
 }  // namespace
 
 struct ilsim_gpu_ctx {
@@ -250,10 +259,11 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
       c->win_ev.push_back(e);
     }
     const ilsim_trace_view* t = c->deferred;
+    const uint64_t row0 = view_row(t, P);
     auto copy2d = [&](void* dev, const void* host, size_t esz, const Group& g, uint64_t p0, uint64_t len) {
       const size_t pitch = g.stride * esz, width = len * esz;
       CUDA_OK(cudaMemcpy2DAsync(static_cast<char*>(dev) + (g.first_begin + p0) * esz, pitch,
-                                static_cast<const char*>(host) + (P.g0 + g.first_begin + p0) * esz, pitch, width,
+                                static_cast<const char*>(host) + (row0 + g.first_begin + p0) * esz, pitch, width,
                                 g.count, cudaMemcpyHostToDevice, c->copy_stream));
     };
     CUDA_OK(cudaEventRecord(c->ev[6], c->stream));  // buffers free of earlier users
@@ -588,8 +598,9 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
       throw ApiError("drain made no progress at tick " + std::to_string(st.err_tick) + " (sub-trace " +
                      std::to_string(i) + ")");
     if (st.status == kErrWriteRing)
-      throw ApiError("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
-                     std::to_string(i) + "; raise write_ring");
+      throw WriteRingOverflow("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
+                                  std::to_string(i) + "; raise write_ring",
+                              wcap);
     if (st.pos != st.len) throw ApiError("internal: sub-trace did not finish");
     ilsim_sub_result& r = subs[j];
     r.instructions = st.len - st.warm;
@@ -612,6 +623,29 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   tot->device_ms = ms;
   for (int q = 0; q < 4; ++q) tot->kernel_ms[q] = kms[q];
   tot->launches = launches;
+}
+
+// run_impl, rerun with a doubled write ring while a sub-trace's write queue
+// outgrows it and the caller left write_ring on auto (0); the reference's write
+// queue is an unbounded deque (simcore.hpp:61-90).  Bounded at 2^22 entries
+// and 64 GB of rings; past that the overflow is reported.
+template <class Reset>
+void run_growing_ring(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* subs, uint64_t sub_cap,
+                      uint32_t* predicted_fetch, ilsim_totals* totals, Reset reset) {
+  ilsim_sim_config cur = cfg;
+  for (;;) {
+    try {
+      *totals = ilsim_totals{};
+      run_impl(c, cur, subs, sub_cap, predicted_fetch, totals);
+      return;
+    } catch (const WriteRingOverflow& e) {
+      const uint64_t next = 2ull * e.capacity;
+      const uint64_t k = cur.shard_end > cur.shard_begin ? cur.shard_end - cur.shard_begin : std::max<uint64_t>(cur.k, 1);
+      if (cfg.write_ring != 0 || next > (1ull << 22) || next * k * sizeof(RingEntry) > (64ull << 30)) throw;
+      cur.write_ring = static_cast<int32_t>(next);
+      reset();
+    }
+  }
 }
 
 // Shared tail of the trace loaders: flags + (model loaded) normalised static
@@ -749,7 +783,7 @@ int ilsim_gpu_load_trace(ilsim_gpu_ctx* c, const ilsim_trace_view* t, const ilsi
     c->t_total = t->n;
     c->g0 = P.g0;
     c->g1 = P.g1;
-    const uint64_t g0 = P.g0, m = P.g1 - P.g0;
+    const uint64_t g0 = view_row(t, P), m = P.g1 - P.g0;
     upload(c->pc, t->pc + g0, m, c->stream);
     upload(c->addr, t->data_addr + g0, m, c->stream);
     upload(c->op, t->op + 13 * g0, 13 * m, c->stream);
@@ -806,7 +840,7 @@ int ilsim_gpu_load_trace_records(ilsim_gpu_ctx* c, const void* records, uint64_t
 
 int ilsim_gpu_run(ilsim_gpu_ctx* c, const ilsim_sim_config* cfg, ilsim_sub_result* subs, uint64_t sub_cap,
                   uint32_t* predicted_fetch, ilsim_totals* totals) {
-  return guard(c, [&] { run_impl(c, *cfg, subs, sub_cap, predicted_fetch, totals); });
+  return guard(c, [&] { run_growing_ring(c, *cfg, subs, sub_cap, predicted_fetch, totals, [] {}); });
 }
 
 int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, const ilsim_sim_config* cfg,
@@ -825,6 +859,7 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, con
   }
   const int rc = guard(c, [&] {
     const Plan P = make_plan(*cfg, t->n);
+    view_row(t, P);
     c->has_trace = false;
     c->t_total = t->n;
     c->g0 = P.g0;
@@ -844,7 +879,11 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* c, const ilsim_trace_view* t, con
     if (!c->copy_stream) CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     c->deferred = t;
     try {
-      run_impl(c, *cfg, subs, sub_cap, predicted_fetch, totals);
+      // a rerun with a larger write ring uploads and packs the windows again
+      run_growing_ring(c, *cfg, subs, sub_cap, predicted_fetch, totals, [&] {
+        c->packed_gen = c->model_gen;
+        c->has_trace = true;
+      });
     } catch (...) {
       c->deferred = nullptr;
       c->packed_gen = ~0ull;  // the device trace may be partial: it must be loaded again
@@ -892,6 +931,28 @@ int ilsim_gpu_predict(ilsim_gpu_ctx* c, const float* inputs, uint64_t n, const u
       CUDA_OK(cudaMemcpyAsync(triples + 3 * f, dt, m * 12, cudaMemcpyDeviceToHost, c->stream));
       CUDA_OK(cudaStreamSynchronize(c->stream));
     }
+  });
+}
+
+int ilsim_gpu_decode_outputs(ilsim_gpu_ctx* c, const float* outputs, uint64_t n, const uint8_t* is_store,
+                             uint32_t* triples, int32_t path) {
+  return guard(c, [&] {
+    if (!c->has_model) throw ApiError("no model loaded");
+    if (path != 0 && path != 1) throw ApiError("decode path must be 0 (per-thread) or 1 (warp)");
+    if (n == 0) return;
+    const int od = output_dim_of(c->cfg);
+    DevBuf d_y, d_store, d_trip;
+    float* dy = static_cast<float*>(d_y.need(n * od * sizeof(float)));
+    uint8_t* ds = static_cast<uint8_t*>(d_store.need(n));
+    uint32_t* dt = static_cast<uint32_t*>(d_trip.need(n * 12));
+    CUDA_OK(cudaMemcpyAsync(dy, outputs, n * od * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ds, is_store, n, cudaMemcpyHostToDevice, c->stream));
+    (path == 0 ? launch_decode_only : launch_decode_warp)(dy, od, n, ds, c->nc_dev.as<NormConsts>(),
+                                                           c->cfg.class_fetch, c->cfg.class_exec,
+                                                           c->cfg.class_store, dt, c->stream);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(triples, dt, n * 12, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
   });
 }
 

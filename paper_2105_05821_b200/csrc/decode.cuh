@@ -20,9 +20,13 @@ __device__ __forceinline__ uint32_t decode_head(const float* y, int base, int n,
   if (best < n - 1) return static_cast<uint32_t>(best);
   // overflow class: de-normalise out of log1p space (cnn.cpp:399-401); the
   // reference's -march=native build contracts r*sigma+mu into one fp64 FMA.
-  const double z = fmin(fma(static_cast<double>(r), sigma, mu), 22.0);
-  const double raw = fmax(0.0, expm1(z));
-  const long long v = llround(fmin(raw, 4.0e9));
+  // std::min / std::max operand order (a NaN regression passes min and max
+  // turns it into 0, as in the reference; fmin/fmax would drop the NaN instead)
+  const double x = fma(static_cast<double>(r), sigma, mu);
+  const double z = (22.0 < x) ? 22.0 : x;        // std::min(x, 22.0)
+  const double e = expm1(z);
+  const double raw = (0.0 < e) ? e : 0.0;        // std::max(0.0, e)
+  const long long v = llround((4.0e9 < raw) ? 4.0e9 : raw);  // std::min(raw, 4.0e9)
   return static_cast<uint32_t>(v > 0xffffffffLL ? 0xffffffffLL : v);
 }
 

@@ -12,6 +12,14 @@ struct ApiError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// A sub-trace's write queue outgrew its device ring (the reference's queue is
+// an unbounded deque): the round loop reruns with a larger ring when the
+// caller left write_ring on auto (0).
+struct WriteRingOverflow : ApiError {
+  uint32_t capacity;
+  WriteRingOverflow(const std::string& m, uint32_t cap) : ApiError(m), capacity(cap) {}
+};
+
 #define CUDA_OK(expr)                                                                      \
   do {                                                                                     \
     cudaError_t e_ = (expr);                                                               \

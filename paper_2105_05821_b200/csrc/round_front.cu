@@ -971,6 +971,9 @@ void launch_final_decode(const FrontParams& p, cudaStream_t s) {
   const uint64_t n = p.last - p.first;
   if (n == 0) return;
   const size_t sm = (static_cast<size_t>(p.fc.od + 8) * p.fc.hidden + 8 * kFcMaxOut) * 4;
+  if (sm > 48 * 1024)  // (od + 8) x hidden W2 / h staging: output_dim >= 39 at hidden 256
+    CUDA_OK(cudaFuncSetAttribute(final_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sm)));
   final_decode_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, sm, s>>>(p);
 }
 

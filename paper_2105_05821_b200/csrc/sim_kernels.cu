@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "decode.cuh"
+#include "fc_decode.cuh"
 #include "k1_device.cuh"
 #include "launch.cuh"
 #include "sim_kernels.cuh"
@@ -254,6 +255,36 @@ void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t*
   if (n == 0) return;
   decode_only_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(
       y, y_stride, n, is_store, nc, cf, ce, cs, out);
+}
+
+// Test hook (ilsim_gpu_decode_outputs, path 1): the fused round's
+// warp-cooperative decode (warp_decode_triple, one warp per sample, the label
+// statistics in shared memory as the round front stages them).
+__global__ void decode_warp_kernel(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
+                                   const NormConsts* nc, int cf, int ce, int cs, uint32_t* out) {
+  __shared__ double lab[6];
+  if (threadIdx.x < 3) {
+    lab[threadIdx.x] = nc->label_mean[threadIdx.x];
+    lab[3 + threadIdx.x] = nc->label_sd[threadIdx.x];
+  }
+  __syncthreads();
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  uint32_t t[3];
+  warp_decode_triple(y + i * y_stride, lab, cf, ce, cs, is_store[i] != 0, t);
+  if ((threadIdx.x & 31) == 0) {
+    out[3 * i + 0] = t[0];
+    out[3 * i + 1] = t[1];
+    out[3 * i + 2] = t[2];
+  }
+}
+
+void launch_decode_warp(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
+                        const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
+                        cudaStream_t stream) {
+  if (n == 0) return;
+  decode_warp_kernel<<<static_cast<unsigned>((n + 3) / 4), 128, 0, stream>>>(y, y_stride, n, is_store, nc, cf,
+                                                                             ce, cs, out);
 }
 
 // ---------------------------------------------------------------------------

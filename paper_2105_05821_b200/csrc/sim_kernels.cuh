@@ -65,6 +65,10 @@ void launch_decode(const DecodeParams& p, cudaStream_t stream);
 void launch_decode_only(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
                         const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
                         cudaStream_t stream);
+// Same decode, the fused round's warp-cooperative form (test hook).
+void launch_decode_warp(const float* y, int y_stride, uint64_t n, const uint8_t* is_store,
+                        const NormConsts* nc, int cf, int ce, int cs, uint32_t* out,
+                        cudaStream_t stream);
 void launch_pack(const PackParams& p, cudaStream_t stream);
 
 // SNT1 records (108 B, trace.cpp:49-83) -> device structure-of-arrays.

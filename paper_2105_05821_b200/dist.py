@@ -48,12 +48,21 @@ class Totals:
         return self.total_cycles / self.instructions if self.instructions else 0.0
 
 
+def _device(device):
+    """The collective's tensor device: CPU tensors under gloo, else `device`."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_backend() == "gloo":
+        return "cpu"
+    return device
+
+
 def all_reduce_totals(t: Totals, device=None) -> Totals:
     """Sum the shard totals over all ranks (exact: integer sums)."""
     import torch
     import torch.distributed as dist
 
-    v = torch.tensor(t.as_list(), dtype=torch.int64, device=device)
+    v = torch.tensor(t.as_list(), dtype=torch.int64, device=_device(device))
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
     return Totals(*[int(x) for x in v.tolist()])
@@ -64,18 +73,27 @@ def max_over_ranks(x: float, device=None) -> float:
     import torch
     import torch.distributed as dist
 
-    v = torch.tensor([x], dtype=torch.float64, device=device)
+    v = torch.tensor([x], dtype=torch.float64, device=_device(device))
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
     return float(v.item())
 
 
-def simulate_sharded(sim, trace, pc, rank: int, world: int, *, oracle: bool = False):
+def simulate_sharded(sim, trace, pc, rank: int, world: int, *, oracle: bool = False, n_total: int | None = None,
+                     base: int = 0, fetch_out=None):
     """Run this rank's shard of the global partition on its GPU and return
-    (shard ParallelResult, global Totals)."""
-    from .api import GpuSimulator
+    (shard ParallelResult, global Totals).  ``trace`` is the whole trace, or
+    (``n_total``/``base``) only the slice [base, base + trace.n) that holds
+    this rank's instructions.  A rank with no sub-traces (world > k) still
+    joins the one collective with zero totals, so no rank is left waiting."""
+    from .api import GpuSimulator, ParallelResult
 
-    k = GpuSimulator._num_sub(pc, trace.n, False)
+    n = trace.n if n_total is None else n_total
+    k = GpuSimulator._num_sub(pc, n, False)
     shard = shard_range(k, rank, world)
-    res = sim.simulate_parallel(trace, pc, oracle=oracle, shard=shard)
+    if shard[0] == shard[1]:
+        res = ParallelResult([], 0, 0, 0.0, None)
+    else:
+        res = sim.simulate_parallel(trace, pc, oracle=oracle, shard=shard, n_total=n_total, base=base,
+                                    fetch_out=fetch_out)
     return res, all_reduce_totals(Totals.of(res.sub_results), device="cuda")

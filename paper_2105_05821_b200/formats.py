@@ -71,6 +71,15 @@ class Trace:
                      f(self.data_size), f(self.hist), f(self.truth), f(self.fetch_tick), self.config_hash)
 
     @staticmethod
+    def concat(parts: list["Trace"]) -> "Trace":
+        """The traces one after another (the simulator ignores fetch_tick)."""
+        if len(parts) == 1:
+            return parts[0]
+        f = lambda name: np.ascontiguousarray(np.concatenate([getattr(t, name) for t in parts]))
+        return Trace(f("pc"), f("op"), f("src"), f("dst"), f("has_data"), f("data_addr"), f("data_size"), f("hist"),
+                     f("truth"), f("fetch_tick"), parts[0].config_hash)
+
+    @staticmethod
     def from_records(rec: np.ndarray, config_hash: int = 0) -> "Trace":
         c = lambda x: np.ascontiguousarray(x)
         has = c(rec["has_data"] != 0).astype(np.uint8)

@@ -151,9 +151,17 @@ HEAD_GAIN = 200.0  # classification rows of fc2 are scaled by this (input sensit
 
 
 def synthetic_model(trace: Trace, seed: int = 1, regime: str = "default",
-                    config: CnnConfig | None = None) -> Model:
+                    config: CnnConfig | None = None, init_params=None) -> Model:
+    """``init_params(cfg, seed) -> f32[param_count]`` replaces the library's
+    ``init_weights`` (the CPU reference arm draws the same weights through
+    the oracle so that it never loads the product library)."""
     cfg = config or CnnConfig.preset_c3()
-    m = init_weights(cfg, norm_from_trace(trace), seed)
+    if init_params is None:
+        m = init_weights(cfg, norm_from_trace(trace), seed)
+    else:
+        n = cfg.param_count()
+        m = Model(cfg, norm_from_trace(trace), np.asarray(init_params(cfg, seed), np.float32).copy(),
+                  np.zeros(n, np.float32), np.zeros(n, np.float32), 0)
     p = m.params
     L = cfg.param_count()
     od, H = cfg.output_dim, cfg.fc_hidden
@@ -175,3 +183,36 @@ def synthetic_model(trace: Trace, seed: int = 1, regime: str = "default",
     b = np.r_[r["reg"], r["fetch"][: cfg.class_fetch], r["exec_"][: cfg.class_exec], r["store"][: cfg.class_store]]
     p[L - od:] = np.asarray(b, np.float32)
     return m
+
+
+# ---------------------------------------------------------------------------
+# c3 (BASELINE.json configs[2]): one global 100M-instruction trace partitioned
+# into 65,536 sub-traces (partition, parallel.cpp:9-24: base 1525, rem 57,600).
+# The trace is defined as 8 chunks, chunk j = synthetic_trace(len_j, 101 + j)
+# holding global sub-traces [8192 j, 8192 (j + 1)) — one 8-GPU shard each — so
+# a process builds only the chunks its shard touches.
+# ---------------------------------------------------------------------------
+C3_N, C3_K, C3_CHUNKS = 100_000_000, 65_536, 8
+
+
+def partition_start(n: int, k: int, i: int) -> int:
+    """First instruction of sub-trace i (parallel.cpp:9-24)."""
+    base, rem = divmod(n, k)
+    return i * base + min(i, rem)
+
+
+def c3_chunk_bounds() -> list[int]:
+    per = C3_K // C3_CHUNKS
+    return [partition_start(C3_N, C3_K, per * j) for j in range(C3_CHUNKS)] + [C3_N]
+
+
+def c3_trace_slice(lo: int, hi: int) -> Trace:
+    """Instructions [lo, hi) of the c3 global trace."""
+    b = c3_chunk_bounds()
+    parts = []
+    for j in range(C3_CHUNKS):
+        a, e = max(lo, b[j]), min(hi, b[j + 1])
+        if a < e:
+            t = synthetic_trace(b[j + 1] - b[j], seed=101 + j)
+            parts.append(t.slice(a - b[j], e - b[j]) if (a, e) != (b[j], b[j + 1]) else t)
+    return Trace.concat(parts)

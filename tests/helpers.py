@@ -75,3 +75,67 @@ SUB = ["instructions", "total_cycles", "sum_fetch", "delta", "drain_cycles", "ov
 def gpu_subs(pr) -> np.ndarray:
     return np.array([[getattr(s, f) if f != "empty" else int(s.empty) for f in SUB] for s in pr.sub_results],
                     dtype=np.uint64)
+
+
+class RefRng:
+    """The reference's ``Rng`` (common.hpp:27-66: xoshiro256** seeded by
+    splitmix64), so test inputs are drawn exactly as the reference tests draw
+    them (e.g. ``random_input``, test_cnn.cpp:16-21)."""
+
+    M = (1 << 64) - 1
+
+    @staticmethod
+    def splitmix64(x: int) -> int:
+        M = RefRng.M
+        x = (x + 0x9E3779B97F4A7C15) & M
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        return x ^ (x >> 31)
+
+    def __init__(self, seed: int):
+        self.s = []
+        x = seed & self.M
+        for _ in range(4):
+            x = self.splitmix64(x)
+            self.s.append(x)
+
+    @staticmethod
+    def _rotl(x: int, k: int) -> int:
+        return ((x << k) | (x >> (64 - k))) & RefRng.M
+
+    def next_u64(self) -> int:
+        s, M = self.s, self.M
+        result = (self._rotl((s[1] * 5) & M, 7) * 9) & M
+        t = (s[1] << 17) & M
+        s[2] ^= s[0]
+        s[3] ^= s[1]
+        s[1] ^= s[2]
+        s[0] ^= s[3]
+        s[2] ^= t
+        s[3] = self._rotl(s[3], 45)
+        return result
+
+    def next_double(self) -> float:
+        return float(self.next_u64() >> 11) * 2.0 ** -53
+
+    def next_symmetric(self, a: float) -> np.float32:
+        return np.float32((2.0 * self.next_double() - 1.0) * a)
+
+
+def tiny_config(channels: int = 4, seq: int = 8, conv=(6, 6), fc_hidden: int = 8) -> CnnConfig:
+    """``CnnConfig::tiny`` (cnn.cpp:283-291)."""
+    c = CnnConfig.preset_c3(seq - 1)
+    c.input_channels = channels
+    c.max_context = seq - 1
+    c.sequence_length = seq
+    c.conv_channels = list(conv)
+    c.fc_hidden = fc_hidden
+    return c
+
+
+def random_input(cfg: CnnConfig, seed: int) -> np.ndarray:
+    """``random_input`` (test_cnn.cpp:16-21): input_channels x (max_context+1)
+    values U[-1.5, 1.5] from the reference Rng."""
+    r = RefRng(seed)
+    return np.array([r.next_symmetric(1.5) for _ in range(cfg.input_channels * (cfg.max_context + 1))],
+                    np.float32)

@@ -13,15 +13,15 @@ from paper_2105_05821_b200.dist import Totals, all_reduce_totals, max_over_ranks
 
 
 def test_shard_range_covers_partition():
-    for k in (1, 5, 7, 1024, 65536):
+    for k in (1, 2, 5, 7, 1024, 65536):
         for world in (1, 2, 3, 8):
-            if world > k:
-                continue
             spans = [shard_range(k, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == k
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [e - b for b, e in spans]
             assert max(sizes) - min(sizes) <= 1
+            if world > k:  # extra ranks get an empty shard (and still join the all-reduce)
+                assert sizes.count(0) == world - k
 
 
 def _free_port():
@@ -67,3 +67,73 @@ def test_gloo_world2_totals_reduce():
         assert tot[0] == full_total and tot[1] == full_n == 3000
         assert tot[0] == tot[2] + tot[3] and tot[3] == tot[4] + tot[5]  # Eq. 1 identity survives the reduce
         assert tmax == 2.0
+
+
+def _gpu_worker(rank, world, port, q, k, precision):
+    """One rank of a world-`world` gloo group running the GPU library on its
+    shard (every rank on cuda:0: the box has one GPU)."""
+    import torch.distributed as dist
+
+    from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig, read_model, read_trace
+    from paper_2105_05821_b200.dist import simulate_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gold = __import__("conftest").GOLDEN
+        t = read_trace(gold / "mix_3000_s4.trace")
+        m = read_model(gold / "small_dataset.model")
+        pc = ParallelConfig(k=k, sim=SimConfig(max_context=m.config.max_context))
+        with GpuSimulator(0, precision) as g:
+            g.load_model(m)
+            b, e = shard_range(k, rank, world)
+            from paper_2105_05821_b200.api import partition_starts
+
+            starts = partition_starts(t.n, k) + [t.n]
+            # the rank holds only its own slice of the trace (base = its first instruction)
+            lo, hi = (starts[b], starts[e]) if b < e else (0, 0)
+            res, tot = simulate_sharded(g, t.slice(lo, hi) if b < e else t.slice(0, 0), pc, rank, world,
+                                        n_total=t.n, base=lo)
+            subs = [[s.instructions, s.total_cycles, s.sum_fetch, s.delta, s.drain_cycles,
+                     s.overflow_stall_cycles] for s in res.sub_results]
+            pf = res.predicted_fetch.tolist() if res.predicted_fetch is not None else []
+        q.put((rank, subs, pf, tot.as_list()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,k,precision", [(2, 5, "tf32x3"), (3, 2, "fp32")])
+def test_gloo_gpu_shards_match_single_process(world, k, precision):
+    """Each rank simulates its contiguous shard with the CUDA library from its
+    own trace slice; concatenated, the shards reproduce the single-process
+    sub-results and predicted fetch series bit-exactly, and the one
+    all-reduce gives the single-process totals (parallel.cpp:83-92).  world 3,
+    k 2 leaves one rank with no sub-traces (it still joins the collective)."""
+    from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig, read_model, read_trace
+
+    gold = __import__("conftest").GOLDEN
+    t = read_trace(gold / "mix_3000_s4.trace")
+    m = read_model(gold / "small_dataset.model")
+    pc = ParallelConfig(k=k, sim=SimConfig(max_context=m.config.max_context))
+    with GpuSimulator(0, precision) as g:
+        g.load_model(m)
+        full = g.simulate_parallel(t, pc)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, k, precision)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    subs = [row for _, s, _, _ in out for row in s]
+    pf = [v for _, _, f, _ in out for v in f]
+    want = [[s.instructions, s.total_cycles, s.sum_fetch, s.delta, s.drain_cycles, s.overflow_stall_cycles]
+            for s in full.sub_results]
+    assert subs == want
+    assert pf == full.predicted_fetch.tolist()
+    for _, _, _, tot in out:
+        assert tot[0] == full.total_cycles and tot[1] == t.n

@@ -115,6 +115,24 @@ def test_sequential_equals_k1_and_shards_compose(gpu, port):
     assert np.array_equal(np.concatenate([p.predicted_fetch for p in parts]), full.predicted_fetch)
 
 
+def test_write_ring_grows_on_auto(gpu, port):
+    """The reference's write queue is an unbounded deque: with write_ring on
+    auto (0) a queue longer than the default 2048-entry ring reruns with a
+    larger ring and matches the port bit-exactly; an explicit write_ring is
+    a hard bound (reported overflow)."""
+    g = gpu("fp32")
+    t = store_heavy(5, 12000, lat_hi=400)
+    first = int(np.flatnonzero(t.op[:, 2])[0])
+    t.truth[first, 2] = 50_000_000  # the head store blocks the in-order write queue
+    assert int(t.op[:, 2].sum()) > 2048
+    r = run_gpu(g, t, pcfg(1))
+    want = port.simulate(t, oracle=True, k=1)
+    assert gpu_subs(r).tolist() == want["subs"].tolist()
+    assert np.array_equal(r.predicted_fetch, want["predicted_fetch"])
+    with pytest.raises(IlsimError, match="write queue ring overflow"):
+        run_gpu(g, t, pcfg(1, write_ring=2048))
+
+
 def test_errors_and_validation(gpu):
     g = gpu("fp32")
     t = store_heavy(9, 3000, lat_hi=100000)
@@ -178,23 +196,44 @@ def test_input_tensor_store_heavy(gpu, port, golden):
 
 
 # ---- CNN: teacher-forced and free-running ------------------------------------
-def near_tie(y, tri_a, tri_b, cfg, norm):
-    """True when a decode disagreement is attributable to a near-tie: top-2
-    logit gap below 1e-4 relative, or regression within 1e-3 of a .5."""
+def tie_explained(y_ref, y_gpu, tri_ref, tri_gpu, cfg, norm):
+    """Why a decoded triple differs, or None when the difference is NOT
+    explained by the two forwards' output difference.  Absolute criteria
+    (no tolerance relative to the decoded value):
+      * a class flip needs the reference's top-2 logit gap to be at most
+        twice that head's largest |y_gpu - y_ref| (each logit moved by at
+        most that much, so only then can their order swap);
+      * a regression-path flip (both in the overflow class) must be to the
+        neighbouring integer, with the reference's de-normalised value within
+        sigma * (v + 1) * |dr| (1st-order expm1 propagation of the actual
+        regression output difference dr, x1.01) of the .5 rounding boundary.
+    Returns the gap that excused it (logit gap or distance to .5)."""
     heads = [(3, cfg.class_fetch, 0), (3 + cfg.class_fetch, cfg.class_exec, 1),
              (3 + cfg.class_fetch + cfg.class_exec, cfg.class_store, 2)]
+    gaps = []
     for h, (base, n, j) in enumerate(heads):
-        if tri_a[h] == tri_b[h]:
+        if tri_ref[h] == tri_gpu[h]:
             continue
-        lg = np.sort(y[base: base + n].astype(np.float64))
-        if lg[-1] - lg[-2] <= 1e-4 * max(1.0, abs(lg[-1])):
+        lr = y_ref[base: base + n].astype(np.float64)
+        lg = y_gpu[base: base + n].astype(np.float64)
+        cls_r, cls_g = int(np.argmax(lr)), int(np.argmax(lg))
+        if cls_r != cls_g:
+            top = np.sort(lr)
+            err = float(np.max(np.abs(lg - lr)))
+            if top[-1] - top[-2] <= 2.0 * err:
+                gaps.append(("logit", top[-1] - top[-2], err))
+                continue
+            return None
+        # both overflow class: regression rounding
+        sd, mu = norm[103 + j], norm[100 + j]
+        v = max(0.0, float(np.expm1(min(float(y_ref[j]) * sd + mu, 22.0))))
+        dr = abs(float(y_gpu[j]) - float(y_ref[j]))
+        dist = abs(v - np.floor(v) - 0.5)
+        if abs(int(tri_ref[h]) - int(tri_gpu[h])) == 1 and dist <= 1.01 * sd * (v + 1.0) * dr:
+            gaps.append(("regression", dist, dr))
             continue
-        z = min(float(y[j]) * norm[103 + j] + norm[100 + j], 22.0)
-        v = max(0.0, np.expm1(z))
-        if abs(v - np.floor(v) - 0.5) < 1e-3 * max(1.0, v):
-            continue
-        return False
-    return True
+        return None
+    return gaps
 
 
 @pytest.mark.parametrize("precision,rtol,exact", [("fp32", 2e-5, True), ("tf32x3", 1e-4, True),
@@ -210,9 +249,16 @@ def test_teacher_forced_predict(gpu, port, golden, precision, rtol, exact):
     err = np.abs(out - ref) / np.maximum(1.0, np.abs(ref))
     assert err.max() <= rtol, err.max()
     bad = [i for i in range(tri.shape[0]) if not np.array_equal(tri[i], want["cap_triples"][i])]
+    # the device decode of the device outputs must itself be the reference decode
+    assert np.array_equal(port.decode(m, out, want["cap_is_store"]), tri)
     if exact:
+        excused = []
         for i in bad:
-            assert near_tie(ref[i], tri[i], want["cap_triples"][i], m.config, m.norm), i
+            why = tie_explained(ref[i], out[i], want["cap_triples"][i], tri[i], m.config, m.norm)
+            assert why is not None, (i, ref[i], out[i], want["cap_triples"][i], tri[i])
+            excused.append((i, why))
+        print(f"{precision}: {len(excused)} of {tri.shape[0]} triples differ, all explained: {excused}")
+        assert len(excused) <= 0.01 * tri.shape[0], excused
     else:  # reduced precision: decode agreement is reported, not required exact
         assert len(bad) <= 0.05 * tri.shape[0], len(bad)
 
@@ -542,10 +588,11 @@ def test_overlapped_upload_matches_load_then_run(gpu, extra):
     assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
 
 
-@pytest.mark.parametrize("heads", [(6, 9, 12), (4, 4, 5)])
+@pytest.mark.parametrize("heads", [(6, 9, 12), (4, 4, 5), (20, 20, 20)])
 def test_fc2_head_sizes(gpu, port, golden, heads):
-    """Head sizes other than 10/10/10 (output_dim 30 and 16: FC2's od % 8
-    remainder is 6 and 0, spread over the warps): teacher-forced outputs vs the
+    """Head sizes other than 10/10/10 (output_dim 30, 16 and 63: FC2's od % 8
+    remainder is 6, 0 and 7, spread over the warps; 63 needs more than 48 KB
+    of shared memory in the final decode): teacher-forced outputs vs the
     port, the fused round bit-identical to the unfused one and within 0.1% of
     the CPU oracle."""
     g = gpu("tf32x3")
@@ -567,3 +614,91 @@ def test_fc2_head_sizes(gpu, port, golden, heads):
     assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
     full = port.simulate(t, m, k=16)
     assert abs(a.total_cycles - full["total_cycles"]) <= 1e-3 * full["total_cycles"]
+
+
+# ---- the reference's decode goldens on the device decode functions ----------
+def _decode_model(norm=None):
+    from helpers import model_from_params
+
+    cfg = small_config()
+    return model_from_params(cfg, np.zeros(cfg.param_count(), np.float32), norm)
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_decode_goldens_on_device(gpu, path):
+    """test_cnn.cpp:183-224 replayed on decode.cuh (path 0) and the fused
+    round's warp_decode_triple (path 1) through ilsim_gpu_decode_outputs."""
+    from paper_2105_05821_b200.formats import identity_norm
+
+    g = gpu("fp32")
+
+    def dec(vals, is_store=False, norm=None):
+        g.load_model(_decode_model(norm))
+        y = np.zeros((1, 33), np.float32)
+        for i, v in vals.items():
+            y[0, i] = v
+        return g.decode(y, np.array([is_store], np.uint8), path)[0]
+
+    assert dec({3 + 3: 2.0})[0] == 3                                          # argmax at c_3
+    assert dec({3 + 9: 5.0, 0: np.float32(np.log1p(20.4))})[0] == 20           # overflow -> regression
+    assert dec({3 + 9: 5.0, 0: -3.0})[0] == 0                                  # clamps at 0
+    assert dec({3: 1.5, 4: 1.5})[0] == 0                                       # exact tie -> smaller class
+    t = dec({13: 3.0, 23 + 7: 3.0})
+    assert t[1] == 1 and t[2] == 0                                             # exec floor 1, store masked
+    assert dec({13: 3.0, 23 + 7: 3.0}, is_store=True)[2] == 7
+    norm = identity_norm()
+    norm[100], norm[103] = 1.0, 0.5
+    assert dec({12: 5.0, 0: np.float32((np.log1p(18.0) - 1.0) / 0.5)}, norm=norm)[0] == 18
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_decode_device_equals_port(gpu, port, path):
+    """Bit-exact decode of the same head outputs on the device and in the
+    port (cnn.cpp:388-417): ties, overflow-class regression near .5
+    boundaries, NaN / inf logits and regressions, values past 22 and 4e9."""
+    from paper_2105_05821_b200.formats import identity_norm
+
+    rng = np.random.default_rng(7)
+    n = 4096
+    y = rng.normal(0, 2, (n, 33)).astype(np.float32)
+    y[::7, 3:13] = 1.25                                   # full ties
+    y[1::7, 12] = 50.0                                    # overflow class wins (fetch)
+    y[2::7, 22] = 50.0                                    # exec
+    y[3::7, 32] = 50.0                                    # store
+    y[1::7, 0] = rng.uniform(-5, 30, y[1::7, 0].shape)    # includes clamp at 22 and 4e9
+    y[2::7, 1] = np.float32(np.log1p(np.floor(rng.uniform(0, 900, y[2::7, 1].shape)) + 0.5))  # .5 boundaries
+    y[3::7, 2] = np.nan                                   # NaN regression in the overflow class
+    y[4::7, 3 + 4] = np.nan                               # NaN logit never wins
+    y[5::7, 13:23] = -np.inf
+    y[6::7, 23 + 9] = np.inf
+    y[6::7, 2] = np.inf
+    st = (rng.random(n) < 0.5).astype(np.uint8)
+    norm = identity_norm()
+    norm[100:103] = [0.7, 1.6, 0.4]
+    norm[103:106] = [0.6, 0.9, 1.2]
+    m = _decode_model(norm)
+    g = gpu("fp32")
+    g.load_model(m)
+    got = g.decode(y, st, path)
+    want = port.decode(m, y, st)
+    assert np.array_equal(got, want), np.nonzero((got != want).any(1))[0][:10]
+
+
+def test_forward_tiny_pin_gpu(gpu, port):
+    """The reference's forward pin (test_cnn.cpp:155-168: tiny config with
+    conv {7, 9}, init_weights(cfg, NormStats{}, seed), random_input from the
+    reference Rng, 1e-6 relative vs the straight-line double forward) through
+    ilsim_gpu_predict in fp32.  The device feature layout has 50 slots per
+    column, so the config is tiny(50, 16) instead of tiny(5, 16)."""
+    from helpers import model_from_params, random_input, tiny_config
+    from test_oracle import naive_forward
+
+    g = gpu("fp32")
+    for seed in (1, 2, 3):
+        cfg = tiny_config(50, 16, conv=(7, 9))
+        m = model_from_params(cfg, port.init_params(cfg, seed))
+        g.load_model(m)
+        x = random_input(cfg, seed + 100)
+        out, _ = g.predict(x[None, :], np.zeros(1, np.uint8))
+        want = naive_forward(cfg, m.params, x)
+        assert np.all(np.abs(out[0] - want) <= 1e-6 * np.maximum(1.0, np.abs(want))), (seed, out[0] - want)

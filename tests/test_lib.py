@@ -31,7 +31,7 @@ def test_exports_every_header_symbol(L):
     assert set(syms) == set(_lib.EXPORTS)
     for s in syms:
         assert hasattr(L, s), s
-    assert L.ilsim_gpu_abi_version() == 1
+    assert L.ilsim_gpu_abi_version() == _lib.ABI_VERSION == 2
 
 
 STRUCTS = {"ilsim_gpu_options": _lib.Options, "ilsim_trace_view": _lib.TraceView, "ilsim_cnn_config": _lib.CnnCfg,

@@ -6,7 +6,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from helpers import SUB, instr_trace, model_from_params, random_trace, small_config
+from helpers import SUB, instr_trace, model_from_params, random_input, random_trace, small_config, tiny_config
 from paper_2105_05821_b200.formats import CnnConfig, Model, identity_norm, read_model, read_trace
 
 GOLD = __import__("conftest").GOLDEN
@@ -154,6 +154,21 @@ def test_forward_matches_naive_double(port, seed):  # test_cnn.cpp:155-168
     for i in range(4):
         want = naive_forward(cfg, m.params, x[i])
         assert np.all(np.abs(y[i] - want) <= 1e-6 * np.maximum(1.0, np.abs(want)) * 50)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_forward_tiny_pin(port, seed):
+    """The reference's own forward pin, verbatim (test_cnn.cpp:155-168):
+    CnnConfig::tiny(5, 16) with conv {7, 9}, init_weights(cfg, NormStats{},
+    seed), random_input(cfg, seed + 100) from the reference Rng, every output
+    within 1e-6 relative of the straight-line double forward."""
+    cfg = tiny_config(5, 16, conv=(7, 9))
+    m = model_from_params(cfg, port.init_params(cfg, seed))
+    x = random_input(cfg, seed + 100)
+    y, _ = port.forward(m, x[None, :], np.zeros(1, np.uint8))
+    want = naive_forward(cfg, m.params, x)
+    assert y.shape[1] == want.size
+    assert np.all(np.abs(y[0] - want) <= 1e-6 * np.maximum(1.0, np.abs(want)))
 
 
 def test_init_weights_matches_reference_rule(port, golden):  # cnn.cpp:335-352
