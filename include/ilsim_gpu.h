@@ -11,9 +11,12 @@
  * "batch_max must be >= 1" (parallel.cpp:40).
  *
  * Threading: one context per GPU, one caller per context (the reference calls
- * predict from one thread, parallel.cpp:70-75).  Multi-GPU = one process per
- * GPU, each simulating a contiguous shard of the global partition
- * (ilsim_sim_config.shard_*); the caller sums the totals (NCCL all-reduce).
+ * predict from one thread, parallel.cpp:70-75).  Multi-GPU, either
+ *  - one process per GPU, each simulating a contiguous shard of the global
+ *    partition (ilsim_sim_config.shard_*) from its own slice of the trace
+ *    (ilsim_trace_view.base); the caller sums the totals (NCCL all-reduce), or
+ *  - one process, several GPUs: ilsim_gpu_group_* (one host thread per
+ *    device inside the library, results gathered in sub-trace order).
  */
 #ifndef ILSIM_GPU_H_
 #define ILSIM_GPU_H_
@@ -161,6 +164,27 @@ int ilsim_gpu_simulate_parallel(ilsim_gpu_ctx* ctx, const ilsim_trace_view* trac
  * NULL); triples: n x {fetch, execution, store}.                              */
 int ilsim_gpu_predict(ilsim_gpu_ctx* ctx, const float* inputs, uint64_t n, const uint8_t* is_store,
                       float* outputs, uint32_t* triples);
+
+/* ---- multi-device group (one process, several GPUs) -------------------------
+ * simulate_parallel (parallel.hpp:43-44) over a list of devices: the library
+ * owns one context and one host thread per device, shards the global
+ * partition contiguously (device i gets sub-traces [i*k/n ...), the first
+ * k % n devices one more), uploads each device only its slice of the view,
+ * and returns every sub-result in sub-trace order plus the summed totals
+ * (device_ms = the slowest device).  Results are identical for any device
+ * list (test_parallel.cpp:114-146).  A device may appear more than once (its
+ * shards then run concurrently on separate streams).                         */
+typedef struct ilsim_gpu_group ilsim_gpu_group;
+int ilsim_gpu_group_create(const ilsim_gpu_options* opts, const int32_t* devices, int32_t n_devices,
+                           ilsim_gpu_group** out, char* err, int errlen);
+void ilsim_gpu_group_destroy(ilsim_gpu_group* group);
+const char* ilsim_gpu_group_last_error(const ilsim_gpu_group* group);
+int ilsim_gpu_group_size(const ilsim_gpu_group* group);
+int ilsim_gpu_group_load_model(ilsim_gpu_group* group, const ilsim_cnn_config* cfg, const double* norm,
+                               const float* params, uint64_t n_params);
+int ilsim_gpu_group_simulate_parallel(ilsim_gpu_group* group, const ilsim_trace_view* trace,
+                                      const ilsim_sim_config* cfg, ilsim_sub_result* subs, uint64_t sub_cap,
+                                      uint32_t* predicted_fetch, ilsim_totals* totals);
 
 /* Test hook: hybrid decode (decode_hybrid, cnn.cpp:388-417) of caller head
  * outputs (n x output_dim floats, the ilsim_gpu_predict output layout) with

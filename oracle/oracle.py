@@ -31,6 +31,9 @@ class OracleError(RuntimeError):
 def build(ref: bool = True) -> None:
     """Build the port (always) and the reference library (when the sources exist)."""
     targets = ["port"] + (["ref"] if ref and REF_SRC.exists() else [])
+    gpu_lib = HERE.parent / "paper_2105_05821_b200" / "libilsim_gpu.so"
+    if "ref" in targets and gpu_lib.exists():
+        targets.append("dropin")  # the C++ drop-in test driver (tests/cpp/dropin_main.cpp)
     env = dict(os.environ)
     env.pop("CXXFLAGS", None)
     subprocess.run(["make", "-s", "-C", str(HERE), "-j8", *targets], check=True, env=env)

@@ -8,6 +8,7 @@ reference interface over it.
 from .errors import IlsimError
 from .formats import CnnConfig, Model, Trace, identity_norm, read_model, read_trace, write_model, write_trace
 from .api import (
+    GpuGroup,
     GpuSimulator,
     ParallelConfig,
     ParallelResult,
@@ -22,6 +23,7 @@ from .api import (
 
 __all__ = [
     "CnnConfig",
+    "GpuGroup",
     "GpuSimulator",
     "IlsimError",
     "Model",

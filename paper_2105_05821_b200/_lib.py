@@ -117,6 +117,12 @@ EXPORTS = [
     "ilsim_gpu_predict",
     "ilsim_gpu_set_capture",
     "ilsim_gpu_decode_outputs",
+    "ilsim_gpu_group_create",
+    "ilsim_gpu_group_destroy",
+    "ilsim_gpu_group_last_error",
+    "ilsim_gpu_group_size",
+    "ilsim_gpu_group_load_model",
+    "ilsim_gpu_group_simulate_parallel",
     "ilsim_gpu_partition",
     "ilsim_gpu_model_flops",
     "ilsim_gpu_param_count",
@@ -153,6 +159,15 @@ def lib() -> C.CDLL:
     L.ilsim_gpu_predict.argtypes = [vp, vp, u64, vp, vp, vp]
     L.ilsim_gpu_set_capture.argtypes = [vp, C.c_uint32, vp, u64]
     L.ilsim_gpu_decode_outputs.argtypes = [vp, vp, u64, vp, vp, i32]
+    L.ilsim_gpu_group_create.argtypes = [C.POINTER(Options), vp, i32, C.POINTER(vp), C.c_char_p, C.c_int]
+    L.ilsim_gpu_group_destroy.argtypes = [vp]
+    L.ilsim_gpu_group_destroy.restype = None
+    L.ilsim_gpu_group_last_error.argtypes = [vp]
+    L.ilsim_gpu_group_last_error.restype = C.c_char_p
+    L.ilsim_gpu_group_size.argtypes = [vp]
+    L.ilsim_gpu_group_load_model.argtypes = [vp, C.POINTER(CnnCfg), vp, vp, u64]
+    L.ilsim_gpu_group_simulate_parallel.argtypes = [vp, C.POINTER(TraceView), C.POINTER(SimCfg), vp, u64, vp,
+                                                    C.POINTER(Totals)]
     L.ilsim_gpu_partition.argtypes = [u64, u64, vp, C.c_char_p, C.c_int]
     L.ilsim_gpu_model_flops.argtypes = [C.POINTER(CnnCfg)]
     L.ilsim_gpu_model_flops.restype = u64
@@ -162,7 +177,9 @@ def lib() -> C.CDLL:
     for f in (L.ilsim_gpu_create, L.ilsim_gpu_load_model, L.ilsim_gpu_load_trace, L.ilsim_gpu_load_trace_records,
               L.ilsim_gpu_run,
               L.ilsim_gpu_simulate_parallel, L.ilsim_gpu_predict, L.ilsim_gpu_set_capture,
-              L.ilsim_gpu_partition, L.ilsim_gpu_init_weights, L.ilsim_gpu_decode_outputs):
+              L.ilsim_gpu_partition, L.ilsim_gpu_init_weights, L.ilsim_gpu_decode_outputs,
+              L.ilsim_gpu_group_create, L.ilsim_gpu_group_size, L.ilsim_gpu_group_load_model,
+              L.ilsim_gpu_group_simulate_parallel):
         f.restype = i32
     _lib = L
     return L

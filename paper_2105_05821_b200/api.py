@@ -388,6 +388,74 @@ class GpuSimulator:
         self._check(self.L.ilsim_gpu_set_capture(self._h, 0xFFFFFFFF, None, 0))
 
 
+class GpuGroup:
+    """Several GPUs of one process behind one ``simulate_parallel``
+    (ilsim_gpu_group_*: one host thread per device inside the library, the
+    partition sharded contiguously, results gathered in sub-trace order)."""
+
+    def __init__(self, devices: list[int], precision: str = "tf32x3"):
+        if precision not in _lib.PREC:
+            raise IlsimError("unknown precision: " + precision)
+        self.L = _lib.lib()
+        self.devices = list(devices)
+        dev = (C.c_int32 * len(self.devices))(*self.devices)
+        opts = _lib.Options(self.devices[0] if self.devices else 0, _lib.PREC[precision])
+        h = C.c_void_p()
+        err = C.create_string_buffer(_ERRLEN)
+        if self.L.ilsim_gpu_group_create(C.byref(opts), dev, len(self.devices), C.byref(h), err, _ERRLEN) != 0:
+            raise IlsimError(_err(err))
+        self._h = h
+        self.model: Model | None = None
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self.L.ilsim_gpu_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, rc: int) -> None:
+        if rc != 0:
+            raise IlsimError(self.L.ilsim_gpu_group_last_error(self._h).decode(errors="replace"))
+
+    def load_model(self, model: Model | str) -> None:
+        if isinstance(model, str):
+            model = read_model(model)
+        cfg = _cnn_cfg(model.config)
+        norm = np.ascontiguousarray(model.norm, dtype=np.float64)
+        params = np.ascontiguousarray(model.params, dtype=np.float32)
+        self._check(self.L.ilsim_gpu_group_load_model(self._h, C.byref(cfg), norm.ctypes.data, params.ctypes.data,
+                                                      params.size))
+        self.model = model
+
+    def simulate_parallel(self, trace: Trace, pc: ParallelConfig | None = None, *, oracle=False,
+                          sequential=False) -> ParallelResult:
+        pc = pc or ParallelConfig()
+        cfg = GpuSimulator._sim_cfg(self, pc, sequential=sequential, oracle=oracle)
+        view, keep = trace_view(trace, with_truth=oracle)
+        n = trace.n
+        k = GpuSimulator._num_sub(pc, n, sequential)
+        subs = (_lib.SubResult * k)()
+        pf = np.zeros(max(n, 1), dtype=np.uint32) if pc.sim.record_fetch else None
+        tot = _lib.Totals()
+        self._check(self.L.ilsim_gpu_group_simulate_parallel(self._h, C.byref(view), C.byref(cfg), subs, k,
+                                                             pf.ctypes.data if pf is not None else None,
+                                                             C.byref(tot)))
+        del keep
+        starts = partition_starts(n, k) if n > 0 else [0]
+        return GpuSimulator._collect(subs, int(tot.sub_traces), pf, n, tot, starts, 0, pc)
+
+
 def throughput_csv(rows: list[tuple[int, int, float]]) -> str:
     """``throughput_csv`` (parallel.cpp:95-105); rows are (k, instructions, seconds)."""
     out = ["k,instructions,seconds,mips"]

@@ -9,6 +9,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ilsim_gpu.h"
@@ -987,6 +988,135 @@ int ilsim_gpu_init_weights(const ilsim_cnn_config* cfg, uint64_t seed, float* pa
     return 0;
   } catch (const std::exception& e) {
     put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-device group: the C++ drop-in for simulate_parallel over several GPUs
+// of one process (parallel.cpp:26-93 with the sub-traces sharded contiguously,
+// SURVEY.md §8(e)).  One context and one host thread per device; each thread
+// uploads only its shard's slice of the borrowed trace view and runs its
+// rounds; the per-sub-trace results land in the caller's arrays in sub-trace
+// order and the totals are summed on the host exactly as parallel.cpp:83-92
+// sums sub_results (integer sums: identical for any device count).
+// ---------------------------------------------------------------------------
+struct ilsim_gpu_group {
+  std::vector<ilsim_gpu_ctx*> ctx;
+  std::string err;
+};
+
+extern "C" {
+
+int ilsim_gpu_group_create(const ilsim_gpu_options* opts, const int32_t* devices, int32_t n_devices,
+                           ilsim_gpu_group** out, char* err, int errlen) {
+  try {
+    if (!out) throw ApiError("null output pointer");
+    if (n_devices < 1 || !devices) throw ApiError("a device group needs at least one device");
+    auto g = std::make_unique<ilsim_gpu_group>();
+    for (int32_t i = 0; i < n_devices; ++i) {
+      ilsim_gpu_options o = opts ? *opts : ilsim_gpu_options{};
+      o.device = devices[i];
+      ilsim_gpu_ctx* c = nullptr;
+      char e[512] = {0};
+      if (ilsim_gpu_create(&o, &c, e, sizeof(e)) != 0) {
+        for (auto* x : g->ctx) ilsim_gpu_destroy(x);
+        throw ApiError("device " + std::to_string(devices[i]) + ": " + e);
+      }
+      g->ctx.push_back(c);
+    }
+    *out = g.release();
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+void ilsim_gpu_group_destroy(ilsim_gpu_group* g) {
+  if (!g) return;
+  for (auto* c : g->ctx) ilsim_gpu_destroy(c);
+  delete g;
+}
+
+const char* ilsim_gpu_group_last_error(const ilsim_gpu_group* g) { return g ? g->err.c_str() : ""; }
+
+int ilsim_gpu_group_size(const ilsim_gpu_group* g) { return g ? static_cast<int>(g->ctx.size()) : 0; }
+
+int ilsim_gpu_group_load_model(ilsim_gpu_group* g, const ilsim_cnn_config* cfg, const double* norm,
+                               const float* params, uint64_t n_params) {
+  if (!g) return 1;
+  for (size_t i = 0; i < g->ctx.size(); ++i)
+    if (ilsim_gpu_load_model(g->ctx[i], cfg, norm, params, n_params) != 0) {
+      g->err = "device " + std::to_string(g->ctx[i]->device) + ": " + g->ctx[i]->err;
+      return 1;
+    }
+  g->err.clear();
+  return 0;
+}
+
+int ilsim_gpu_group_simulate_parallel(ilsim_gpu_group* g, const ilsim_trace_view* t, const ilsim_sim_config* cfg,
+                                      ilsim_sub_result* subs, uint64_t sub_cap, uint32_t* predicted_fetch,
+                                      ilsim_totals* totals) {
+  if (!g) return 1;
+  try {
+    if (!t || !cfg || !totals) throw ApiError("null argument");
+    if (cfg->shard_begin != 0 || cfg->shard_end != 0)
+      throw ApiError("a device group shards the partition itself (shard_begin / shard_end must be 0)");
+    *totals = ilsim_totals{};
+    const size_t nd = g->ctx.size();
+    // the global partition (validation errors with the reference's texts)
+    const Plan P = make_plan(*cfg, t->n);
+    const uint64_t k = cfg->sequential ? 1 : P.k;
+    if (t->n == 0 || cfg->sequential || nd == 1) {  // one device does it all (simcore.cpp:185-196)
+      if (ilsim_gpu_simulate_parallel(g->ctx[0], t, cfg, subs, sub_cap, predicted_fetch, totals) != 0)
+        throw ApiError(g->ctx[0]->err);
+      g->err.clear();
+      return 0;
+    }
+    if (k > sub_cap) throw ApiError("sub_cap too small");
+    std::vector<ilsim_totals> tot(nd);
+    std::vector<std::string> errs(nd);
+    std::vector<std::thread> th;
+    for (size_t d = 0; d < nd; ++d) {
+      // contiguous blocks, the first k % nd devices one sub-trace more (dist.shard_range)
+      const uint64_t base = k / nd, rem = k % nd;
+      const uint64_t sb = d * base + std::min<uint64_t>(d, rem);
+      const uint64_t se = sb + base + (d < rem ? 1 : 0);
+      if (sb == se) continue;
+      th.emplace_back([&, d, sb, se] {
+        ilsim_sim_config c = *cfg;
+        c.shard_begin = sb;
+        c.shard_end = se;
+        const uint64_t own0 = P.starts[sb];
+        if (ilsim_gpu_simulate_parallel(g->ctx[d], t, &c, subs + sb, se - sb,
+                                        predicted_fetch ? predicted_fetch + own0 : nullptr, &tot[d]) != 0)
+          errs[d] = "device " + std::to_string(g->ctx[d]->device) + ": " + g->ctx[d]->err;
+      });
+    }
+    for (auto& x : th) x.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw ApiError(e);
+    for (const auto& x : tot) {
+      totals->sub_traces += x.sub_traces;
+      totals->instructions += x.instructions;
+      totals->total_cycles += x.total_cycles;
+      totals->sum_fetch += x.sum_fetch;
+      totals->delta += x.delta;
+      totals->drain_cycles += x.drain_cycles;
+      totals->overflow_stall_cycles += x.overflow_stall_cycles;
+      totals->rounds = std::max(totals->rounds, x.rounds);
+      totals->device_ms = std::max(totals->device_ms, x.device_ms);  // the slowest device
+      for (int q = 0; q < 4; ++q) totals->kernel_ms[q] = std::max(totals->kernel_ms[q], x.kernel_ms[q]);
+      totals->launches += x.launches;
+    }
+    totals->cpi = totals->instructions ? static_cast<double>(totals->total_cycles) / totals->instructions : 0.0;
+    g->err.clear();
+    return 0;
+  } catch (const std::exception& e) {
+    g->err = e.what();
     return 1;
   }
 }

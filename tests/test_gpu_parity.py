@@ -702,3 +702,30 @@ def test_forward_tiny_pin_gpu(gpu, port):
         out, _ = g.predict(x[None, :], np.zeros(1, np.uint8))
         want = naive_forward(cfg, m.params, x)
         assert np.all(np.abs(out[0] - want) <= 1e-6 * np.maximum(1.0, np.abs(want))), (seed, out[0] - want)
+
+
+@pytest.mark.parametrize("devices,k,precision", [([0], 5, "tf32x3"), ([0, 0], 5, "tf32x3"), ([0, 0, 0], 17, "fp32"),
+                                                 ([0, 0, 0, 0], 3, "bf16")])
+def test_device_group_matches_single_context(gpu, devices, k, precision):
+    """ilsim_gpu_group_simulate_parallel (one host thread per listed device;
+    the box has one GPU, so the shards share it) reproduces the single-context
+    sub-results, predicted fetch series and totals bit-exactly for any device
+    list, including a device with no sub-traces (test_parallel.cpp:114-146)."""
+    from paper_2105_05821_b200 import GpuGroup
+
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    m = read_model(GOLD / "small_dataset.model")
+    pc = pcfg(k, mc=m.config.max_context)
+    g = gpu(precision)
+    g.load_model(m)
+    want = g.simulate_parallel(t, pc)
+    with GpuGroup(devices, precision) as grp:
+        grp.load_model(m)
+        got = grp.simulate_parallel(t, pc)
+        assert gpu_subs(got).tolist() == gpu_subs(want).tolist()
+        assert np.array_equal(got.predicted_fetch, want.predicted_fetch)
+        assert got.total_cycles == want.total_cycles and got.instructions == t.n
+        o = grp.simulate_parallel(t, pc, oracle=True)
+        assert o.instructions == t.n
+        with pytest.raises(IlsimError, match="batch_max must be >= 1"):
+            grp.simulate_parallel(t, pcfg(k, batch_max=0, mc=m.config.max_context))

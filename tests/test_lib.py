@@ -190,3 +190,33 @@ def test_trace_records_header_checks(tmp_path):
     (tmp_path / "short.trace").write_bytes(raw[:-5])
     with _pt.raises(IlsimError, match="trace truncated at record"):
         trace_records(tmp_path / "short.trace")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision,k,devices", [(1, 16, [0]), (0, 5, [0, 0]), (1, 7, [0, 0, 0])])
+def test_cpp_dropin_on_gpu(precision, k, devices):
+    """The C++ drop-in end to end on the GPU (tests/cpp/dropin_main.cpp, built
+    by `make -C oracle dropin` against the reference's own libraries): the
+    reference's simulate_parallel with CudaCnnPredictor plugged in, the
+    whole-loop simulate_parallel_gpu and the multi-device group, against the
+    reference's CPU CnnPredictor run (total cycles within 0.1%; group ==
+    single-device bit-exactly) and OraclePredictor (bit-exact)."""
+    import json
+    import subprocess
+
+    exe = ROOT / "oracle" / "_ref" / "ilsim_dropin"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/ilsim_dropin not built (needs /root/reference at build time)")
+    gold = __import__("conftest").GOLDEN
+    out = subprocess.run([str(exe), str(gold / "mix_3000_s4.trace"), str(gold / "small_dataset.model"), str(k),
+                          str(precision)] + [str(d) for d in devices], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    r = json.loads(out.stdout)
+    cpu = r["cpu"]
+    for name in ("plugin", "gpu", "group"):
+        assert r[name]["instructions"] == cpu["instructions"] == 3000
+        assert abs(r[name]["total_cycles"] - cpu["total_cycles"]) <= 1e-3 * cpu["total_cycles"], (name, r)
+    assert r["group"]["total_cycles"] == r["gpu"]["total_cycles"]
+    assert r["group"]["same_subs"] == r["group"]["subs"] == k and r["group"]["same_fetch"] == 3000
+    o = r["oracle_gpu"]
+    assert o["total_cycles"] == r["oracle_cpu"]["total_cycles"] and o["same_subs"] == k and o["same_fetch"] == 3000

@@ -4,7 +4,8 @@ with the Eigen-free restated forward) run ONCE in the CPU container on the
 exact bench workloads, stored as small fixtures under tests/golden/scale/,
 and compared with the GPU run inside bench.py / tools/configs.py.
 
-  python tools/scale_parity.py make [--only c2,c4,c3s] [--threads 8]
+  python tools/scale_parity.py make [--only c2,c4,c3s] [--threads 8]   (CPU, reference)
+  python tools/scale_parity.py gpu  [--only ...] [--precisions tf32x3,fp32,tf32,bf16,fp8]
 
 TEST INFRASTRUCTURE: `make` runs the CPU reference; the GPU side only reads
 the committed fixtures (the GPU box has no /root/reference).
@@ -173,13 +174,40 @@ def make(names, threads: int):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("cmd", choices=["make"])
+    p.add_argument("cmd", choices=["make", "gpu"])
     p.add_argument("--only", default="c2,c4,c3s")
     p.add_argument("--threads", type=int, default=0)
+    p.add_argument("--precisions", default="tf32x3,fp32,tf32,bf16,fp8")
     a = p.parse_args()
     import os
 
-    make([s.strip() for s in a.only.split(",")], a.threads or os.cpu_count() or 1)
+    names = [s.strip() for s in a.only.split(",")]
+    if a.cmd == "gpu":
+        gpu_sweep(names, [s.strip() for s in a.precisions.split(",")])
+    else:
+        make(names, a.threads or os.cpu_count() or 1)
+
+
+
+def gpu_sweep(names, precisions):
+    """GPU side: every precision on every fixture workload, one JSON line each
+    (the bf16 / fp8 / tf32 CPI errors against the reference that north_star
+    asks to be reported separately)."""
+    from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig
+
+    for name in names:
+        trace, model, w = build_workload(name)
+        digests = (trace_digest(trace), model_digest(model))
+        pc = ParallelConfig(k=w["k"], sim=SimConfig(max_context=model.config.max_context))
+        for prec in precisions:
+            with GpuSimulator(0, prec) as g:
+                g.load_model(model)
+                g.load_trace(trace, pc)
+                r = g.run(pc)
+            out = compare(name, r, digests=digests)
+            out.update(workload=name, precision=prec, gpu_mips=trace.n / (r.device_ms / 1e3) / 1e6,
+                       us_per_round=1e3 * r.device_ms / r.rounds)
+            print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
