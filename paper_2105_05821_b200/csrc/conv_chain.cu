@@ -7,7 +7,11 @@
 // activations ("flat", 4 KB per sample) leave the SM.
 //
 //   TMEM (f32 columns): conv0 4 tiles x 64 [0,256) | conv1 2 x 64 [256,384) |
-//                       conv2 64 [384,448)
+//                       conv2 64 [384,448);
+//   3xTF32: every tile's accumulator is 128 columns [Ahi.Whi | Ahi.Wlo + Alo.Whi]
+//   (the round front's stacked k-step, round_front.cu): conv0 t at 128t,
+//   conv1 u at 128u, conv2 at 256 (conv0 of the next item waits for the
+//   conv2 drain)
 //   SMEM: R1 128 KB  = conv0 input ring (4 stages of 16 KB chunk (+16 KB lo))
 //                      or the restaged A tile of conv1 / conv2
 //         R2  64 KB  = the current layer's weights (hi + lo), TMA-loaded
@@ -55,6 +59,10 @@ struct ChainShape {
   static constexpr uint32_t kWBytes = kC * 128 * kKChunks;     // one weight copy (hi or lo)
   static constexpr uint32_t kStage = 128 * 128;                // one A chunk
   static constexpr uint32_t kALo = kKChunks * kStage;          // offset of the lo copy of a restaged A
+  static constexpr uint32_t kWChunk = kC * 128 * (kSplit ? 2 : 1);  // per K chunk: hi rows (+ lo rows)
+  static constexpr uint32_t kAccW = kSplit ? 2 * kC : kC;
+  static constexpr uint32_t kConv1Col = kSplit ? 0 : 256;
+  static constexpr uint32_t kConv2Col = kSplit ? 256 : 384;
 };
 
 // Restage 64 accumulator columns of TMEM lane-row `tl` (one conv output row)
@@ -65,6 +73,12 @@ __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, int ar, int
   for (int c0 = 0; c0 < kC; c0 += 16) {
     float v[16];
     tmem_ld16(tl + c0, v);
+    if constexpr (S::kSplit) {  // + the cross half (Ahi.Wlo + Alo.Whi)
+      float x[16];
+      tmem_ld16(tl + kC + c0, x);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += x[i];
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + bias[c0 + i], 0.0f);
     if constexpr (kMode == kBF16) {
@@ -170,8 +184,8 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint64_t* b = &bar_w[layer];
     mbar_expect_tx(b, S::kWBytes * (S::kSplit ? 2u : 1u) / S::kKChunks * chunks);
     for (int c = 0; c < chunks; ++c) {
-      tma_load_2d(R2 + c * (kC * 128), hi, b, c * S::kElems, 0);
-      if (S::kSplit) tma_load_2d(R2 + S::kWBytes + c * (kC * 128), lo, b, c * S::kElems, 0);
+      tma_load_2d(R2 + c * S::kWChunk, hi, b, c * S::kElems, 0);
+      if (S::kSplit) tma_load_2d(R2 + c * S::kWChunk + kC * 128, lo, b, c * S::kElems, 0);
     }
   };
 
@@ -208,6 +222,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = instr_desc(mode_fmt(kMode), kC);
+      const uint32_t idesc2 = instr_desc(mode_fmt(kMode), 2 * kC);  // 3xTF32: Ahi x [Whi; Wlo]
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -215,12 +230,11 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       auto gemm_resident_a = [&](uint32_t d, int ksteps) {  // A restaged in R1, W in R2
         for (int s = 0; s < ksteps; ++s) {
           const int c = s >> 2, j = s & 3;
-          const uint32_t ao = c * S::kStage + j * 32, wo = c * (kC * 128) + j * 32;
+          const uint32_t ao = c * S::kStage + j * 32, wo = c * S::kWChunk + j * 32;
           const uint64_t ad = smem_desc_sw128(r1 + ao), bd = smem_desc_sw128(r2 + wo);
           if (S::kSplit) {
-            mma<kMode>(d, smem_desc_sw128(r1 + S::kALo + ao), bd, idesc, s > 0);
-            mma<kMode>(d, ad, smem_desc_sw128(r2 + S::kWBytes + wo), idesc, 1);
-            mma<kMode>(d, ad, bd, idesc, 1);
+            mma<kMode>(d, ad, bd, idesc2, s > 0);
+            mma<kMode>(d + kC, smem_desc_sw128(r1 + S::kALo + ao), bd, idesc, 1);
           } else {
             mma<kMode>(d, ad, bd, idesc, s > 0);
           }
@@ -230,21 +244,21 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         // conv0: 4 tiles of 128 rows (2 samples each) streamed through the ring
         mbar_wait(&bar_w[0], it & 1);
         if (it == 0) mark(4);
+        if (S::kSplit && it > 0) mbar_wait(&bar_out, (it - 1) & 1);  // conv0 tile 2 overwrites the conv2 columns
         tc_fence_after();
         for (int tile = 0; tile < 4; ++tile) {
-          const uint32_t d = tmem + tile * kC;
+          const uint32_t d = tmem + tile * S::kAccW;
           for (int kc = 0; kc < S::kK0Chunks; ++kc) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const int steps = kc == S::kK0Chunks - 1 ? S::kK0Steps - 4 * (S::kK0Chunks - 1) : 4;
             for (int j = 0; j < steps; ++j) {
               const uint32_t ao = su32(ringA) + stage * S::kStage + j * 32;
-              const uint32_t wo = r2 + kc * (kC * 128) + j * 32;
+              const uint32_t wo = r2 + kc * S::kWChunk + j * 32;
               const uint32_t acc = (kc == 0 && j == 0) ? 0u : 1u;
               if (S::kSplit) {
-                mma<kMode>(d, smem_desc_sw128(ao + kRing * S::kStage), smem_desc_sw128(wo), idesc, acc);
-                mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo + S::kWBytes), idesc, 1);
-                mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo), idesc, 1);
+                mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo), idesc2, acc);
+                mma<kMode>(d + kC, smem_desc_sw128(ao + kRing * S::kStage), smem_desc_sw128(wo), idesc, 1);
               } else {
                 mma<kMode>(d, smem_desc_sw128(ao), smem_desc_sw128(wo), idesc, acc);
               }
@@ -264,12 +278,12 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         mbar_wait(&bar_w[1], it & 1);
         if (it == 0) mark(7);
         tc_fence_after();
-        gemm_resident_a(tmem + 256, 4 * S::kKChunks);
+        gemm_resident_a(tmem + S::kConv1Col, 4 * S::kKChunks);
         mma_commit(&bar_m1a);
         mbar_wait(&bar_a[1], it & 1);
         if (it == 0) mark(8);
         tc_fence_after();
-        gemm_resident_a(tmem + 256 + kC, 4 * S::kKChunks);
+        gemm_resident_a(tmem + S::kConv1Col + S::kAccW, 4 * S::kKChunks);
         mma_commit(&bar_m1b);
         // conv2: one tile of 128 rows (8 samples)
         mbar_wait(&bar_a[2], it & 1);
@@ -278,7 +292,7 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         if (it == 0) mark(10);
         if (it > 0) mbar_wait(&bar_out, (it - 1) & 1);  // previous conv2 accumulator drained
         tc_fence_after();
-        gemm_resident_a(tmem + 384, 4 * S::kKChunks);
+        gemm_resident_a(tmem + S::kConv2Col, 4 * S::kKChunks);
         mma_commit(&bar_m2);
         if (it == 0) mark(11);
       }
@@ -302,7 +316,8 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         tc_fence_after();
         for (int t2 = 0; t2 < 2; ++t2) {
           // conv0 row m of tile (2*pass + t2) = (sample, pos) -> A1 row t2*64 + m/2, K half m%2
-          restage_row<kMode>(R1, tmem + lane_off + (2 * pass + t2) * kC, t2 * 64 + (m >> 1), (m & 1) * kC, sbias[0]);
+          restage_row<kMode>(R1, tmem + lane_off + (2 * pass + t2) * S::kAccW, t2 * 64 + (m >> 1), (m & 1) * kC,
+                             sbias[0]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
@@ -312,7 +327,8 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       mbar_wait(&bar_m1b, it & 1);
       tc_fence_after();
       for (int t2 = 0; t2 < 2; ++t2)
-        restage_row<kMode>(R1, tmem + lane_off + 256 + t2 * kC, t2 * 64 + (m >> 1), (m & 1) * kC, sbias[1]);
+        restage_row<kMode>(R1, tmem + lane_off + S::kConv1Col + t2 * S::kAccW, t2 * 64 + (m >> 1), (m & 1) * kC,
+                           sbias[1]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&bar_a[2]);
@@ -323,7 +339,13 @@ conv_chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const int sample = item * kItem + (m >> 4);
       for (int c0 = 0; c0 < kC; c0 += 16) {
         float v[16];
-        tmem_ld16(tmem + lane_off + 384 + c0, v);
+        tmem_ld16(tmem + lane_off + S::kConv2Col + c0, v);
+        if constexpr (S::kSplit) {
+          float x[16];
+          tmem_ld16(tmem + lane_off + S::kConv2Col + kC + c0, x);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += x[i];
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sbias[2][c0 + i], 0.0f);
         if (sample < p.samples) {

@@ -19,7 +19,11 @@
 // Per-row results are identical to the unfused path (ctx_kernel + TMA
 // conv_chain_kernel): every accumulator row depends only on its own A row.
 //
-//   TMEM (f32 columns): conv0 4 x 64 [0,256) | conv1 2 x 64 [256,384) | conv2 [384,448)
+//   TMEM (f32 columns): conv0 4 x 64 [0,256) | conv1 2 x 64 [256,384) | conv2 [384,448);
+//   3xTF32: every tile's accumulator is 128 columns, [Ahi.Whi | Ahi.Wlo + Alo.Whi]
+//   (one N = 128 MMA of Ahi against the stacked [Whi; Wlo] plus one N = 64
+//   MMA of Alo, summed by the epilogue): conv0 t at 128t, conv1 u at 128u
+//   (over conv0 tiles already restaged), conv2 at 256.
 //   SMEM: R1 128 KB  conv0 A tile (hi | lo) / restaged conv1 / conv2 A tile
 //         R2  64 KB  current layer's weights (hi | lo), TMA
 //         T   20 KB  column tables
@@ -96,6 +100,12 @@ struct Shape {
   static constexpr int kPadUnits = kMode == kFP8 ? 14 : (kMode == kBF16 ? 6 : 2);  // pairs of zeros after K = 100
   static constexpr int kKChunks = kMode == kFP8 ? 1 : (kMode == kBF16 ? 2 : 4);    // conv1/2 K = 128
   static constexpr uint32_t kWBytes = kC * 128 * kKChunks;  // one weight copy (hi or lo)
+  // 3xTF32 weights: per K chunk the 64 hi rows then the 64 lo rows (16 KB), so
+  // [Whi; Wlo] is one N = 128 B operand; other modes: one 8 KB chunk per K chunk
+  static constexpr uint32_t kWChunk = kC * 128 * (kSplit ? 2 : 1);
+  static constexpr uint32_t kAccW = kSplit ? 2 * kC : kC;     // TMEM columns per tile accumulator
+  static constexpr uint32_t kConv1Col = kSplit ? 0 : 256;     // conv1 tile u at kConv1Col + u * kAccW
+  static constexpr uint32_t kConv2Col = kSplit ? 256 : 384;
   static constexpr uint32_t kStage = 128 * 128;             // one A chunk (128 rows x 128 B)
   static constexpr uint32_t kALo = kKChunks * kStage;       // lo plane of a restaged A
   static constexpr uint32_t kA0Lo = 4 * kStage;             // lo plane of the conv0 A tile
@@ -171,10 +181,89 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
 //   conv2: natural (slot = position), so flat needs no reordering.
 __device__ __forceinline__ int conv1_slot(int p) { return (p & 1) ? 8 + ((p >> 1) ^ 4) : (p >> 1); }
 
+// 16 accumulator values (raw f32 bits, columns c0..c0+15 of the row) ->
+// bias + ReLU -> the next layer's A operand at row `ar`, K offset k0 + c0.
+template <int kMode>
+__device__ __forceinline__ void restage16(uint8_t* a, const uint32_t* raw, int c0, int ar, int k0,
+                                          const float* bias, float scale) {
+  using S = Shape<kMode>;
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float x = __uint_as_float(raw[i]);
+    if constexpr (kMode == kFP8) x *= scale;  // undo the weight scale
+    v[i] = fmaxf(x + bias[c0 + i], 0.0f);
+  }
+  if constexpr (kMode == kFP8) {  // 16 e4m3 values: one 16-B unit of row ar
+    uint4 pk;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      w[i] = static_cast<uint32_t>(fp8x2(v[4 * i], v[4 * i + 1])) |
+             (static_cast<uint32_t>(fp8x2(v[4 * i + 2], v[4 * i + 3])) << 16);
+    *reinterpret_cast<uint4*>(a + ar * 128 + ((((k0 + c0) >> 4) ^ (ar & 7)) << 4)) = pk;
+  } else if constexpr (kMode == kBF16) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint4 pk;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * h + 2 * i], v[8 * h + 2 * i + 1]);
+        w[i] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      const int k = k0 + c0 + 8 * h;
+      const int chunk = k >> 6, kk = k & 63;
+      *reinterpret_cast<uint4*>(a + chunk * (128 * 128) + ar * 128 + (((kk >> 3) ^ (ar & 7)) << 4)) = pk;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + c0 + 4 * q;
+      float4 hi;
+      if constexpr (S::kSplit) {
+        uint32_t u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) u[i] = (__float_as_uint(v[4 * q + i]) + 0x1000u) & 0xffffe000u;
+        hi = make_float4(__uint_as_float(u[0]), __uint_as_float(u[1]), __uint_as_float(u[2]), __uint_as_float(u[3]));
+        const float4 lo = make_float4(v[4 * q] - hi.x, v[4 * q + 1] - hi.y, v[4 * q + 2] - hi.z, v[4 * q + 3] - hi.w);
+        *reinterpret_cast<float4*>(a + S::kALo + sw128_f32(ar, k)) = lo;
+      } else {
+        hi = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      *reinterpret_cast<float4*>(a + sw128_f32(ar, k)) = hi;
+    }
+  }
+}
+
 template <int kMode>
 __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float* accv, int ar, int k0,
                                             const float* bias, float scale) {
   using S = Shape<kMode>;
+  if constexpr (S::kSplit) {
+    // [hi.hi | cross] accumulator: per 32 columns both halves in flight, one
+    // wait, summed (hi.hi + cross), restaged
+#pragma unroll
+    for (int h = 0; h < kC; h += 32) {
+      uint32_t raw[32];
+      if (accv) {  // accumulator row known in advance (shared memory), no TMEM read
+#pragma unroll
+        for (int i = 0; i < 32; ++i) raw[i] = __float_as_uint(accv[h + i]);
+      } else {
+        uint32_t x[32];
+        tmem_ld16_async(tl + h, raw);
+        tmem_ld16_async(tl + h + 16, raw + 16);
+        tmem_ld16_async(tl + kC + h, x);
+        tmem_ld16_async(tl + kC + h + 16, x + 16);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 32; ++i) raw[i] = __float_as_uint(__uint_as_float(raw[i]) + __uint_as_float(x[i]));
+      }
+      restage16<kMode>(a, raw, h, ar, k0, bias, scale);
+      restage16<kMode>(a, raw + 16, h + 16, ar, k0, bias, scale);
+    }
+    return;
+  }
   uint32_t raw[kC];
   if (accv) {  // accumulator row known in advance (shared memory), no TMEM read
 #pragma unroll
@@ -219,17 +308,7 @@ __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int k = k0 + c0 + 4 * q;
-        float4 hi;
-        if constexpr (S::kSplit) {
-          uint32_t u[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) u[i] = (__float_as_uint(v[4 * q + i]) + 0x1000u) & 0xffffe000u;
-          hi = make_float4(__uint_as_float(u[0]), __uint_as_float(u[1]), __uint_as_float(u[2]), __uint_as_float(u[3]));
-          const float4 lo = make_float4(v[4 * q] - hi.x, v[4 * q + 1] - hi.y, v[4 * q + 2] - hi.z, v[4 * q + 3] - hi.w);
-          *reinterpret_cast<float4*>(a + S::kALo + sw128_f32(ar, k)) = lo;
-        } else {
-          hi = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
+        const float4 hi = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         *reinterpret_cast<float4*>(a + sw128_f32(ar, k)) = hi;
       }
     }
@@ -352,8 +431,8 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         uint64_t* b = &bar_w[layer];
         mbar_expect_tx(b, S::kWBytes * (S::kSplit ? 2u : 1u) / S::kKChunks * chunks);
         for (int c = 0; c < chunks; ++c) {
-          tma_load_2d(R2 + c * (kC * 128), hi, b, c * S::kElems, 0);
-          if (S::kSplit) tma_load_2d(R2 + S::kWBytes + c * (kC * 128), lo, b, c * S::kElems, 0);
+          tma_load_2d(R2 + c * S::kWChunk, hi, b, c * S::kElems, 0);
+          if (S::kSplit) tma_load_2d(R2 + c * S::kWChunk + kC * 128, lo, b, c * S::kElems, 0);
         }
       };
       int it = 0;
@@ -464,18 +543,18 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = instr_desc(mode_fmt(kMode), kC);
+      const uint32_t idesc2 = instr_desc(mode_fmt(kMode), 2 * kC);  // 3xTF32: Ahi x [Whi; Wlo]
       const uint32_t r1 = su32(R1), r2 = su32(R2);
       uint32_t n_a0 = 0, n_a1 = 0;
       int it = 0;
       auto gemm = [&](uint32_t d, uint32_t alo, int ksteps) {  // A in R1 (lo plane at +alo), W in R2
         for (int s = 0; s < ksteps; ++s) {
           const int c = s >> 2, j = s & 3;
-          const uint32_t ao = c * S::kStage + j * 32, wo = c * (kC * 128) + j * 32;
+          const uint32_t ao = c * S::kStage + j * 32, wo = c * S::kWChunk + j * 32;
           const uint64_t ad = smem_desc_sw128(r1 + ao), bd = smem_desc_sw128(r2 + wo);
           if (S::kSplit) {
-            mma<kMode>(d, smem_desc_sw128(r1 + alo + ao), bd, idesc, s > 0);
-            mma<kMode>(d, ad, smem_desc_sw128(r2 + S::kWBytes + wo), idesc, 1);
-            mma<kMode>(d, ad, bd, idesc, 1);
+            mma<kMode>(d, ad, bd, idesc2, s > 0);                            // [hi.hi | hi.lo]
+            mma<kMode>(d + kC, smem_desc_sw128(r1 + alo + ao), bd, idesc, 1);  // cross half += lo.hi
           } else {
             mma<kMode>(d, ad, bd, idesc, s > 0);
           }
@@ -496,13 +575,12 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
                 tc_fence_after();
               }
               for (int s = 4 * c; s < 4 * c + 4 && s < S::kK0Steps; ++s) {
-                const uint32_t ao = c * S::kStage + (s & 3) * 32, wo = c * (kC * 128) + (s & 3) * 32;
+                const uint32_t ao = c * S::kStage + (s & 3) * 32, wo = c * S::kWChunk + (s & 3) * 32;
                 const uint64_t ad = smem_desc_sw128(r1 + ao), bd = smem_desc_sw128(r2 + wo);
-                const uint32_t d = tmem + t * kC;
+                const uint32_t d = tmem + t * S::kAccW;
                 if (S::kSplit) {
-                  mma<kMode>(d, smem_desc_sw128(r1 + S::kA0Lo + ao), bd, idesc, s > 0);
-                  mma<kMode>(d, ad, smem_desc_sw128(r2 + S::kWBytes + wo), idesc, 1);
-                  mma<kMode>(d, ad, bd, idesc, 1);
+                  mma<kMode>(d, ad, bd, idesc2, s > 0);
+                  mma<kMode>(d + kC, smem_desc_sw128(r1 + S::kA0Lo + ao), bd, idesc, 1);
                 } else {
                   mma<kMode>(d, ad, bd, idesc, s > 0);
                 }
@@ -520,7 +598,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
               mbar_wait(&bar_a0, n_a0++ & 1);
               tc_fence_after();
             }
-            gemm(tmem + t * kC, S::kA0Lo, S::kK0Steps);
+            gemm(tmem + t * S::kAccW, S::kA0Lo, S::kK0Steps);
             mma_commit(&bar_t0);
           }
         }
@@ -532,7 +610,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
           mbar_wait(&bar_a1, n_a1++ & 1);
           if (u == 0) mbar_wait(&bar_w[1], it & 1);
           tc_fence_after();
-          gemm(tmem + 256 + u * kC, S::kALo, 4 * S::kKChunks);
+          gemm(tmem + S::kConv1Col + u * S::kAccW, S::kALo, 4 * S::kKChunks);
           mma_commit(&bar_m1);
         }
         mma_commit(&bar_w1f);
@@ -540,7 +618,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         mbar_wait(&bar_a2, it & 1);
         mbar_wait(&bar_w[2], it & 1);
         tc_fence_after();
-        gemm(tmem + 384, S::kALo, 4 * S::kKChunks);
+        gemm(tmem + S::kConv2Col, S::kALo, 4 * S::kKChunks);
         mma_commit(&bar_m2);
       }
     }
@@ -820,7 +898,7 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         // conv0 tile t = 2u + half, row m = (sample m/16, slot m%16 = position
         // 16t + 2(m%8) + (m%16)/8) -> conv1 tile u, position 8*half + m%8, K half (m%16)/8
         const int t = 2 * u + half;
-        restage_row<kMode>(R1, tmem + lane_off + t * kC, t >= T ? s_zacc : nullptr,
+        restage_row<kMode>(R1, tmem + lane_off + t * S::kAccW, t >= T ? s_zacc : nullptr,
                            (m >> 4) * 16 + conv1_slot(8 * half + (m & 7)), ((m >> 3) & 1) * kC, sbias[0],
                            p.wscale[0]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -832,19 +910,26 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       tc_fence_after();
       mark(9);
       if (p.c1acc_out && item == 0 && warp == 0) {  // calibration: conv1 row (sample 0, position 0)
-        uint32_t raw[kC];
-#pragma unroll
-        for (int c0 = 0; c0 < kC; c0 += 16) tmem_ld16_async(tmem + lane_off + 256 + c0, raw + c0);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (lane == 0)
-          for (int c = 0; c < kC; ++c) p.c1acc_out[c] = __uint_as_float(raw[c]);
+#pragma unroll 1
+        for (int c0 = 0; c0 < kC; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + lane_off + S::kConv1Col + c0, v);
+          if constexpr (S::kSplit) {  // + the cross half
+            float x[16];
+            tmem_ld16(tmem + lane_off + S::kConv1Col + kC + c0, x);
+            for (int i = 0; i < 16; ++i) v[i] += x[i];
+          }
+          if (lane == 0)
+            for (int i = 0; i < 16; ++i) p.c1acc_out[c0 + i] = v[i];
+        }
       }
       // conv1 tile `half`, row m = (sample m/16, slot m%16 holding position
       // 16*half + p, conv1_slot(p) = m%16) -> conv2 row (m/16)*16 + 8*half + p/2, K half p%2
       {
         const int sl = m & 15;
         const int pair = sl < 8 ? sl : ((sl & 7) ^ 4);  // p / 2
-        restage_row<kMode>(R1, tmem + lane_off + 256 + half * kC, (half == 1 && n_c1 == 1) ? s_c1 : nullptr,
+        restage_row<kMode>(R1, tmem + lane_off + S::kConv1Col + half * S::kAccW,
+                           (half == 1 && n_c1 == 1) ? s_c1 : nullptr,
                            (m >> 4) * 16 + 8 * half + pair, (sl >> 3) * kC, sbias[1], p.wscale[1]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -864,8 +949,15 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
         // each warp TMA-stores its 32 x 32 box, rows past the batch clipped
         uint8_t* stg = R1 + kOutStage + half * S::kStage;
         float v[32];
-        tmem_ld16(tmem + lane_off + 384 + half * 32, v);
-        tmem_ld16(tmem + lane_off + 384 + half * 32 + 16, v + 16);
+        tmem_ld16(tmem + lane_off + S::kConv2Col + half * 32, v);
+        tmem_ld16(tmem + lane_off + S::kConv2Col + half * 32 + 16, v + 16);
+        if constexpr (S::kSplit) {  // + the cross half
+          float x[32];
+          tmem_ld16(tmem + lane_off + S::kConv2Col + kC + half * 32, x);
+          tmem_ld16(tmem + lane_off + S::kConv2Col + kC + half * 32 + 16, x + 16);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += x[i];
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(stg + m * 128 + ((q ^ (m & 7)) << 4)) =
@@ -882,7 +974,13 @@ round_front_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_consta
       }
       for (int c0 = half * 32; c0 < half * 32 + 32 && !out_tma; c0 += 16) {
         float v[16];
-        tmem_ld16(tmem + lane_off + 384 + c0, v);
+        tmem_ld16(tmem + lane_off + S::kConv2Col + c0, v);
+        if constexpr (S::kSplit) {
+          float x[16];
+          tmem_ld16(tmem + lane_off + S::kConv2Col + kC + c0, x);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += x[i];
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if constexpr (kMode == kFP8) v[i] *= p.wscale[2];
