@@ -138,6 +138,13 @@ def ncu_traffic(precision: str):
         return None
 
 
+def tc_peaks():
+    try:
+        return json.loads((ROOT / "profiles" / "peaks_tc.json").read_text())["dense_tflops"]
+    except (OSError, ValueError, KeyError):
+        return {}
+
+
 def peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -425,12 +432,20 @@ def main():
     launch_ms = dom_ms / rounds
     pk = peaks()
     if tc:
-        div = {"bf16": 1.0, "fp8": 0.5}.get(args.precision, 2.0)
-        peak_val = pk.get("bf16_tflops_sustained", 1365.8) / div
-        peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" + {1.0: "", 0.5: " x 2 (fp8 e4m3 rate)"}.get(
-            div, " / 2 (tf32 rate)")
+        # the tcgen05 dense pipe peak of this kind, measured on B200 by
+        # tools/probes/tc_peak.py (profiles/peaks_tc.json, sustained: the front
+        # runs inside a long step); fallback MEASURED_PEAKS.json bf16 (cuBLAS)
+        kind = {"bf16": "bf16", "fp8": "fp8"}.get(args.precision, "tf32")
+        tcp = tc_peaks().get(kind)
+        if tcp:
+            peak_val = tcp["sustained"]
+            peak_src = f"profiles/peaks_tc.json {kind} dense sustained (tcgen05 M=128 N=256, tools/probes/tc_peak.py)"
+        else:
+            div = {"bf16": 1.0, "fp8": 0.5}.get(args.precision, 2.0)
+            peak_val = pk.get("bf16_tflops_sustained", 1365.8) / div
+            peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained scaled (peaks_tc.json absent)"
         if args.precision == "tf32x3":
-            peak_src += "; 3xTF32 issues 3 tensor ops per algorithmic op"
+            peak_src += "; 3xTF32 issues 3 tf32 products per algorithmic multiply-add (fp32-faithful ceiling = peak / 3)"
     else:
         sm_mhz = pk.get("sm_max_mhz", 1965.0)
         peak_val, peak_src = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "derived FFMA peak 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
@@ -438,6 +453,7 @@ def main():
     roofline = {"bound": "tensor" if tc else "fp32-ffma", "kernel": dom_name, "achieved": achieved, "peak": peak_val,
                 "unit": "TFLOP/s", "frac": achieved / peak_val, "peak_source": peak_src,
                 "algorithmic_flops_per_launch": flops_launch, "launch_us": 1e3 * launch_ms,
+                "frac_of_3xtf32_ceiling": achieved / (peak_val / 3) if args.precision == "tf32x3" else None,
                 "traffic": ncu_traffic(args.precision)}
 
     # e2e through the public C-ABI with host buffers (pinned), copies inside

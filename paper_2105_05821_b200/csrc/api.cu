@@ -212,7 +212,10 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   const uint64_t K = P.se - P.sb;
   if (K > sub_cap) throw ApiError("sub_cap too small");
   const uint32_t pcap = next_pow2(static_cast<uint32_t>(mc));
-  const uint32_t wcap = next_pow2(cfg.write_ring > 0 ? static_cast<uint32_t>(cfg.write_ring) : 2048u);
+  // write ring: explicit, or auto = 2048 entries capped by the longest
+  // sub-trace (its write queue never holds more stores than it has
+  // instructions), so 1M short sub-traces do not reserve 96 KB each; an auto
+  // ring that overflows is regrown (run_growing_ring)
 
   // per-sub-trace initial state
   std::vector<SubState> hs(K);
@@ -231,6 +234,8 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     st.count_drain = (cfg.drain_trim && i + 1 < P.k) ? 0u : 1u;
     rounds = std::max(rounds, st.len);
   }
+  const uint32_t wcap =
+      next_pow2(cfg.write_ring > 0 ? static_cast<uint32_t>(cfg.write_ring) : std::min<uint32_t>(2048u, rounds + 1u));
   // Overlapped upload (simulate_parallel): round r reads trace position r of
   // every sub-trace (and older ones), so the trace goes up in windows of
   // positions, each copied (2-D copies over runs of equal-length sub-traces)

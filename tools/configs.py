@@ -3,10 +3,12 @@
 
   python tools/configs.py [--only c1,c3,c4,c5] [--precision tf32x3]
 
-c1  FC-only predictor (paper FC2), one sub-trace (sequential), GPU fp32 path,
-    next to the CPU oracle port on a bounded sample.
+c1  FC-only predictor (paper FC2), one sub-trace (sequential), 1M
+    instructions, GPU fp32 path, against the CPU run of the same config
+    (tests/golden/scale/c1_k1_ref.json, tools/cpu_long_refs.py).
 c3  per-GPU shard of the 8-GPU config: 100M instructions / 65,536 sub-traces
-    over 8 GPUs = 12.5M instructions as 8,192 sub-traces per GPU.
+    over 8 GPUs = 12.5M instructions as 8,192 sub-traces per GPU, with parity
+    against the reference fixture (tools/scale_parity.py).
 c4  memory-heavy regime (store head active, long queues, full contexts).
 c5  sub-trace count sweep x warm-up overlap x drain-trim: MIPS vs CPI error
     against the K=1 run with the same weights (acceptance_main.cpp:326-334).
@@ -19,8 +21,11 @@ import sys
 import time
 from pathlib import Path
 
+import numpy as np
+
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tools"))
 
 from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig  # noqa: E402
 from paper_2105_05821_b200.formats import CnnConfig, Model  # noqa: E402
@@ -39,30 +44,43 @@ def run(g, t, pc, reps=2):
     return r
 
 
+def _k1_ref(which):
+    p = ROOT / "tests" / "golden" / "scale" / f"{which}_k1_ref.json"
+    return json.loads(p.read_text()) if p.exists() else None
+
+
 def c1(args):
+    """FC-only predictor, one sub-trace, 1M instructions: the GPU fp32 path vs
+    the CPU run of the same configuration (tools/cpu_long_refs.py c1)."""
     from oracle.oracle import Port
+    from scale_parity import block_hashes, model_digest, trace_digest
 
     t = synthetic_trace(args.c1_n, 101)
+    port = Port()
     base = synthetic_model(synthetic_trace(200_000, 101), 1)
     cfg = CnnConfig.preset_fc2()
-    port = Port()
     m = Model(cfg, base.norm, port.init_params(cfg, 1))
     g = GpuSimulator(0, "fp32")
     g.load_model(m)
     pc = ParallelConfig(k=1, sim=SimConfig(max_context=cfg.max_context))
     r = run(g, t, pc, reps=1)
-    n_cpu = min(args.c1_n, 2000)
-    t0 = time.perf_counter()
-    want = port.simulate(t.slice(0, n_cpu), m, sequential=True)
-    cpu_s = time.perf_counter() - t0
-    emit({"config": "c1", "predictor": "FC2 5550-1024-33 (5,716,992 mults)", "precision": "fp32 (SIMT)",
-          "instructions": t.n, "sub_traces": 1, "gpu_mips": t.n / (r.device_ms / 1e3) / 1e6, "gpu_cpi": r.cpi,
-          "cpu_port_mips": n_cpu / cpu_s / 1e6, "cpu_sample_instructions": n_cpu,
-          "cpu_port_cpi_on_sample": want["total_cycles"] / n_cpu})
+    out = {"config": "c1", "predictor": "FC2 5550-1024-33 (5,716,992 mults)", "precision": "fp32 (SIMT)",
+           "instructions": t.n, "sub_traces": 1, "gpu_mips": t.n / (r.device_ms / 1e3) / 1e6, "gpu_cpi": r.cpi}
+    ref = _k1_ref("c1")
+    if ref and ref["instructions"] == t.n and ref["trace_digest"] == trace_digest(t) and \
+            ref["model_digest"] == model_digest(m):
+        got = block_hashes(r.predicted_fetch)
+        out.update(cpu_ref_cpi=ref["cpi"], cpu_ref_mips=ref["cpu_mips"], cpu_ref_impl=ref["impl"],
+                   cpi_error_percent=100.0 * (r.cpi - ref["cpi"]) / ref["cpi"],
+                   fetch_block_identical_frac=float((got == np.array(ref["fetch_blocks"], np.uint64)).mean()),
+                   gpu_over_cpu=out["gpu_mips"] / ref["cpu_mips"])
+    emit(out)
 
 
 def c3(args):
-    n, k = 12_500_000, 8192
+    from scale_parity import compare
+
+    n, k = 12_500_992, 8192  # rank 0's shard of the 100M / 65,536 partition (1526 instructions each)
     t = synthetic_trace(n, 101)
     m = synthetic_model(synthetic_trace(200_000, 101), 1)
     g = GpuSimulator(0, args.precision)
@@ -70,11 +88,13 @@ def c3(args):
     r = run(g, t, ParallelConfig(k=k, sim=SimConfig(max_context=m.config.max_context)))
     emit({"config": "c3 (per-GPU shard)", "precision": args.precision, "instructions": n, "sub_traces": k,
           "rounds": r.rounds, "mips_per_gpu": n / (r.device_ms / 1e3) / 1e6,
-          "us_per_round": 1e3 * r.device_ms / r.rounds, "cpi": r.cpi,
+          "us_per_round": 1e3 * r.device_ms / r.rounds, "cpi": r.cpi, "parity": compare("c3s", r, t, m),
           "note": "8 GPUs run 8 such shards with no communication until one all-reduce of the totals"})
 
 
 def c4(args):
+    from scale_parity import compare
+
     n, k = 2_000_000, 1024
     t = synthetic_trace(n, 101, kind="memory")
     m = synthetic_model(synthetic_trace(200_000, 101, kind="memory"), 1, regime="memory")
@@ -84,37 +104,46 @@ def c4(args):
     emit({"config": "c4 memory-heavy", "precision": args.precision, "instructions": n, "sub_traces": k,
           "mips": n / (r.device_ms / 1e3) / 1e6, "us_per_round": 1e3 * r.device_ms / r.rounds, "cpi": r.cpi,
           "overflow_stall_cycles": sum(s.overflow_stall_cycles for s in r.sub_results),
-          "drain_cycles": sum(s.drain_cycles for s in r.sub_results)})
+          "drain_cycles": sum(s.drain_cycles for s in r.sub_results), "parity": compare("c4", r, t, m)})
 
 
 def c5(args):
+    """Sub-trace count sweep on the c2 trace (10M instructions) up to 1M
+    sub-traces x warm-up overlap x drain-trim: owned-instruction MIPS vs the
+    CPI error against the reference's K = 1 run of the same trace and weights
+    (tools/cpu_long_refs.py c5; acceptance_main.cpp:326-334)."""
     n = args.c5_n
     t = synthetic_trace(n, 101)
     m = synthetic_model(synthetic_trace(200_000, 101), 1)
     g = GpuSimulator(0, args.precision)
     g.load_model(m)
     mc = m.config.max_context
-    ref = run(g, t, ParallelConfig(k=1, sim=SimConfig(max_context=mc)), reps=1)
-    emit({"config": "c5 reference", "precision": args.precision, "instructions": n, "sub_traces": 1, "cpi": ref.cpi,
-          "mips": n / (ref.device_ms / 1e3) / 1e6})
-    for k in (1024, 4096, 16384, 65536, 262144):
+    ref = _k1_ref("c5")
+    if ref and ref["instructions"] == n:
+        ref_cpi, ref_src = ref["cpi"], ref["impl"]
+    else:
+        r1 = run(g, t, ParallelConfig(k=1, sim=SimConfig(max_context=mc)), reps=1)
+        ref_cpi, ref_src = r1.cpi, f"GPU {args.precision} K=1"
+    emit({"config": "c5 reference", "instructions": n, "sub_traces": 1, "cpi": ref_cpi, "source": ref_src})
+    for k in (1024, 4096, 16384, 65536, 262144, 1048576):
         if k > n:
             continue
         for w in (0, 110, 500):
             for trim in (False, True):
                 pc = ParallelConfig(k=k, warmup=w, drain_trim=trim, sim=SimConfig(max_context=mc))
-                r = run(g, t, pc)
+                r = run(g, t, pc, reps=1)
                 emit({"config": "c5", "precision": args.precision, "instructions": n, "sub_traces": k, "warmup": w,
                       "drain_trim": trim, "mips_owned": n / (r.device_ms / 1e3) / 1e6, "rounds": r.rounds,
-                      "cpi": r.cpi, "cpi_error_pct_vs_k1": 100.0 * (r.cpi - ref.cpi) / ref.cpi})
+                      "us_per_round": 1e3 * r.device_ms / r.rounds,
+                      "cpi": r.cpi, "cpi_error_pct_vs_k1": 100.0 * (r.cpi - ref_cpi) / ref_cpi})
 
 
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="c1,c3,c4,c5")
     p.add_argument("--precision", default="tf32x3")
-    p.add_argument("--c1-n", type=int, default=20_000)
-    p.add_argument("--c5-n", type=int, default=1_000_000)
+    p.add_argument("--c1-n", type=int, default=1_000_000)
+    p.add_argument("--c5-n", type=int, default=10_000_000)
     args = p.parse_args()
     for name in args.only.split(","):
         globals()[name.strip()](args)
