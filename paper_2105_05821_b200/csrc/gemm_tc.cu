@@ -621,6 +621,7 @@ struct TcModel {
   TcWeights fc1;
   DevBuf w2t;   // fc2 weights transposed to [out_dim][hidden] (k contiguous)
   DevBuf part;  // split-K partials
+  DevBuf conv_part;  // split-K partials of conv layers wider than the resident weight slice
   DevBuf c1acc; // calibrated conv1 accumulator row of an all-constant window (fused front)
   DevBuf calib_out;
 };
@@ -700,6 +701,35 @@ int num_sms() {
   return g_num_sms;
 }
 
+// Split-K conv layer: out = ReLU(sum over q ascending of part[q] + bias) in a
+// fixed order (batch-independent), written f32 or bf16 like the unsplit
+// epilogue.  Four consecutive elements per thread.
+__global__ void conv_splitk_reduce_kernel(const float* part, int nsplit, uint64_t plane, const float* bias,
+                                          int cout, void* out, int out_bf16) {
+  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i >= plane) return;
+  float4 acc = *reinterpret_cast<const float4*>(part + i);
+  for (int q = 1; q < nsplit; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(part + q * plane + i);
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  const int col = static_cast<int>(i % cout);
+  float r[4] = {acc.x + bias[col], acc.y + bias[col + 1], acc.z + bias[col + 2], acc.w + bias[col + 3]};
+  for (int j = 0; j < 4; ++j) r[j] = fmaxf(r[j], 0.0f);
+  if (out_bf16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(r[0], r[1]), b = __floats2bfloat162_rn(r[2], r[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&a);
+    pk.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + i) = pk;
+  } else {
+    *reinterpret_cast<float4*>(static_cast<float*>(out) + i) = make_float4(r[0], r[1], r[2], r[3]);
+  }
+}
+
 void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
                  const CUtensorMap& out, const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
   num_sms();
@@ -724,15 +754,13 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
 TcModel* tc_model_create(const DevModel& m, const float* host_params, int precision, cudaStream_t s) {
   const ilsim_cnn_config& c = m.cfg;
   const int mode = mode_of(precision);
-  const int esz = mode == kBF16 ? 2 : 4;
   if (c.n_conv == 0) throw ApiError("tensor-core path: the FC-only predictor runs with precision fp32");
   // constraints of this kernel family (the FP32 SIMT path has none)
   int cin = c.input_channels;
   for (int l = 0; l < c.n_conv; ++l) {
-    const int k = 2 * cin;
+    // any input width: layers wider than kMaxChunks K chunks run split-K (tc_forward)
     if (c.conv[l] % 16 != 0 || (c.conv[l] > 128 && c.conv[l] % 128 != 0))
       throw ApiError("tensor-core path: conv channels must be multiples of 16 (and of 128 above 128)");
-    if ((k * esz + 127) / 128 > kMaxChunks) throw ApiError("tensor-core path: conv input width too large");
     cin = c.conv[l];
   }
   if (128 % (c.sequence_length / 2) != 0) throw ApiError("tensor-core path: sequence_length/2 must divide 128");
@@ -800,6 +828,21 @@ int fc1_cps(int mode) {
   return mode == kFP8 ? 2 : kMaxChunks;  // fp8: flat is 8 chunks -> 4 planes of 2
 }
 
+// Split-K conv layers (K wider than kMaxChunks chunks): the largest layer's
+// partial planes per sample (olen x cout x nsplit floats), 0 if none splits.
+uint64_t conv_split_floats_per_sample(const ilsim_cnn_config& c, int esz) {
+  uint64_t best = 0;
+  int cin = c.input_channels, len = c.sequence_length;
+  for (int l = 0; l < c.n_conv; ++l) {
+    const int olen = len / 2, k = 2 * cin;
+    const int nsplit = ((k * esz + 127) / 128 + kMaxChunks - 1) / kMaxChunks;
+    if (nsplit > 1) best = std::max<uint64_t>(best, static_cast<uint64_t>(olen) * c.conv[l] * nsplit);
+    cin = c.conv[l];
+    len = olen;
+  }
+  return best;
+}
+
 // Allocations the forward needs, done before any graph capture.
 void tc_prepare(const DevModel& m, uint64_t samples) {
   TcModel& t = *m.tc;
@@ -807,6 +850,10 @@ void tc_prepare(const DevModel& m, uint64_t samples) {
   const int total_chunks = (m.L.flat * esz + 127) / 128;
   const int nsplit = (total_chunks + fc1_cps(t.mode) - 1) / fc1_cps(t.mode);
   t.part.need(samples * static_cast<uint64_t>(m.cfg.fc_hidden) * nsplit * sizeof(float));
+  if (!t.chain) {
+    const uint64_t per = conv_split_floats_per_sample(m.cfg, esz);
+    if (per) t.conv_part.need(samples * per * sizeof(float));
+  }
 }
 
 bool tc_split_input(const TcModel* t) { return t->chain && t->mode == kTF32x3; }
@@ -864,7 +911,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.out_split_stride = plane;
     p.out_scale = t.fc1.inv_scale;
     p.trace = chain_trace_active();
-    if (total_chunks % per != 0) throw ApiError("tensor-core path: flat dim must be a multiple of 4 chunks");
+    // a last plane with fewer chunks reads TMA zero fill past the flat dim (exact zeros)
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
     // partial planes as a 3-D tensor [nsplit][samples][hidden]: the TMA store
     // clips rows past `samples` within each plane
@@ -1033,15 +1080,44 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     p.m = static_cast<int>(m_rows);
     p.m_tiles = static_cast<int>((m_rows + kBM - 1) / kBM);
     p.n = bn;
-    p.chunks = (k * esz + 127) / 128;
-    p.ksteps_last = ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
-    p.bias = P + m.L.b[l];
-    p.relu = 1;
-    p.out = fb.act[l];
+    // K wider than the resident weight slice (kMaxChunks 128-B chunks): split-K
+    // over grid z, f32 partial planes, then a fixed-order reduce + bias + ReLU.
+    // K past the tensor (the last split's tail) is TMA zero fill: exact zeros.
+    const int total_chunks = (k * esz + 127) / 128;
+    const int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
+    p.chunks = nsplit > 1 ? kMaxChunks : total_chunks;
+    p.ksteps_last = nsplit > 1 ? 4 : ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
+    p.stages = kStages;
+    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages) > 226 * 1024) --p.stages;
     p.ldo = cout;
-    p.out_bf16 = bf;
-    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, amap, p, cout / bn, 1, s);  // no TMA store
+    const uint64_t plane = m_rows * static_cast<uint64_t>(cout);
+    if (nsplit == 1) {
+      p.bias = P + m.L.b[l];
+      p.relu = 1;
+      p.out = fb.act[l];
+      p.out_bf16 = bf;
+    } else {
+      // this slice's own block (slices of one round run concurrently), prepared by tc_prepare
+      const uint64_t per = conv_split_floats_per_sample(c, esz);
+      if (t.conv_part.bytes < (fb.part_off + samples) * per * sizeof(float))
+        throw ApiError("internal: conv split-K buffer not prepared");
+      float* part = t.conv_part.as<float>() + fb.part_off * per;
+      p.bias = nullptr;
+      p.relu = 0;
+      p.out = part;
+      p.out_bf16 = 0;
+      p.out_split_stride = plane;
+    }
+    launch_mode(mode, amap, t.conv[l].map_hi, t.conv[l].map_lo, amap, p, cout / bn, nsplit, s);  // no TMA store
     ++launches;
+    if (nsplit > 1) {
+      const float* part_conv = static_cast<const float*>(p.out);
+      const uint64_t threads = plane / 4;
+      conv_splitk_reduce_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+          part_conv, nsplit, plane, P + m.L.b[l], cout, fb.act[l], bf);
+      CUDA_OK(cudaGetLastError());
+      ++launches;
+    }
     in = fb.act[l];
     cin = cout;
     len = olen;

@@ -198,6 +198,20 @@ class CnnConfig:
         return CnnConfig(max_context=max_context, sequence_length=max(seq, 1 << 3))
 
     @staticmethod
+    def preset_rb7(max_context: int = 110, channels: int = 384) -> "CnnConfig":
+        """A paper-scale residual CNN (PAPER.md:794-810 lists RB7, 93 MFLOPs):
+        seven residual conv blocks (cnn.cpp:54-57, 104-107) of `channels`
+        channels over the 128 padded columns (128 -> 1 positions), FC 256.
+        At 384 channels: 85,071,872 FLOPs per instruction (2 x model_flops).
+        The reference has no such preset, but its CnnConfig takes any
+        conv_channels list, so this is a reference-expressible model (ILMD
+        files round-trip) and the oracle port runs it unchanged."""
+        c = CnnConfig.preset_c3(max_context)
+        c.conv_channels = [channels] * 7
+        c.residual_blocks = True
+        return c
+
+    @staticmethod
     def preset_fc2(max_context: int = 110, hidden: int = 1024) -> "CnnConfig":
         """The paper's FC2 latency predictor: 5550 -> 1024 -> 33,
         5,716,992 multiplications.  No reference implementation (the reference's

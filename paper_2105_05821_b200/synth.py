@@ -168,10 +168,12 @@ def synthetic_model(trace: Trace, seed: int = 1, regime: str = "default",
     # Zero the hidden biases: U(+-1) biases (cnn.cpp:346 draws biases with
     # cols == 1) otherwise swamp the input signal and every decode is constant.
     off, cin = 0, cfg.input_channels
-    for cout in cfg.conv_channels:
+    for cout in cfg.conv_channels:  # tensor table order (cnn.cpp:293-315): w, b (, p)
         off += cout * 2 * cin
         p[off: off + cout] = 0.0
         off += cout
+        if cfg.residual_blocks:
+            off += cout * 2 * cin
         cin = cout
     off += H * cfg.flat_dim
     p[off: off + H] = 0.0

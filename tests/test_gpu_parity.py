@@ -729,3 +729,30 @@ def test_device_group_matches_single_context(gpu, devices, k, precision):
         assert o.instructions == t.n
         with pytest.raises(IlsimError, match="batch_max must be >= 1"):
             grp.simulate_parallel(t, pcfg(k, batch_max=0, mc=m.config.max_context))
+
+
+# ---- a paper-scale residual model (RB7-like, 84 MFLOPs) through the same kernels
+@pytest.mark.parametrize("precision,rtol", [("fp32", 1e-5), ("tf32x3", 1e-5), ("bf16", 5e-3)])
+def test_rb7_teacher_forced_and_free_running(gpu, port, golden, precision, rtol):
+    """Seven residual 384-channel conv blocks (CnnConfig.preset_rb7, the scale
+    of the paper's RB7): the tensor-core path runs the wide layers split-K
+    (K up to 768 per layer), the fp32 path SIMT.  Teacher-forced outputs vs
+    the port's forward, and a free-running simulation vs the port."""
+    g = gpu(precision)
+    cfg = CnnConfig.preset_rb7()
+    gm = golden["models"]["c3_mix_seed1"]
+    m = Model(cfg, np.array(gm["norm"]), port.init_params(cfg, 3))
+    g.load_model(m)
+    t = read_trace(GOLD / "mix_3000_s4.trace").slice(0, 400)
+    want = port.simulate(t, m, k=4, capture=200, capture_inputs=True, capture_outputs=True)
+    out, tri = g.predict(want["cap_inputs"], want["cap_is_store"])
+    ref = want["cap_outputs"]
+    err = np.abs(out - ref) / np.maximum(1.0, np.abs(ref))
+    print(f"rb7 {precision}: max rel err {err.max():.3g}, triples equal {np.mean((tri == want['cap_triples']).all(1)):.4f}")
+    assert err.max() <= rtol, err.max()
+    assert np.array_equal(port.decode(m, out, want["cap_is_store"]), tri)
+    r = run_gpu(g, t, pcfg(4), oracle=False)
+    tot, wtot = r.total_cycles, want["total_cycles"]
+    print(f"rb7 {precision}: total cycles {tot} vs port {wtot} ({100 * (tot - wtot) / wtot:+.3f}%)")
+    if precision != "bf16":
+        assert abs(tot - wtot) <= 1e-3 * wtot, (tot, wtot)

@@ -138,12 +138,31 @@ def c5(args):
                       "cpi": r.cpi, "cpi_error_pct_vs_k1": 100.0 * (r.cpi - ref_cpi) / ref_cpi})
 
 
+def rb7(args):
+    """A paper-scale model (RB7-like: 7 residual 384-channel conv blocks,
+    84 MFLOPs per instruction) through the same kernels: the generic
+    per-layer tensor-core path (split-K for the wide layers)."""
+    n, k = args.rb7_n, 1024
+    t = synthetic_trace(n, 101)
+    cfg = CnnConfig.preset_rb7()
+    m = synthetic_model(synthetic_trace(200_000, 101), 1, config=cfg)
+    g = GpuSimulator(0, args.precision)
+    g.load_model(m)
+    r = run(g, t, ParallelConfig(k=k, sim=SimConfig(max_context=cfg.max_context)), reps=1)
+    mflop = 84_361_728
+    emit({"config": "rb7-like (f2)", "precision": args.precision, "instructions": n, "sub_traces": k,
+          "mips": n / (r.device_ms / 1e3) / 1e6, "us_per_round": 1e3 * r.device_ms / r.rounds, "cpi": r.cpi,
+          "mflop_per_instruction": mflop / 1e6,
+          "achieved_tflops": n * mflop / (r.device_ms / 1e3) / 1e12})
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="c1,c3,c4,c5")
     p.add_argument("--precision", default="tf32x3")
     p.add_argument("--c1-n", type=int, default=1_000_000)
     p.add_argument("--c5-n", type=int, default=10_000_000)
+    p.add_argument("--rb7-n", type=int, default=200_000)
     args = p.parse_args()
     for name in args.only.split(","):
         globals()[name.strip()](args)
