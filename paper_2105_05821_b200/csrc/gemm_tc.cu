@@ -71,6 +71,8 @@ struct TcGemmParams {
                               // next to the accumulators) and the MMAs read A from there (SMEM: W only)
   int tma_out;                // f32 split-K partials through tmOut: CTAs owning one M tile stage the
                               // accumulator in the idle A ring and TMA-store it (coalesced, async)
+  int diag_skip_w;            // diagnostics (SIMNET_DIAG_FC1_SKIP_W, timing only: results are garbage):
+                              // no weight loads, to measure their share of FC1
 };
 
 template <int kMode, bool kAInTmem = false>
@@ -127,6 +129,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+
   const uint32_t tmem = tmem_slot;
   const int elems = mode_chunk_elems(kMode);  // elements per 128 B chunk
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -225,10 +228,14 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {
       // resident weights for this CTA's (N tile, K split)
-      mbar_expect_tx(&bar_w, p.chunks * bBytes * (kSplit ? 2u : 1u));
-      for (int c = 0; c < p.chunks; ++c) {
-        tma_load_2d(sW + c * bBytes, &tmB, &bar_w, (kc0 + c) * elems, ntile * p.n);
-        if (kSplit) tma_load_2d(sWlo + c * bBytes, &tmBlo, &bar_w, (kc0 + c) * elems, ntile * p.n);
+      if (p.diag_skip_w) {
+        mbar_arrive(&bar_w);
+      } else {
+        mbar_expect_tx(&bar_w, p.chunks * bBytes * (kSplit ? 2u : 1u));
+        for (int c = 0; c < p.chunks; ++c) {
+          tma_load_2d(sW + c * bBytes, &tmB, &bar_w, (kc0 + c) * elems, ntile * p.n);
+          if (kSplit) tma_load_2d(sWlo + c * bBytes, &tmBlo, &bar_w, (kc0 + c) * elems, ntile * p.n);
+        }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (tr) tr[12] = global_ns();  // the previous kernel's results are visible
@@ -911,6 +918,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.out_split_stride = plane;
     p.out_scale = t.fc1.inv_scale;
     p.trace = chain_trace_active();
+    p.diag_skip_w = std::getenv("SIMNET_DIAG_FC1_SKIP_W") != nullptr;
     // a last plane with fewer chunks reads TMA zero fill past the flat dim (exact zeros)
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
     // partial planes as a 3-D tensor [nsplit][samples][hidden]: the TMA store

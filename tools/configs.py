@@ -57,9 +57,8 @@ def c1(args):
 
     t = synthetic_trace(args.c1_n, 101)
     port = Port()
-    base = synthetic_model(synthetic_trace(200_000, 101), 1)
     cfg = CnnConfig.preset_fc2()
-    m = Model(cfg, base.norm, port.init_params(cfg, 1))
+    m = synthetic_model(synthetic_trace(200_000, 101), 1, config=cfg)
     g = GpuSimulator(0, "fp32")
     g.load_model(m)
     pc = ParallelConfig(k=1, sim=SimConfig(max_context=cfg.max_context))

@@ -43,9 +43,10 @@ def main():
     if a.which == "c1":
         n = a.n or 1_000_000
         t = synthetic_trace(n, 101)
-        base = synthetic_model(synthetic_trace(200_000, 101), 1, init_params=port.init_params)
-        cfg = CnnConfig.preset_fc2()
-        m = Model(cfg, base.norm, port.init_params(cfg, 1))
+        # the bench model recipe (synth.synthetic_model: reference init rule,
+        # hidden biases zeroed, head gains / biases for a DES-like regime)
+        m = synthetic_model(synthetic_trace(200_000, 101), 1, config=CnnConfig.preset_fc2(),
+                            init_params=port.init_params)
         r = port.simulate(t, m, sequential=True, threads=1)
         out = {"config": "c1", "predictor": "FC2 5550-1024-33", "impl": "oracle port (1 thread)",
                "instructions": n, "total_cycles": r["total_cycles"], "cpi": r["total_cycles"] / n,
