@@ -28,7 +28,7 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tools"))
 
 from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig  # noqa: E402
-from paper_2105_05821_b200.formats import CnnConfig, Model  # noqa: E402
+from paper_2105_05821_b200.formats import CnnConfig  # noqa: E402
 from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace  # noqa: E402
 
 
