@@ -242,8 +242,9 @@ __device__ __forceinline__ void restage_row(uint8_t* a, uint32_t tl, const float
   using S = Shape<kMode>;
   if constexpr (S::kSplit) {
     // [hi.hi | cross] accumulator: per 32 columns both halves in flight, one
-    // wait, summed (hi.hi + cross), restaged
-#pragma unroll
+    // wait, summed (hi.hi + cross), restaged; not unrolled (instruction-fetch
+    // stalls dominate this phase: one body is half the code)
+#pragma unroll 1
     for (int h = 0; h < kC; h += 32) {
       uint32_t raw[32];
       if (accv) {  // accumulator row known in advance (shared memory), no TMEM read
