@@ -346,9 +346,8 @@ def run_reference_impl(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(x["seconds"] for x in per_step),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"{args.config}: C3 CNN, {args.k} sub-traces, {args.regime} regime "
-                               f"(bounded steady-state CPU sample)",
-                   "sub_traces": args.k, "instructions_per_step": n_step},
+        "config": config_dict(args, world),  # the GPU arm's workload; each step times a bounded sample of it
+        "instructions_per_step": n_step,
         "cpu_baseline": dict(base, value=mips, min=vals[0], max=vals[-1]),
         "single_thread_k1": cpu_single_thread_k1(trace, model),
         "e2e": {"value": mips, "unit": "MIPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -360,6 +359,16 @@ def run_reference_impl(args):
 # ---------------------------------------------------------------------------
 # our implementation
 # ---------------------------------------------------------------------------
+def config_dict(args, world: int) -> dict:
+    """The workload both arms report (the reference arm times a bounded
+    steady-state sample of it, described in its cpu_baseline.sample)."""
+    n_all = args.n if args.config == "c3" else args.n * world
+    k = args.k if args.config == "c3" else args.k * world
+    return {"workload": workload_name(args, world), "precision": args.precision, "regime": args.regime,
+            "sub_traces": k, "instructions": n_all, "rounds": -(-args.n // args.k),
+            "l2": "trace+state > 126 MB L2 per step (no flush needed)"}
+
+
 def workload_name(args, world: int) -> str:
     if args.config == "c3":
         return (f"c3: C3 CNN predictor, one {args.n}-instruction trace as {args.k} sub-traces sharded over "
@@ -494,10 +503,7 @@ def main():
         "scaling": "strong" if args.config == "c3" else "weak",
         "vs_baseline": None, "dtype": "f32" if args.precision in ("fp32", "tf32x3") else ("e4m3" if args.precision == "fp8" else args.precision),
         "data": "synthetic trace + random-init C3 weights (reference init rule), resident in HBM",
-        "config": {"workload": workload_name(args, world), "precision": args.precision, "regime": args.regime,
-                   "sub_traces": args.k * world if args.config != "c3" else args.k,
-                   "instructions": n_all, "rounds": r0.rounds,
-                   "l2": "trace+state > 126 MB L2 per step (no flush needed)"},
+        "config": config_dict(args, world),
         "cpi": tot.cpi,
         "parity": parity,
         "wall_ms_per_step": 1e3 * wall / args.steps,
