@@ -756,3 +756,36 @@ def test_rb7_teacher_forced_and_free_running(gpu, port, golden, precision, rtol)
     print(f"rb7 {precision}: total cycles {tot} vs port {wtot} ({100 * (tot - wtot) / wtot:+.3f}%)")
     if precision != "bf16":
         assert abs(tot - wtot) <= 1e-3 * wtot, (tot, wtot)
+
+
+# ---- parity at BASELINE scale against the reference's own runs --------------
+@pytest.mark.parametrize("name,precision,exact", [("c4", "fp32", True), ("c2", "tf32x3", False),
+                                                  ("c4", "tf32x3", False)])
+def test_scale_parity_against_reference_fixture(gpu, name, precision, exact):
+    """The reference's simulate_parallel (oracle/_ref) was run once on the exact
+    bench workloads (tools/scale_parity.py, tests/golden/scale/): the fp32 path
+    must reproduce every per-sub-trace counter and every predicted-fetch block;
+    tf32x3 must be within 0.1% of the total cycles (acceptance_main.cpp:326-334)
+    with >= 99% of the fetch blocks identical."""
+    import sys
+
+    sys.path.insert(0, str(GOLD.parents[1] / "tools"))
+    from scale_parity import build_workload, compare, load_fixture
+
+    trace, model, w = build_workload(name)
+    g = gpu(precision)
+    g.load_model(model)
+    pc = pcfg(w["k"], mc=model.config.max_context)
+    g.load_trace(trace, pc, truth=False)
+    r = g.run(pc)
+    out = compare(name, r, trace, model)
+    print(name, precision, {k: out.get(k) for k in ("cpi_error_percent", "subtrace_identical_frac",
+                                                     "fetch_block_identical_frac")})
+    assert "error" not in out, out
+    assert out["within_0p1pct"], out
+    if exact:
+        fx = load_fixture(name)
+        assert gpu_subs(r).tolist() == fx["subs"].tolist()
+        assert out["fetch_block_identical_frac"] == 1.0
+    else:
+        assert out["fetch_block_identical_frac"] >= 0.99, out
