@@ -71,6 +71,7 @@ struct TcGemmParams {
                               // next to the accumulators) and the MMAs read A from there (SMEM: W only)
   int tma_out;                // f32 split-K partials through tmOut: CTAs owning one M tile stage the
                               // accumulator in the idle A ring and TMA-store it (coalesced, async)
+  int gx_max;                 // CTAs per (N tile, K split) group along M (0 = as many as fit the SMs)
   int diag_skip_w;            // diagnostics (SIMNET_DIAG_FC1_SKIP_W, timing only: results are garbage):
                               // no weight loads, to measure their share of FC1
 };
@@ -741,7 +742,8 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
                  const CUtensorMap& out, const TcGemmParams& p, int ny, int nz, cudaStream_t s) {
   num_sms();
   const int groups = ny * nz;
-  const int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
+  int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
+  if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
   const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0);
   if (mode == kFP8)
@@ -906,7 +908,10 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     // chunk ahead of the MMAs); with one tile per CTA the split sits on the
     // critical path and A from shared memory is faster (measured at K = 1024 / 8192)
     const int groups = (t.fc1.npad / fc_tile) * nsplit;
-    const int gx = std::max(1, std::min(p.m_tiles, std::max(1, num_sms() / groups)));
+    static const int fc1_gx = std::getenv("SIMNET_FC1_GX") ? std::atoi(std::getenv("SIMNET_FC1_GX")) : 0;
+    p.gx_max = fc1_gx;
+    int gx = std::max(1, std::min(p.m_tiles, std::max(1, num_sms() / groups)));
+    if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
     p.a_tmem = mode == kTF32x3 && p.n <= 128 && p.m_tiles > gx && !std::getenv("SIMNET_FC1_SS");
     p.stages = kStages;
     while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0) > 226 * 1024) --p.stages;
