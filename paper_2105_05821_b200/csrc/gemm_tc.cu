@@ -74,6 +74,8 @@ struct TcGemmParams {
   int gx_max;                 // CTAs per (N tile, K split) group along M (0 = as many as fit the SMs)
   int diag_skip_w;            // diagnostics (SIMNET_DIAG_FC1_SKIP_W, timing only: results are garbage):
                               // no weight loads, to measure their share of FC1
+  int tma_multi;              // f32 split-K partials through tmOut for CTAs that loop over M tiles: two
+                              // 16 KB staging buffers past the A ring, one 32-column group at a time
 };
 
 template <int kMode, bool kAInTmem = false>
@@ -90,6 +92,8 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint8_t* sA = sWlo + (kSplit ? p.chunks * bBytes : 0);   // [stages][16 KB]
   const int ns = p.stages > 0 ? p.stages : kStages;       // A ring depth
   uint8_t* sAlo = sA + ns * kAChunk;                       // tf32x3 only
+  // tma_multi: 2 x 16 KB epilogue staging past the A ring (and its lo plane)
+  uint8_t* sStg = sAlo + (kSplit && !kAInTmem ? ns * kAChunk : 0);
 
   __shared__ __align__(8) uint64_t bar_w;
   __shared__ __align__(8) uint64_t bar_full[kStages], bar_split[kStages], bar_empty[kStages];
@@ -185,6 +189,39 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (stamp) tr[19] = clock64();  // stores issued
       bulk_wait_read();  // staging read; the stores complete with the grid (dependents wait for it)
       if (stamp) tr[20] = clock64();  // staging read back
+    }
+  };
+  // CTAs looping over M tiles: accumulator `acc` of tile t, 32-column groups
+  // staged alternately in the two staging buffers (each warp its own 32 rows
+  // x 128 B, SWIZZLE_128B) and TMA-stored, instead of per-thread row stores
+  // (each of those touches 32 lines per instruction).  `ng` counts this
+  // warp's groups, so a buffer is rewritten only after the store issued two
+  // groups earlier has read it.
+  auto epilogue_tma_multi = [&](int t, int acc, uint32_t& ng) {
+    const int quad = warp & 3;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * p.n;
+    for (int c0 = 0; c0 < p.n; c0 += 32, ++ng) {
+      float v[32];
+      tmem_ld16(tl + c0, v);
+      tmem_ld16(tl + c0 + 16, v + 16);
+      if constexpr (kMode == kFP8) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= p.out_scale;
+      }
+      uint8_t* box = sStg + (ng & 1u) * kAChunk + quad * 32 * 128;
+      if (ng >= 2 && lane == 0) bulk_wait_read1();  // the store from this buffer two groups ago has read it
+      __syncwarp();
+      uint8_t* stg = box + lane * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(stg + ((q ^ (lane & 7)) << 4)) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&tmOut, box, ntile * p.n + c0, t * kBM + quad * 32, ks);
+        bulk_commit();
+      }
     }
   };
   auto epilogue = [&](int t, int acc, int cb, int ce) {
@@ -406,6 +443,8 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // epilogue warps 6..9: TMEM lane quadrant = warp % 4
     asm volatile("griddepcontrol.wait;" ::: "memory");
     int it = 0;
+    uint32_t ng = 0;
+    const bool multi_tma = !solo && p.tma_multi;
     for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
       mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
@@ -413,6 +452,8 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (tr && warp == 6 && lane == 0 && it == 0) tr[14] = clock64();  // accumulator complete
       if (tma_out)
         epilogue_tma(t, 0, p.n / 2);
+      else if (multi_tma)
+        epilogue_tma_multi(t, acc, ng);
       else
         epilogue(t, acc, 0, solo ? p.n / 2 : p.n);
       tc_fence_before();
@@ -422,6 +463,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tr[10] = global_ns();
       }
     }
+    if (multi_tma && lane == 0) bulk_wait_read();  // staging read (the stores complete with the grid)
   }
   tc_fence_before();
   __syncthreads();
@@ -692,11 +734,11 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
 }
 
-size_t smem_bytes(int mode, int n, int chunks, int stages, bool a_tmem = false) {
+size_t smem_bytes(int mode, int n, int chunks, int stages, bool a_tmem = false, bool tma_multi = false) {
   const size_t w = static_cast<size_t>(chunks) * n * 128 * (mode == kTF32x3 ? 2 : 1);
   const size_t a =
       static_cast<size_t>(stages > 0 ? stages : kStages) * kAChunk * (mode == kTF32x3 && !a_tmem ? 2 : 1);
-  return w + a + 1024;
+  return w + a + (tma_multi ? 2 * kAChunk : 0) + 1024;
 }
 
 int g_num_sms = 0;
@@ -745,7 +787,7 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
-  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0);
+  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0);
   if (mode == kFP8)
     launch_pdl_tag("layer_bf16", tc_layer_kernel<kFP8>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
   else if (mode == kBF16)
@@ -913,8 +955,14 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     int gx = std::max(1, std::min(p.m_tiles, std::max(1, num_sms() / groups)));
     if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
     p.a_tmem = mode == kTF32x3 && p.n <= 128 && p.m_tiles > gx && !std::getenv("SIMNET_FC1_SS");
+    // CTAs that loop over M tiles TMA-store their partial tiles through two
+    // staging buffers when those fit next to a full A ring (SIMNET_FC1_MULTI_DIRECT: row stores, A/B)
+    const bool multi_direct = std::getenv("SIMNET_FC1_MULTI_DIRECT") != nullptr;
+    p.tma_multi = p.m_tiles > gx && fc_tile % 32 == 0 && !multi_direct &&
+                  smem_bytes(mode, p.n, p.chunks, kStages, p.a_tmem != 0, true) <= 226 * 1024;
     p.stages = kStages;
-    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0) > 226 * 1024) --p.stages;
+    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0) > 226 * 1024)
+      --p.stages;
     p.bias = nullptr;
     p.relu = 0;
     p.out = part;

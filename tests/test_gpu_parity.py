@@ -417,22 +417,30 @@ def test_fc1_tma_store_matches_direct_store(gpu, port, golden, precision, monkey
         assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch), k
 
 
-def test_fc1_tmem_a_multi_tile(gpu, port, monkeypatch):
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_fc1_tmem_a_multi_tile(gpu, port, precision, monkeypatch):
     """FC1 CTAs looping over several M tiles (K > 9 x 128 sub-traces) take A
-    from tensor memory (3xTF32); results equal A read from shared memory, bit
-    for bit, and stay within 0.1% of the CPU oracle."""
-    g = gpu("tf32x3")
+    from tensor memory (3xTF32) and TMA-store their partial tiles through two
+    staging buffers; results equal A read from shared memory and per-thread
+    row stores, bit for bit (1500 sub-traces: CTAs with one and with two M
+    tiles, a partial last tile clipped by the tensor map), and stay within
+    0.1% of the CPU oracle."""
+    g = gpu(precision)
     m, t = _bench_like("default", n=24_000)
     g.load_model(m)
     pc = pcfg(1500)
     g.load_trace(t, pc)
-    monkeypatch.delenv("SIMNET_FC1_SS", raising=False)
+    toggles = ("SIMNET_FC1_SS", "SIMNET_FC1_MULTI_DIRECT")
+    for v in toggles:
+        monkeypatch.delenv(v, raising=False)
     a = g.run(pc)
-    monkeypatch.setenv("SIMNET_FC1_SS", "1")
-    b = g.run(pc)
-    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
-    want = port.simulate(t, m, k=1500)
-    assert abs(a.total_cycles - want["total_cycles"]) <= 1e-3 * want["total_cycles"]
+    for v in toggles:
+        monkeypatch.setenv(v, "1")
+        b = g.run(pc)
+        assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch), v
+    if precision == "tf32x3":
+        want = port.simulate(t, m, k=1500)
+        assert abs(a.total_cycles - want["total_cycles"]) <= 1e-3 * want["total_cycles"]
 
 
 @pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
