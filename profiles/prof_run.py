@@ -21,10 +21,15 @@ p.add_argument("--k", type=int, default=1024)
 p.add_argument("--regime", default="default")
 p.add_argument("--runs", type=int, default=1)
 p.add_argument("--unfused", action="store_true")
+p.add_argument("--model", default=None, help="ILMD model file instead of the synthetic one")
 a = p.parse_args()
 kind = "memory" if a.regime == "memory" else "mix"
 t = synthetic_trace(a.n, 101, kind=kind)
-m = synthetic_model(synthetic_trace(200_000, 101, kind=kind), 1, regime=a.regime)
+if a.model:
+    from paper_2105_05821_b200 import read_model
+    m = read_model(a.model)
+else:
+    m = synthetic_model(synthetic_trace(200_000, 101, kind=kind), 1, regime=a.regime)
 g = GpuSimulator(0, a.precision)
 g.load_model(m)
 pc = ParallelConfig(k=a.k, sim=SimConfig(max_context=m.config.max_context))
@@ -32,5 +37,6 @@ g.load_trace(t, pc)
 for _ in range(a.runs):
     r = g.run(pc, fused=not a.unfused)
 import os
-print(f"{a.precision}{' unfused' if a.unfused else ''} n={a.n} k={a.k}: {r.rounds} rounds, {r.device_ms:.1f} ms, "
+print(f"{a.precision}{' unfused' if a.unfused else ''}{' ' + a.model if a.model else ''} n={a.n} k={a.k}: "
+      f"{r.rounds} rounds, {r.device_ms:.1f} ms, CPI {r.total_cycles / a.n:.4f}, "
       f"{1000 * r.device_ms / max(r.rounds, 1):.2f} us/round, launches {r.launches}")

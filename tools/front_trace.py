@@ -4,16 +4,18 @@ os.environ["SIMNET_CHAIN_TRACE"] = "1"
 sys.path.insert(0, '/root/repo')
 from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, _lib
 from paper_2105_05821_b200.synth import synthetic_trace, synthetic_model
-N = int(os.environ.get("N", "300000")); t = synthetic_trace(N, 101); m = synthetic_model(synthetic_trace(200_000, 101), 1)
+N = int(os.environ.get("N", "300000")); t = synthetic_trace(N, 101)
+K = int(os.environ.get("K", "1024")); NC = min(148, (K + 7) // 8)
+m = synthetic_model(synthetic_trace(200_000, 101), 1)
 for prec in os.environ.get("PRECS", "tf32x3,bf16").split(","):
     g = GpuSimulator(0, prec); g.load_model(m)
-    pc = ParallelConfig(k=1024); g.load_trace(t, pc); g.run(pc)
+    pc = ParallelConfig(k=K); g.load_trace(t, pc); g.run(pc)
     W = 148 * 32 + 256 * 32 + 148 * 16
     full = np.zeros(W, np.int64)
     _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(full.ctypes.data), C.c_int(W))
     buf = full[:148 * 32]
-    tx = full[148 * 32 + 256 * 32:].reshape(148, 16)[:128].astype(np.float64)
-    tr = buf.reshape(148, 32)[:128].astype(np.float64)
+    tx = full[148 * 32 + 256 * 32:].reshape(148, 16)[:NC].astype(np.float64)
+    tr = buf.reshape(148, 32)[:NC].astype(np.float64)
     T = tr[:, 20]
     base = tr[:, :1]
     names = {0: "start", 15: "dep wait done", 16: "apply done (warp0)", 1: "table done", 2: "tile0 gathered",
