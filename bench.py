@@ -50,6 +50,14 @@ N_INSTR = 10_000_000
 K_SUB = 1024
 
 
+DEFAULT_WEIGHTS = "synthetic"
+TRAINED_MODEL = ROOT / "tests" / "golden" / "c3_trained.model"
+WEIGHTS_DESC = {
+    "synthetic": "random-init C3 weights (reference init rule, synth.py head-bias recipe)",
+    "trained": "C3 trained on the reference's DES traces (tests/golden/c3_trained.model, tests/golden/train_c3.py)",
+}
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -61,6 +69,10 @@ def parse():
     p.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
     p.add_argument("--instructions", dest="n", type=int, default=0, help="c2/c4 trace length (0 = the config's)")
     p.add_argument("--k", type=int, default=0, help="sub-traces per GPU (c2/c4) or global (c3); 0 = the config's")
+    p.add_argument("--weights", default=os.environ.get("SIMNET_WEIGHTS", DEFAULT_WEIGHTS),
+                   choices=["synthetic", "trained"],
+                   help="synthetic: reference init rule + head-bias recipe (synth.py); trained: the C3 trained "
+                        "on the reference's DES traces (tests/golden/c3_trained.model)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rounds", type=int, default=0, help="rounds in the CPU-baseline sample (0 = auto)")
     a = p.parse_args()
@@ -152,9 +164,13 @@ def peaks():
         return {}
 
 
-def model_for(regime: str, init_params=None):
+def model_for(regime: str, init_params=None, weights: str = "synthetic"):
     from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace
 
+    if weights == "trained":
+        from paper_2105_05821_b200.formats import read_model
+
+        return read_model(TRAINED_MODEL)
     kind = "memory" if regime == "memory" else "mix"
     return synthetic_model(synthetic_trace(200_000, seed=101, kind=kind), seed=1, regime=regime,
                            init_params=init_params)
@@ -165,17 +181,19 @@ def workload(args, rank: int, world: int, init_params=None):
     from paper_2105_05821_b200.dist import shard_range
     from paper_2105_05821_b200.synth import c3_trace_slice, partition_start, synthetic_trace
 
-    model = model_for(args.regime, init_params)
+    model = model_for(args.regime, init_params, args.weights)
     if args.config == "c3":
         sb, se = shard_range(args.k, rank, world)
         lo, hi = partition_start(args.n, args.k, sb), partition_start(args.n, args.k, se)
-        fixture = "c3s" if (sb == 0 and se >= 8192 and args.k == 65_536) else None
+        fixture = "c3s" if (sb == 0 and se >= 8192 and args.k == 65_536 and args.weights == "synthetic") else None
         return c3_trace_slice(lo, hi), model, args.n, lo, (sb, se), fixture
     kind = "memory" if args.regime == "memory" else "mix"
     trace = synthetic_trace(args.n, seed=101 + rank, kind=kind)
     fixture = None
     if rank == 0 and args.k == K_SUB:
         fixture = {("c2", N_INSTR): "c2", ("c4", 2_000_000): "c4"}.get((args.config, args.n))
+        if fixture and args.weights == "trained":
+            fixture += "t"
     return trace, model, args.n, 0, None, fixture
 
 
@@ -326,12 +344,12 @@ def run_reference_impl(args):
 
         subs = min(args.k, 1024)
         trace = c3_trace_slice(0, partition_start(args.n, args.k, subs))
-        model = model_for(args.regime, port.init_params)
+        model = model_for(args.regime, port.init_params, args.weights)
     else:
         from paper_2105_05821_b200.synth import synthetic_trace
 
         trace = synthetic_trace(args.n, seed=101, kind="memory" if args.regime == "memory" else "mix")
-        model = model_for(args.regime, port.init_params)
+        model = model_for(args.regime, port.init_params, args.weights)
     per_step, base = [], None
     for i in range(args.warmup + args.steps):
         b = cpu_reference(trace, model, args.n, args.k, r1=args.cpu_rounds)
@@ -365,6 +383,7 @@ def config_dict(args, world: int) -> dict:
     n_all = args.n if args.config == "c3" else args.n * world
     k = args.k if args.config == "c3" else args.k * world
     return {"workload": workload_name(args, world), "precision": args.precision, "regime": args.regime,
+            "weights": WEIGHTS_DESC[args.weights],
             "sub_traces": k, "instructions": n_all, "rounds": -(-args.n // args.k),
             "l2": "trace+state > 126 MB L2 per step (no flush needed)"}
 
@@ -502,7 +521,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
         "scaling": "strong" if args.config == "c3" else "weak",
         "vs_baseline": None, "dtype": "f32" if args.precision in ("fp32", "tf32x3") else ("e4m3" if args.precision == "fp8" else args.precision),
-        "data": "synthetic trace + random-init C3 weights (reference init rule), resident in HBM",
+        "data": f"synthetic trace + {WEIGHTS_DESC[args.weights]}, resident in HBM",
         "config": config_dict(args, world),
         "cpi": tot.cpi,
         "parity": parity,

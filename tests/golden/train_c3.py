@@ -41,7 +41,7 @@ import torch
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
-from oracle.oracle import Ref  # noqa: E402  (test infrastructure: fixture generation only)
+from oracle.oracle import Port, Ref  # noqa: E402  (test infrastructure: fixture generation only)
 from paper_2105_05821_b200.formats import CnnConfig, Model, read_model, read_trace, write_model, write_trace  # noqa: E402
 from paper_2105_05821_b200.formats import Trace  # noqa: E402
 
@@ -87,8 +87,8 @@ class C3(torch.nn.Module):
         out = []
         with torch.no_grad():
             for lin in list(self.convs) + [self.fc1, self.fc2]:
-                out.append(lin.weight.detach().cpu().numpy().T.reshape(-1))
-                out.append(lin.bias.detach().cpu().numpy().reshape(-1))
+                out.append(lin.weight.detach().float().cpu().numpy().T.reshape(-1))
+                out.append(lin.bias.detach().float().cpu().numpy().reshape(-1))
         return np.concatenate(out).astype(np.float32)
 
 
@@ -116,6 +116,10 @@ def main() -> None:
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--threads", type=int, default=8)
     ap.add_argument("--device", default="cuda" if torch.cuda.is_available() else "cpu")
+    ap.add_argument("--val-n", type=int, default=20_000, help="instructions per closed-loop validation trace")
+    ap.add_argument("--dagger", type=int, default=0,
+                    help="after each epoch, add this many closed-loop requests per training trace (the model's "
+                         "own simulation, K = 32) labelled with the DES latencies of their instructions")
     ap.add_argument("--out", default=str(ROOT / "tests" / "golden" / "c3_trained.model"))
     a = ap.parse_args()
     torch.manual_seed(0)
@@ -124,7 +128,7 @@ def main() -> None:
     work = Path(tempfile.mkdtemp(prefix="train_c3_"))
     t0 = time.time()
     # 1. DES traces (train: seeds 1..S; held out: seed 100), every workload kind
-    train_paths, held_paths = [], []
+    train_paths, held_paths, val_paths = [], [], []
     for kind in KINDS:
         for s in range(1, a.seeds + 1):
             pth = work / f"{kind}_{s}.trace"
@@ -133,6 +137,9 @@ def main() -> None:
         pth = work / f"{kind}_held.trace"
         ref.make_trace(kind, a.n_per_trace, 100_000 + KINDS.index(kind), pth)
         held_paths.append(pth)
+        pth = work / f"{kind}_val.trace"
+        ref.make_trace(kind, a.val_n, 50_000 + KINDS.index(kind), pth)
+        val_paths.append(pth)
     merged = work / "train_all.trace"
     parts, tick = [], 0
     for pth in train_paths:  # fetch ticks made monotonic across the seams (read by the dataset builder)
@@ -171,10 +178,28 @@ def main() -> None:
     opt = torch.optim.Adam(net.parameters(), lr=a.lr, betas=(0.9, 0.999), eps=1e-8)
     pad = cfg.sequence_length - (cfg.max_context + 1)
     rng = np.random.default_rng(0)
+    # Closed-loop validation selects the epoch (as the reference's validation loss does,
+    # cnn.cpp:540-566): the simulation feeds the model's own latencies back into its
+    # inputs, which teacher-forced loss does not see; score = mean |log(C3 / DES cycles)|
+    # over the validation traces, simulated by the oracle port (K = 32).
+    port = Port()
+    val = [(read_trace(pth), ref.simulate(pth, None, sequential=True, n_hint=a.val_n)["total_cycles"])
+           for pth in val_paths]
+
+    def closed_loop_score(params):
+        m = Model(cfg, init.norm, params)
+        errs = []
+        for t, des in val:
+            tot = port.simulate(t, m, k=32)["total_cycles"]
+            errs.append(abs(np.log(max(tot, 1) / des)))
+        return float(np.mean(errs)), errs
+
+    best = (float("inf"), init.params, -1)
+    n_all = X.shape[0]
     for ep in range(a.epochs):
-        perm = rng.permutation(X.shape[0])
+        perm = rng.permutation(n_all)
         tot, cnt = 0.0, 0
-        for b0 in range(0, X.shape[0] - a.batch + 1, a.batch):
+        for b0 in range(0, n_all - a.batch + 1, a.batch):
             idx = torch.from_numpy(perm[b0:b0 + a.batch]).to(dev)
             x = Xd[idx].float().reshape(-1, cfg.max_context + 1, 50)
             x = torch.nn.functional.pad(x, (0, 0, 0, pad))  # pad_input: zero columns to 128 (cnn.cpp:219-225)
@@ -184,14 +209,38 @@ def main() -> None:
             opt.step()
             tot += float(loss.detach()) * len(idx)
             cnt += len(idx)
-        print(f"epoch {ep}: loss {tot / cnt:.4f} ({time.time() - t0:.1f} s)", flush=True)
-    params = net.cpu().export_reference()
+        params = net.export_reference()
+        if a.dagger > 0 and ep + 1 < a.epochs:
+            # DAgger-style aggregation: contexts the simulation reaches with the current
+            # model (ref_capture mode 0), labelled with the DES truth of each instruction
+            cur = work / "c3_cur.model"
+            write_model(cur, Model(cfg, init.norm, params))
+            add_x, add_t = [], []
+            for pth in train_paths:
+                tr = read_trace(pth)
+                cap = ref.capture(pth, cur, tr.n, mode=0, k=32, width=width)
+                n = min(cap["count"], tr.n)
+                pick = rng.choice(n, size=min(a.dagger, n), replace=False)
+                add_x.append(torch.from_numpy(cap["inputs"][pick].astype(np.float16)))
+                add_t.append(torch.from_numpy(tr.truth[cap["index"][pick].astype(np.int64)].astype(np.int64)))
+                del cap
+            Xd = torch.cat([Xd, torch.cat(add_x).to(dev)])
+            Td = torch.cat([Td, torch.cat(add_t).to(dev)])
+            n_all = Xd.shape[0]
+        score, errs = closed_loop_score(params)
+        if score < best[0]:
+            best = (score, params, ep)
+        print(f"epoch {ep}: samples {n_all} loss {tot / cnt:.4f} closed-loop |log CPI ratio| {score:.4f} "
+              f"({' '.join(f'{e:.3f}' for e in errs)}) ({time.time() - t0:.1f} s)", flush=True)
+    params = best[1]
+    print(f"selected epoch {best[2]} (closed-loop score {best[0]:.4f})", flush=True)
     out = Path(a.out)
     out.parent.mkdir(parents=True, exist_ok=True)
     write_model(out, Model(cfg, init.norm, params))
     # 5. the reference's own simulate_trace with the trained model vs the DES, held-out traces
-    report = {"samples": int(X.shape[0]), "epochs": a.epochs, "kinds": KINDS, "n_per_trace": a.n_per_trace,
-              "seeds": a.seeds, "device": a.device, "final_loss": tot / cnt, "held_out": {}}
+    report = {"samples": int(X.shape[0]), "samples_final": int(n_all), "dagger_per_trace": a.dagger, "epochs": a.epochs, "kinds": KINDS, "n_per_trace": a.n_per_trace,
+              "seeds": a.seeds, "device": a.device, "final_loss": tot / cnt, "selected_epoch": best[2],
+              "closed_loop_score": best[0], "held_out": {}}
     for pth in held_paths:
         des = read_trace(pth)
         r = ref.simulate(pth, out, sequential=True, n_hint=des.n)

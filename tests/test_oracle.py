@@ -265,3 +265,28 @@ def test_extensions_defaults_and_identities(port):
         assert np.array_equal(r["predicted_fetch"], base["predicted_fetch"])  # truth latencies
     r = port.simulate(t, oracle=True, k=6, drain_trim=True)
     assert np.all(r["subs"][:-1, 4] == 0) and r["subs"][-1].tolist() == base["subs"][-1].tolist()
+
+
+def test_trained_model_fixture(ref, port, tmp_path):
+    """The trained C3 the benches can load (tests/golden/train_c3.py): a C3 in
+    the reference's ILMD layout, its training report, and the port and the
+    reference library agreeing bit for bit on its forward and on a free-running
+    simulation."""
+    import json
+
+    mpath = GOLD / "c3_trained.model"
+    m = read_model(mpath)
+    c3 = CnnConfig.preset_c3()
+    assert m.config.hash() == c3.hash() and m.params.size == c3.param_count()
+    assert np.all(np.isfinite(m.params))
+    rep = json.loads((GOLD / "c3_trained.json").read_text())
+    assert set(rep["held_out"]) == {f"{k}_held" for k in rep["kinds"]} and rep["selected_epoch"] >= 0
+    path = GOLD / "mix_3000_s4.trace"
+    cap = ref.capture(path, mpath, 64, k=4)
+    a_out, a_tri = port.forward(m, cap["inputs"], cap["is_store"])
+    b_out, b_tri = ref.forward(mpath, cap["inputs"], cap["is_store"])
+    assert np.array_equal(a_out, b_out) and np.array_equal(a_tri, b_tri)
+    t = read_trace(path)
+    a = port.simulate(t, m, k=9)
+    b = ref.simulate(path, mpath, k=9, n_hint=t.n)
+    assert np.array_equal(a["subs"], b["subs"]) and np.array_equal(a["predicted_fetch"], b["predicted_fetch"][:t.n])

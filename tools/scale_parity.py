@@ -52,7 +52,11 @@ WORKLOADS = {
     "c2": dict(n=10_000_000, k=1024, kind="mix", regime="default", seed=101),
     "c4": dict(n=2_000_000, k=1024, kind="memory", regime="memory", seed=101),
     "c3s": dict(n=C3_SHARD_N, k=8192, kind="mix", regime="default", seed=101),
+    # the same workloads with the trained C3 (tests/golden/c3_trained.model, tests/golden/train_c3.py)
+    "c2t": dict(n=10_000_000, k=1024, kind="mix", regime="trained", seed=101),
+    "c4t": dict(n=2_000_000, k=1024, kind="memory", regime="trained", seed=101),
 }
+TRAINED_MODEL = ROOT / "tests" / "golden" / "c3_trained.model"
 
 
 def build_workload(name: str, init_params=None):
@@ -61,8 +65,13 @@ def build_workload(name: str, init_params=None):
 
     w = WORKLOADS[name]
     trace = synthetic_trace(w["n"], seed=w["seed"], kind=w["kind"])
-    model = synthetic_model(synthetic_trace(200_000, seed=101, kind=w["kind"]), seed=1, regime=w["regime"],
-                            init_params=init_params)
+    if w["regime"] == "trained":
+        from paper_2105_05821_b200.formats import read_model
+
+        model = read_model(TRAINED_MODEL)
+    else:
+        model = synthetic_model(synthetic_trace(200_000, seed=101, kind=w["kind"]), seed=1, regime=w["regime"],
+                                init_params=init_params)
     return trace, model, w
 
 
