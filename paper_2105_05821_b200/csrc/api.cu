@@ -18,6 +18,7 @@
 #include "gemm.cuh"
 #include "host_util.cuh"
 #include "model.cuh"
+#include "seq_fc.cuh"
 #include "sim_kernels.cuh"
 
 using namespace simnet;
@@ -123,6 +124,7 @@ struct ilsim_gpu_ctx {
   // run buffers
   DevBuf state, proc, wq, x, y, act, pred_fetch;
   DevBuf rec_stage;  // SNT1 record staging for the GPU trace ingest
+  DevBuf seq_flags;  // persistent FC kernel: publish / count / error words
 
   // simulate_parallel with the trace upload overlapped with the rounds: the
   // borrowed host view, uploaded window by window on copy_stream
@@ -362,7 +364,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   auto x_at = [&](uint64_t off) -> void* {
     return d_x ? static_cast<void*>(static_cast<char*>(d_x) + off * x_stride * input_elem_bytes(xprec)) : nullptr;
   };
-  auto do_ctx = [&](uint64_t f, uint64_t l, bool gather, uint64_t off, cudaStream_t st) {
+  auto make_ctx = [&](uint64_t f, uint64_t l, bool gather, uint64_t off) {
     CtxParams cp{};
     cp.state = d_state;
     cp.proc = d_proc;
@@ -389,6 +391,10 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     cp.page = cfg.page_size;
     cp.per_cycle = cfg.per_cycle_advance;
     cp.gather = gather && needs_input;
+    return cp;
+  };
+  auto do_ctx = [&](uint64_t f, uint64_t l, bool gather, uint64_t off, cudaStream_t st) {
+    const CtxParams cp = make_ctx(f, l, gather, off);
     launch_ctx(cp, st);
     return uint64_t{1};
   };
@@ -485,6 +491,109 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     return launches;
   };
 
+  // result collection (both the graph rounds and the persistent FC kernel)
+  auto finish = [&](float ms, uint64_t launches, const double* kms) {
+    CUDA_OK(cudaMemcpy(hs.data(), d_state, K * sizeof(SubState), cudaMemcpyDeviceToHost));
+    if (predicted_fetch && d_pf)
+      CUDA_OK(cudaMemcpy(predicted_fetch, d_pf, owned * 4, cudaMemcpyDeviceToHost));
+
+    for (uint64_t j = 0; j < K; ++j) {
+      const SubState& st = hs[j];
+      const uint64_t i = P.sb + j;
+      if (st.status == kErrStall)
+        throw ApiError("processor queue stalled without progress at tick " + std::to_string(st.err_tick) +
+                       " (sub-trace " + std::to_string(i) + ")");
+      if (st.status == kErrDrain)
+        throw ApiError("drain made no progress at tick " + std::to_string(st.err_tick) + " (sub-trace " +
+                       std::to_string(i) + ")");
+      if (st.status == kErrWriteRing)
+        throw WriteRingOverflow("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
+                                    std::to_string(i) + "; raise write_ring",
+                                wcap);
+      if (st.pos != st.len) throw ApiError("internal: sub-trace did not finish");
+      ilsim_sub_result& r = subs[j];
+      r.instructions = st.len - st.warm;
+      r.total_cycles = st.cur - st.base_cur;
+      r.sum_fetch = st.sum_fetch;
+      r.delta = r.total_cycles - r.sum_fetch;
+      r.drain_cycles = st.drain;
+      r.overflow_stall_cycles = st.overflow - st.base_overflow;
+      r.empty = r.instructions == 0;
+      tot->total_cycles += r.total_cycles;
+      tot->sum_fetch += r.sum_fetch;
+      tot->delta += r.delta;
+      tot->drain_cycles += r.drain_cycles;
+      tot->overflow_stall_cycles += r.overflow_stall_cycles;
+      tot->instructions += r.instructions;
+    }
+    tot->sub_traces = K;
+    tot->rounds = rounds;
+    tot->cpi = tot->instructions ? static_cast<double>(tot->total_cycles) / tot->instructions : 0.0;
+    tot->device_ms = ms;
+    for (int q = 0; q < 4; ++q) tot->kernel_ms[q] = kms[q];
+    tot->launches = launches;
+  };
+  // FC-only predictor, fp32, a handful of sub-traces (the sequential c1
+  // configuration): the whole simulation is one persistent cooperative launch
+  // (seq_fc.cu), bit-identical to the launch-per-layer rounds below
+  // (SIMNET_NO_SEQ_FC=1 forces those, A/B)
+  {
+    const ilsim_cnn_config& mc_cfg = c->model.cfg;
+    int dev = 0, ctas = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev));
+    const bool seq = !oracle && !capture_mode && cfg.reserved[0] == 0 && c->precision == ILSIM_PREC_FP32 &&
+                     mc_cfg.n_conv == 0 && K == chunk && std::getenv("SIMNET_NO_SEQ_FC") == nullptr &&
+                     seq_fc_fits(c->model.L.flat, mc_cfg.fc_hidden, c->model.L.out_dim, static_cast<int>(K), ctas);
+    if (seq) {
+      uint32_t* d_flags = static_cast<uint32_t*>(c->seq_flags.need(4 * sizeof(uint32_t)));
+      CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t), c->stream));
+      SeqFcParams sp{};
+      sp.ctx = make_ctx(0, K, true, 0);
+      sp.dec = decode_params(0, K, fb);
+      const float* P = c->model.params.as<float>();
+      sp.w1 = P + c->model.L.fc1_w;
+      sp.b1 = P + c->model.L.fc1_b;
+      sp.w2 = P + c->model.L.fc2_w;
+      sp.b2 = P + c->model.L.fc2_b;
+      sp.flat = static_cast<int32_t>(c->model.L.flat);
+      sp.hidden = mc_cfg.fc_hidden;
+      sp.od = c->model.L.out_dim;
+      sp.h = fb.act[0];
+      sp.y = fb.y;
+      sp.flags = d_flags;
+      sp.rounds = rounds;
+      const bool seq_trace = std::getenv("SIMNET_SEQ_TRACE") != nullptr && rounds > 200;
+      if (seq_trace) {
+        sp.trace = static_cast<long long*>(c->seq_flags.need(4 * sizeof(uint32_t) + 16 * sizeof(long long))) + 2;
+        d_flags = static_cast<uint32_t*>(c->seq_flags.p);
+        sp.flags = d_flags;
+        CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t) + 16 * sizeof(long long), c->stream));
+      }
+      wait_windows(UINT32_MAX);
+      CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+      launch_seq_fc(sp, ctas, c->stream);
+      CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+      CUDA_OK(cudaGetLastError());
+      CUDA_OK(cudaEventSynchronize(c->ev[1]));
+      uint32_t hflags[4];
+      CUDA_OK(cudaMemcpy(hflags, d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+      if (hflags[2] != 0) throw ApiError("persistent FC kernel: a CTA timed out waiting for its peers");
+      if (seq_trace) {  // diagnostics: phase boundaries of round 100 (ns from the control CTA's wait)
+        long long tt[16];
+        CUDA_OK(cudaMemcpy(tt, sp.trace, sizeof(tt), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "seq_fc round trace (ns): control wait_h %lld stage_h %lld fc2 %lld decode %lld ctx %lld "
+                     "publish %lld | worker1 x_seen %lld stage_x %lld fc1 %lld h_published %lld\n",
+                     tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5],
+                     tt[9] - tt[6], tt[10] - tt[9], tt[11] - tt[10], tt[12] - tt[11]);
+      }
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      const double zero[4] = {0, 0, 0, 0};
+      finish(ms, 1, zero);
+      return;
+    }
+  }
   if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
   if (capture_mode && !fused && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
   const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs
@@ -590,45 +699,7 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   float ms = 0;
   CUDA_OK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
 
-  CUDA_OK(cudaMemcpy(hs.data(), d_state, K * sizeof(SubState), cudaMemcpyDeviceToHost));
-  if (predicted_fetch && d_pf)
-    CUDA_OK(cudaMemcpy(predicted_fetch, d_pf, owned * 4, cudaMemcpyDeviceToHost));
-
-  for (uint64_t j = 0; j < K; ++j) {
-    const SubState& st = hs[j];
-    const uint64_t i = P.sb + j;
-    if (st.status == kErrStall)
-      throw ApiError("processor queue stalled without progress at tick " + std::to_string(st.err_tick) +
-                     " (sub-trace " + std::to_string(i) + ")");
-    if (st.status == kErrDrain)
-      throw ApiError("drain made no progress at tick " + std::to_string(st.err_tick) + " (sub-trace " +
-                     std::to_string(i) + ")");
-    if (st.status == kErrWriteRing)
-      throw WriteRingOverflow("write queue ring overflow (capacity " + std::to_string(wcap) + ") in sub-trace " +
-                                  std::to_string(i) + "; raise write_ring",
-                              wcap);
-    if (st.pos != st.len) throw ApiError("internal: sub-trace did not finish");
-    ilsim_sub_result& r = subs[j];
-    r.instructions = st.len - st.warm;
-    r.total_cycles = st.cur - st.base_cur;
-    r.sum_fetch = st.sum_fetch;
-    r.delta = r.total_cycles - r.sum_fetch;
-    r.drain_cycles = st.drain;
-    r.overflow_stall_cycles = st.overflow - st.base_overflow;
-    r.empty = r.instructions == 0;
-    tot->total_cycles += r.total_cycles;
-    tot->sum_fetch += r.sum_fetch;
-    tot->delta += r.delta;
-    tot->drain_cycles += r.drain_cycles;
-    tot->overflow_stall_cycles += r.overflow_stall_cycles;
-    tot->instructions += r.instructions;
-  }
-  tot->sub_traces = K;
-  tot->rounds = rounds;
-  tot->cpi = tot->instructions ? static_cast<double>(tot->total_cycles) / tot->instructions : 0.0;
-  tot->device_ms = ms;
-  for (int q = 0; q < 4; ++q) tot->kernel_ms[q] = kms[q];
-  tot->launches = launches;
+  finish(ms, launches, kms);
 }
 
 // run_impl, rerun with a doubled write ring while a sub-trace's write queue

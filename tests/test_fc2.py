@@ -83,3 +83,29 @@ def test_fc2_tensor_core_precision_rejected(gpu, port):
     cfg = fc_config()
     with pytest.raises(IlsimError, match="FC-only"):
         g.load_model(Model(cfg, identity_norm(), port.init_params(cfg, 5)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 2])
+def test_fc2_persistent_kernel(gpu, port, k, monkeypatch):
+    """K <= 2 with the paper-size FC2 (5550 -> 1024 -> 33, config c1's shape):
+    the whole simulation is one persistent cooperative launch (seq_fc.cu), bit
+    for bit the launch-per-layer rounds (SIMNET_NO_SEQ_FC), and the sequential
+    run matches the oracle port's simulate_trace semantics."""
+    g = gpu("fp32")
+    cfg = CnnConfig.preset_fc2()
+    m = Model(cfg, identity_norm(), port.init_params(cfg, 5))
+    g.load_model(m)
+    t = random_trace(6, 2500)
+    pc = ParallelConfig(k=k, sim=SimConfig(max_context=cfg.max_context))
+    g.load_trace(t, pc)
+    monkeypatch.delenv("SIMNET_NO_SEQ_FC", raising=False)
+    a = g.run(pc)
+    assert a.launches == 1  # the persistent kernel ran
+    monkeypatch.setenv("SIMNET_NO_SEQ_FC", "1")
+    b = g.run(pc)
+    assert b.launches > 1000
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    want = port.simulate(t, m, k=k)
+    assert abs(a.total_cycles - want["total_cycles"]) <= 1e-3 * want["total_cycles"]
+    assert np.mean(a.predicted_fetch == want["predicted_fetch"]) >= 0.999

@@ -63,8 +63,11 @@ def c1(args):
     g.load_model(m)
     pc = ParallelConfig(k=1, sim=SimConfig(max_context=cfg.max_context))
     r = run(g, t, pc, reps=1)
+    path = "persistent cooperative kernel (seq_fc.cu, 1 launch)" if r.launches == 1 else \
+        f"launch-per-layer rounds ({r.launches} launches)"
     out = {"config": "c1", "predictor": "FC2 5550-1024-33 (5,716,992 mults)", "precision": "fp32 (SIMT)",
-           "instructions": t.n, "sub_traces": 1, "gpu_mips": t.n / (r.device_ms / 1e3) / 1e6, "gpu_cpi": r.cpi}
+           "path": path, "instructions": t.n, "sub_traces": 1, "gpu_mips": t.n / (r.device_ms / 1e3) / 1e6,
+           "us_per_instruction": 1e3 * r.device_ms / t.n, "gpu_cpi": r.cpi}
     ref = _k1_ref("c1")
     if ref and ref["instructions"] == t.n and ref["trace_digest"] == trace_digest(t) and \
             ref["model_digest"] == model_digest(m):
