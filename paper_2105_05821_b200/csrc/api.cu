@@ -544,7 +544,8 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     CUDA_OK(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev));
     const bool seq = !oracle && !capture_mode && cfg.reserved[0] == 0 && c->precision == ILSIM_PREC_FP32 &&
                      mc_cfg.n_conv == 0 && K == chunk && std::getenv("SIMNET_NO_SEQ_FC") == nullptr &&
-                     seq_fc_fits(c->model.L.flat, mc_cfg.fc_hidden, c->model.L.out_dim, static_cast<int>(K), ctas);
+                     seq_fc_fits(c->model.L.flat, mc_cfg.fc_hidden, c->model.L.out_dim, static_cast<int>(K), ctas,
+                                 static_cast<int>(pcap));
     if (seq) {
       uint32_t* d_flags = static_cast<uint32_t*>(c->seq_flags.need(4 * sizeof(uint32_t)));
       CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t), c->stream));

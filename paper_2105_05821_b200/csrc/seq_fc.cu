@@ -106,7 +106,8 @@ __device__ __forceinline__ void chains(const float* w, const float* x, float* pa
   for (int r = 0; r < rows; ++r) {
     const float* xr = x + (r * nch + c) * kPad;
     // the chain is serial (4-cycle FMA latency); unrolled 32 deep so each
-    // block's 64 shared loads are in flight before its FMAs
+    // block's 64 shared loads are in flight before its FMAs (a two-buffer
+    // software pipeline of 16-step blocks measured slower: 3.1 -> 4.5 us)
     float acc = 0.0f;
     int j = 0;
     for (; j + 32 <= len; j += 32) {
@@ -145,6 +146,19 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
     float* w2s = sm;                                           // [512][nchains]
     float* hs = w2s + kSgemmChunk * nchains;                   // [K][nch][kPad]
     float* part = hs + K * nch * kPad;                         // [K][nchains]
+    // this CTA owns its sub-traces for the whole run: their SubStates and
+    // processor-queue rings live in shared memory (generic pointers, so the K1
+    // and K3 device code is unchanged); the write-queue rings stay in HBM
+    const uint32_t pcap = p.ctx.pmask + 1;
+    RingEntry* s_proc = reinterpret_cast<RingEntry*>(
+        (reinterpret_cast<uintptr_t>(part + K * nchains) + 15) & ~uintptr_t{15});  // [K][pcap], 16-B aligned
+    __shared__ SubState s_sub[8];
+    for (int i = tid; i < K * static_cast<int>(sizeof(SubState) / 4); i += kSeqThreads)
+      reinterpret_cast<uint32_t*>(s_sub)[i] = reinterpret_cast<const uint32_t*>(p.ctx.state + p.ctx.first)[i];
+    CtxParams cx = p.ctx;
+    cx.state = s_sub - p.ctx.first;
+    cx.proc = s_proc - p.ctx.first * pcap;
+    SubState* dstate = s_sub - p.dec.first;
     for (int i = tid; i < kSgemmChunk * nchains; i += kSeqThreads) {
       const int j = i / nchains, t = i % nchains, o = t / nch, c = t % nch, k = c * kSgemmChunk + j;
       w2s[i] = k < p.hidden ? p.w2[static_cast<uint64_t>(k) * p.od + o] : 0.0f;
@@ -174,7 +188,7 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
         __syncthreads();
         if (warp < K) {  // K3 (decode_kernel's decode_triple + apply_decoded): warp w, sub-trace w,
                          // the three heads on lanes 0-2 (warp_decode_triple, the fused rounds' form)
-          SubState* sp = p.dec.state + p.dec.first + warp;
+          SubState* sp = dstate + p.dec.first + warp;
           SubState st = *sp;
           if (st.status == kOk && st.pos < st.len) {
             uint32_t t3[3];
@@ -189,7 +203,7 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
       }
       if (tr) tr[4] = gtimer();
       // K1: apply the decoded step, gather the next rows (the last pass: apply + drain only)
-      CtxParams cp = p.ctx;
+      CtxParams cp = cx;
       cp.gather = r < p.rounds ? p.ctx.gather : 0;
       for (uint64_t s = cp.first; s < cp.last; ++s) {
         ctx_one<kSeqThreads>(cp, s, csm);
@@ -204,6 +218,8 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
     }
     __syncthreads();
     if (tid == 0) st_release(p.flags, kExit);
+    for (int i = tid; i < K * static_cast<int>(sizeof(SubState) / 4); i += kSeqThreads)
+      reinterpret_cast<uint32_t*>(p.ctx.state + p.ctx.first)[i] = reinterpret_cast<const uint32_t*>(s_sub)[i];
     return;
   }
 
@@ -249,27 +265,28 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
   }
 }
 
-size_t seq_fc_smem(int flat, int hidden, int od, int K, int ctas) {
+size_t seq_fc_smem(int flat, int hidden, int od, int K, int ctas, int pcap) {
   const int workers = ctas - 1;
   const int max_outs = (hidden + workers - 1) / workers;
   const int nch1 = (flat + kSgemmChunk - 1) / kSgemmChunk, nch2 = (hidden + kSgemmChunk - 1) / kSgemmChunk;
   const size_t worker = (static_cast<size_t>(kSgemmChunk) * max_outs * nch1 + static_cast<size_t>(K) * nch1 * kPad +
                          static_cast<size_t>(K) * max_outs * nch1) * 4;
   const size_t control = (static_cast<size_t>(kSgemmChunk) * od * nch2 + static_cast<size_t>(K) * nch2 * kPad +
-                          static_cast<size_t>(K) * od * nch2) * 4;
+                          static_cast<size_t>(K) * od * nch2) * 4 + 16 +
+                         static_cast<size_t>(K) * pcap * sizeof(RingEntry);
   return worker > control ? worker : control;
 }
 
-bool seq_fc_fits(int flat, int hidden, int od, int K, int ctas) {
+bool seq_fc_fits(int flat, int hidden, int od, int K, int ctas, int pcap) {
   if (ctas < 2 || K < 1 || K > 8 || hidden < ctas - 1) return false;
-  const size_t need = seq_fc_smem(flat, hidden, od, K, ctas) + sizeof(CtxSmem) + 8 * kFcMaxOut * 4 + 128;
+  const size_t need = seq_fc_smem(flat, hidden, od, K, ctas, pcap) + sizeof(CtxSmem) + 8 * kFcMaxOut * 4 + 128;
   return need <= 227 * 1024;
 }
 
 void launch_seq_fc(SeqFcParams p, int ctas, cudaStream_t s) {
   const int K = static_cast<int>(p.ctx.last - p.ctx.first);
   p.max_outs = (p.hidden + ctas - 2) / (ctas - 1);
-  const size_t smem = seq_fc_smem(p.flat, p.hidden, p.od, K, ctas);
+  const size_t smem = seq_fc_smem(p.flat, p.hidden, p.od, K, ctas, static_cast<int>(p.ctx.pmask + 1));
   CUDA_OK(cudaFuncSetAttribute(seq_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   void* args[] = {&p};
   CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(seq_fc_kernel), dim3(ctas), dim3(kSeqThreads), args,

@@ -20,7 +20,7 @@ struct SeqFcParams {
   long long* trace;      // diagnostics (SIMNET_SEQ_TRACE): %globaltimer at phase boundaries of one round
 };
 
-bool seq_fc_fits(int flat, int hidden, int od, int K, int ctas);
+bool seq_fc_fits(int flat, int hidden, int od, int K, int ctas, int pcap);
 void launch_seq_fc(SeqFcParams p, int ctas, cudaStream_t s);
 
 }  // namespace simnet
