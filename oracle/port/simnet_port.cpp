@@ -101,6 +101,24 @@ struct Net {
     }
   }
 
+  // The FC-only predictor's accumulation order (no reference implementation;
+  // defined here and on the GPU alike, paper_2105_05821_b200/csrc/gemm.cuh):
+  // per output, an fma chain over each 512-wide K chunk starting from 0, the
+  // chunk sums added in chunk order from 0.
+  static void gemm_chunked(const float* W, const float* x, float* y, int rows, int inner) {
+    constexpr int kChunk = 512;
+    for (int o = 0; o < rows; ++o) {
+      float tot = 0.0f;
+      for (int k0 = 0; k0 < inner; k0 += kChunk) {
+        float acc = 0.0f;
+        const int k1 = std::min(inner, k0 + kChunk);
+        for (int k = k0; k < k1; ++k) acc = std::fma(W[static_cast<size_t>(k) * rows + o], x[k], acc);
+        tot += acc;
+      }
+      y[o] = tot;
+    }
+  }
+
   // input: width() floats; out: out_dim floats.
   void forward(const float* input, float* out, std::vector<float>& act_buf) const {
     act_buf.resize(act_n);
@@ -126,10 +144,16 @@ struct Net {
       len = olen;
     }
     float* h = A + act_h;
-    gemm(P + fc1_w, A + act[m->n_conv], h, m->fc_hidden, flat, 1, false);
+    if (m->n_conv == 0)
+      gemm_chunked(P + fc1_w, A + act[m->n_conv], h, m->fc_hidden, flat);
+    else
+      gemm(P + fc1_w, A + act[m->n_conv], h, m->fc_hidden, flat, 1, false);
     for (int o = 0; o < m->fc_hidden; ++o) h[o] = std::max(h[o] + P[fc1_b + o], 0.0f);
     float* y = A + act_y;
-    gemm(P + fc2_w, h, y, out_dim, m->fc_hidden, 1, false);
+    if (m->n_conv == 0)
+      gemm_chunked(P + fc2_w, h, y, out_dim, m->fc_hidden);
+    else
+      gemm(P + fc2_w, h, y, out_dim, m->fc_hidden, 1, false);
     for (int o = 0; o < out_dim; ++o) y[o] += P[fc2_b + o];
     std::copy(y, y + out_dim, out);
   }

@@ -22,11 +22,18 @@ struct LayerGemm {
   int n, ldc;
   int relu;
   float* splitk;           // scratch for the small-batch split-K path ([m][chunks][n] floats), or null
+  int chunk;               // accumulation order: 0 = one fma chain over all of K (k ascending);
+                           // kSgemmChunk = chains over 512-wide K chunks, summed in chunk order
 };
 
-// K is accumulated in chunks of kSgemmChunk: each chunk's fma chain starts at
-// 0 (k ascending), and the chunk sums are added in order.  Every batch size
-// and both kernels below use this order, so results stay batch-independent.
+// Accumulation order.  chunk == 0: one fma chain per output, k ascending from
+// 0 -- the reference's restated forward (oracle/cnn_restated.cpp gemm_cm, cnn.cpp
+// column-major order), used for every layer of the CNN models.  chunk ==
+// kSgemmChunk: each 512-wide chunk's fma chain starts at 0 (k ascending) and
+// the chunk sums are added in order -- the FC-only predictor's definition (no
+// reference implementation; the oracle port defines it the same way), which
+// lets its 5550-wide FC1 split over K.  Every batch size and both kernels below
+// use the layer's order, so results stay batch-independent.
 constexpr int kSgemmChunk = 512;
 constexpr uint64_t kSgemvMaxM = 8;  // batches up to this many rows take the split-K GEMV
 inline uint64_t sgemm_splitk_floats(uint64_t m, int kdim, int n) {

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
   float tot[4][4] = {};  // sum of the finished kSgemmChunk chunks (see gemm.cuh)
   float tpp[4][4] = {};
   for (int k0 = 0; k0 < g.kdim; k0 += BK) {
-    if (k0 > 0 && k0 % kSgemmChunk == 0) {
+    if (g.chunk > 0 && k0 > 0 && k0 % g.chunk == 0) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -135,8 +135,7 @@ __global__ void __launch_bounds__(kGv) sgemv_reduce_kernel(LayerGemm g, int chun
 
 void launch_sgemm(const LayerGemm& g, cudaStream_t stream) {
   if (g.m == 0) return;
-  if (g.splitk && g.m <= kSgemvMaxM && g.rows_per_sample == 1 && g.valid_rows == 1 && !g.w2 &&
-      g.kdim > kSgemmChunk) {
+  if (sgemm_two_launches(g)) {
     const int chunks = (g.kdim + kSgemmChunk - 1) / kSgemmChunk;
     const unsigned gx = static_cast<unsigned>((g.n + kGv - 1) / kGv);
     sgemv_chunk_kernel<<<dim3(gx, chunks, static_cast<unsigned>(g.m)), kGv, 0, stream>>>(g);
@@ -148,8 +147,8 @@ void launch_sgemm(const LayerGemm& g, cudaStream_t stream) {
 }
 
 bool sgemm_two_launches(const LayerGemm& g) {
-  return g.splitk && g.m <= kSgemvMaxM && g.rows_per_sample == 1 && g.valid_rows == 1 && !g.w2 &&
-         g.kdim > kSgemmChunk;
+  return g.splitk && g.chunk == kSgemmChunk && g.m <= kSgemvMaxM && g.rows_per_sample == 1 && g.valid_rows == 1 &&
+         !g.w2 && g.kdim > kSgemmChunk;
 }
 
 }  // namespace simnet

@@ -232,7 +232,12 @@ uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32
     valid = olen / 2;
     sstride = static_cast<uint64_t>(olen) * cout;
   }
+  // accumulation order (gemm.cuh): the CNN models follow the reference's
+  // restated forward (one chain per output); the FC-only predictor its own
+  // 512-wide chunked definition (shared with the oracle port)
+  const int fc_chunk = c.n_conv == 0 ? kSgemmChunk : 0;
   LayerGemm f1{};
+  f1.chunk = fc_chunk;
   f1.a = in;
   f1.m = samples;
   f1.rows_per_sample = 1;
@@ -248,6 +253,7 @@ uint64_t forward_launch(const DevModel& m, int precision, const void* xv, uint32
   f1.splitk = fb.splitk;
   launch_sgemm(f1, s);
   LayerGemm f2{};
+  f2.chunk = fc_chunk;
   f2.a = fb.act[c.n_conv];
   f2.m = samples;
   f2.rows_per_sample = 1;
