@@ -73,25 +73,55 @@ __device__ uint32_t wait_at_least(const uint32_t* p, uint32_t want, uint32_t* er
 
 // Stage `rows` rows of `kdim` floats (row pitch `pitch` in global memory,
 // written by another SM: L2 loads) as [row][chunk][kPad].
-// All of a thread's loads of a block are issued before its first store (one
-// L2 round trip per 24 x 256 floats, not one per element).
+// 16-B loads (rows are 16-B aligned: pitch a multiple of 4 floats), all of a
+// thread's loads of a block issued before its first store.
 __device__ __forceinline__ void stage_rows(float* dst, const float* src, int rows, int kdim, uint64_t pitch,
                                            int nch) {
-  constexpr int kBatch = 24;
-  for (int r = 0; r < rows; ++r)
-    for (int k0 = 0; k0 < kdim; k0 += kBatch * kSeqThreads) {
-      float v[kBatch];
+  constexpr int kBatch = 8;
+  const int n4 = (kdim + 3) / 4;
+  for (int r = 0; r < rows; ++r) {
+    const float4* s4 = reinterpret_cast<const float4*>(src + r * pitch);
+    for (int q0 = 0; q0 < n4; q0 += kBatch * kSeqThreads) {
+      float4 v[kBatch];
 #pragma unroll
       for (int i = 0; i < kBatch; ++i) {
-        const int k = k0 + i * kSeqThreads + threadIdx.x;
-        v[i] = k < kdim ? __ldcg(src + r * pitch + k) : 0.0f;
+        const int q = q0 + i * kSeqThreads + threadIdx.x;
+        v[i] = q < n4 ? __ldcg(s4 + q) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
 #pragma unroll
       for (int i = 0; i < kBatch; ++i) {
-        const int k = k0 + i * kSeqThreads + threadIdx.x;
-        if (k < kdim) dst[(r * nch + k / kSgemmChunk) * kPad + k % kSgemmChunk] = v[i];
+        const int k = 4 * (q0 + i * kSeqThreads + threadIdx.x);  // 4 | 512: a float4 never straddles chunks
+        float* d = dst + (r * nch + k / kSgemmChunk) * kPad + k % kSgemmChunk;
+        if (k < kdim) d[0] = v[i].x;
+        if (k + 1 < kdim) d[1] = v[i].y;
+        if (k + 2 < kdim) d[2] = v[i].z;
+        if (k + 3 < kdim) d[3] = v[i].w;
       }
     }
+  }
+}
+
+// Warm L1 with the static-slot rows the next gather will read (the current
+// context entries' and the next target's, 192 B each; the trace is read-only,
+// so the gather's __ldg hits them), while the control CTA waits on the workers.
+__device__ __forceinline__ void prefetch_context(const CtxParams& cx, const SubState* st_all,
+                                                 const RingEntry* proc_all, uint32_t pcap, int K) {
+  for (int s = 0; s < K; ++s) {
+    const SubState& st = st_all[s];
+    const uint32_t n = st.pt - st.ph;
+    const uint32_t lines = 2 * (n + 2);  // + the next two targets
+    for (uint32_t i = threadIdx.x; i < lines; i += kSeqThreads) {
+      const uint32_t e = i >> 1;
+      uint64_t row;
+      if (e < n)
+        row = st.begin + proc_all[s * pcap + ((st.pt - 1 - e) & (pcap - 1))].idx;
+      else
+        row = st.begin + st.pos + (e - n);
+      if (st.pos + (e >= n ? e - n : 0) >= st.len && e >= n) continue;
+      const float* a = cx.stat + row * kStatStride + (i & 1) * 32;
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    }
+  }
 }
 
 // Chains: thread t < outs * nch owns (output t / nch, chunk t % nch); w is
@@ -169,6 +199,7 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
       if (r > 0) {
         // FC2 + decode of round r-1 (sgemv pair order, then decode_kernel)
         if (tr) tr[0] = gtimer();
+        if (cx.gather) prefetch_context(cx, s_sub, s_proc, pcap, K);
         if (tid == 0) s_flag = wait_at_least(p.flags + 1, r * static_cast<uint32_t>(workers), p.flags + 2);
         __syncthreads();
         if (s_flag == kExit) break;
