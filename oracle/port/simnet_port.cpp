@@ -107,15 +107,17 @@ struct Net {
   // chunk sums added in chunk order from 0.
   static void gemm_chunked(const float* W, const float* x, float* y, int rows, int inner) {
     constexpr int kChunk = 512;
-    for (int o = 0; o < rows; ++o) {
-      float tot = 0.0f;
-      for (int k0 = 0; k0 < inner; k0 += kChunk) {
-        float acc = 0.0f;
-        const int k1 = std::min(inner, k0 + kChunk);
-        for (int k = k0; k < k1; ++k) acc = std::fma(W[static_cast<size_t>(k) * rows + o], x[k], acc);
-        tot += acc;
+    std::vector<float> acc(rows);
+    std::fill(y, y + rows, 0.0f);
+    for (int k0 = 0; k0 < inner; k0 += kChunk) {  // per output: the same chains, weights streamed row by row
+      std::fill(acc.begin(), acc.end(), 0.0f);
+      const int k1 = std::min(inner, k0 + kChunk);
+      for (int k = k0; k < k1; ++k) {
+        const float a = x[k];
+        const float* wk = W + static_cast<size_t>(k) * rows;
+        for (int o = 0; o < rows; ++o) acc[o] = std::fma(wk[o], a, acc[o]);
       }
-      y[o] = tot;
+      for (int o = 0; o < rows; ++o) y[o] += acc[o];
     }
   }
 
