@@ -96,7 +96,7 @@ def test_fc2_persistent_kernel(gpu, port, k, monkeypatch):
     cfg = CnnConfig.preset_fc2()
     m = Model(cfg, identity_norm(), port.init_params(cfg, 5))
     g.load_model(m)
-    t = random_trace(6, 2500)
+    t = random_trace(6, 2501)  # K = 2: sub-traces of 1251 and 1250 (one finishes a round early)
     pc = ParallelConfig(k=k, sim=SimConfig(max_context=cfg.max_context))
     g.load_trace(t, pc)
     monkeypatch.delenv("SIMNET_NO_SEQ_FC", raising=False)
