@@ -45,7 +45,8 @@ namespace simnet {
 //   warps 2-5  (3xTF32) split each landed chunk into hi / lo in place
 //   warps 6-9  epilogue: tcgen05.ld -> bias / ReLU -> global; two TMEM
 //              accumulators so tile t's epilogue overlaps tile t+1's MMAs
-constexpr int kStages = 4;
+constexpr int kStages = 4;     // default A ring depth
+constexpr int kMaxStages = 6;  // CTAs looping over M tiles may trade a staging buffer for two more stages
 constexpr int kWarps = 10;
 constexpr int kLayerThreads = kWarps * 32;
 constexpr uint32_t kAChunk = kBM * 128;  // 16 KB
@@ -76,6 +77,7 @@ struct TcGemmParams {
                               // no weight loads, to measure their share of FC1
   int tma_multi;              // f32 split-K partials through tmOut for CTAs that loop over M tiles: two
                               // 16 KB staging buffers past the A ring, one 32-column group at a time
+  int stg_bufs;               // tma_multi staging buffers (2, or 1 to make room for a deeper A ring)
 };
 
 template <int kMode, bool kAInTmem = false>
@@ -96,9 +98,9 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint8_t* sStg = sAlo + (kSplit && !kAInTmem ? ns * kAChunk : 0);
 
   __shared__ __align__(8) uint64_t bar_w;
-  __shared__ __align__(8) uint64_t bar_full[kStages], bar_split[kStages], bar_empty[kStages];
+  __shared__ __align__(8) uint64_t bar_full[kMaxStages], bar_split[kMaxStages], bar_empty[kMaxStages];
   __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
-  __shared__ __align__(8) uint64_t bar_sfree[kStages], bar_tfree[4];  // a_tmem: SMEM stage read / TMEM A slot free
+  __shared__ __align__(8) uint64_t bar_sfree[kMaxStages], bar_tfree[4];  // a_tmem: SMEM stage read / TMEM A slot free
   __shared__ uint32_t tmem_slot;
   constexpr bool a_tmem = kSplit && kAInTmem;
 
@@ -111,7 +113,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_w, 1);
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kMaxStages; ++i) {
       mbar_init(&bar_full[i], 1);
       mbar_init(&bar_split[i], 128);
       mbar_init(&bar_empty[i], 1);
@@ -208,8 +210,12 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] *= p.out_scale;
       }
-      uint8_t* box = sStg + (ng & 1u) * kAChunk + quad * 32 * 128;
-      if (ng >= 2 && lane == 0) bulk_wait_read1();  // the store from this buffer two groups ago has read it
+      const bool one = p.stg_bufs == 1;
+      uint8_t* box = sStg + (one ? 0u : (ng & 1u)) * kAChunk + quad * 32 * 128;
+      if (lane == 0) {  // the store that last used this buffer has read it
+        if (one && ng >= 1) bulk_wait_read();
+        if (!one && ng >= 2) bulk_wait_read1();
+      }
       __syncwarp();
       uint8_t* stg = box + lane * 128;
 #pragma unroll
@@ -351,6 +357,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         mma_commit(&bar_acc_full[acc]);
         if (tr && it < 1) tr[3] = clock64();
+        if (tr && it < 8) tr[21 + it] = clock64();  // diagnostics: tile it's MMAs all issued
       }
     }
     __syncwarp();
@@ -734,11 +741,12 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
   w.map_lo = mode == kTF32x3 ? make_map(w.lo.p, false, 2, dims, strides, box) : w.map_hi;
 }
 
-size_t smem_bytes(int mode, int n, int chunks, int stages, bool a_tmem = false, bool tma_multi = false) {
+size_t smem_bytes(int mode, int n, int chunks, int stages, bool a_tmem = false, bool tma_multi = false,
+                  int stg_bufs = 2) {
   const size_t w = static_cast<size_t>(chunks) * n * 128 * (mode == kTF32x3 ? 2 : 1);
   const size_t a =
       static_cast<size_t>(stages > 0 ? stages : kStages) * kAChunk * (mode == kTF32x3 && !a_tmem ? 2 : 1);
-  return w + a + (tma_multi ? 2 * kAChunk : 0) + 1024;
+  return w + a + (tma_multi ? static_cast<size_t>(stg_bufs) * kAChunk : 0) + 1024;
 }
 
 int g_num_sms = 0;
@@ -787,7 +795,7 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
-  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0);
+  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0, p.stg_bufs);
   if (mode == kFP8)
     launch_pdl_tag("layer_bf16", tc_layer_kernel<kFP8>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
   else if (mode == kBF16)
@@ -960,8 +968,16 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     const bool multi_direct = std::getenv("SIMNET_FC1_MULTI_DIRECT") != nullptr;
     p.tma_multi = p.m_tiles > gx && fc_tile % 32 == 0 && !multi_direct &&
                   smem_bytes(mode, p.n, p.chunks, kStages, p.a_tmem != 0, true) <= 226 * 1024;
+    p.stg_bufs = 2;
     p.stages = kStages;
-    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0) > 226 * 1024)
+    // SIMNET_FC1_STAGES=N (A/B): an A ring N deep for CTAs looping over M tiles,
+    // with one staging buffer if two do not fit
+    if (const char* e = std::getenv("SIMNET_FC1_STAGES"); e && p.m_tiles > gx)
+      p.stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
+    if (p.tma_multi && smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, true, 2) > 226 * 1024)
+      p.stg_bufs = 1;
+    while (p.stages > 2 &&
+           smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0, p.stg_bufs) > 226 * 1024)
       --p.stages;
     p.bias = nullptr;
     p.relu = 0;

@@ -30,6 +30,13 @@ for prec in os.environ.get("PRECS", "tf32x3,bf16").split(","):
     dw = (tr[:, 12] - tr[:, 8]) * 1.87
     print(f"  MMA issue total      median {np.median(tr[:, 15]):8.0f} cyc")
     print(f"  dependency wait exit median {np.median(dw):8.0f} cyc (globaltimer x 1.87)")
+    per = rel[:, 21:29]
+    ok = per[:, 1:] > 0
+    if ok.any():
+        d = np.diff(per, axis=1)[ok]
+        print(f"  tile MMA-issue period (tiles 1..7) median {np.median(d):8.0f} cyc")
+        print("  tile issue times (median over CTAs):", " ".join(f"{np.median(per[:, i][per[:, i] > 0]):.0f}"
+                                                          for i in range(8) if (per[:, i] > 0).any()))
     for i, n in names.items():
         col = rel[:, i][tr[:, i] > 0]
         if col.size:
