@@ -150,6 +150,7 @@ __device__ inline void apply_step(SubState& st, const Rings& r, const ApplyArgs&
     }
     // drain right after the last step (parallel.cpp:79, simcore.cpp:152-159)
     if (st.pos == st.len && st.count_drain) {
+      __syncwarp();  // lane 0's push above is visible to the lanes reading the queue heads below
       while (err == kOk && (st.ph != st.pt || st.wh != st.wt)) {
         uint64_t gap = ~uint64_t{0};
         if (st.ph != st.pt) {

@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kSeqThreads, 1) seq_fc_kernel(SeqFcParams p) {
             warp_decode_triple(ys + warp * kFcMaxOut, s_lab, p.dec.class_fetch, p.dec.class_exec,
                                p.dec.class_store, (st.t_flags & kFlagStore) != 0, t3);
             apply_decoded_reg(st, t3, p.dec.pred_fetch, p.dec.per_cycle);
+            __syncwarp();  // every lane has read *sp (shared memory) before lane 0 rewrites it
             if (lane == 0) *sp = st;
           }
         }
