@@ -595,6 +595,74 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
       return;
     }
   }
+  // the C3 at one sub-trace (simulate_trace with the CNN), fp32: also one
+  // persistent launch (seq_c3_kernel), bit-identical to the rounds below
+  {
+    const ilsim_cnn_config& mcf = c->model.cfg;
+    int dev = 0, ctas = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev));
+    const bool c3_shape = mcf.n_conv == 3 && mcf.conv[0] == 64 && mcf.conv[1] == 64 && mcf.conv[2] == 64 &&
+                          mcf.input_channels == kSlots && mcf.sequence_length == 128 && !mcf.residual &&
+                          c->model.L.flat == 1024 && mc + 1 <= 128;
+    const bool seq = !oracle && !capture_mode && cfg.reserved[0] == 0 && c->precision == ILSIM_PREC_FP32 &&
+                     c3_shape && K == 1 && chunk == 1 && std::getenv("SIMNET_NO_SEQ_FC") == nullptr &&
+                     seq_c3_fits(mcf.fc_hidden, c->model.L.out_dim, ctas, static_cast<int>(pcap));
+    if (seq) {
+      uint32_t* d_flags = static_cast<uint32_t*>(c->seq_flags.need(4 * sizeof(uint32_t)));
+      CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t), c->stream));
+      SeqC3Params sp{};
+      sp.ctx = make_ctx(0, K, true, 0);
+      sp.dec = decode_params(0, K, fb);
+      const float* P = c->model.params.as<float>();
+      const ParamLayout& L = c->model.L;
+      sp.w0 = P + L.w[0];
+      sp.b0 = P + L.b[0];
+      sp.w1c = P + L.w[1];
+      sp.b1c = P + L.b[1];
+      sp.w2c = P + L.w[2];
+      sp.b2c = P + L.b[2];
+      sp.w1f = P + L.fc1_w;
+      sp.b1f = P + L.fc1_b;
+      sp.w2f = P + L.fc2_w;
+      sp.b2f = P + L.fc2_b;
+      sp.hidden = mcf.fc_hidden;
+      sp.od = L.out_dim;
+      sp.flat = fb.act[2];
+      sp.h = fb.act[3];
+      sp.flags = d_flags;
+      sp.rounds = rounds;
+      const bool seq_trace = std::getenv("SIMNET_SEQ_TRACE") != nullptr && rounds > 200;
+      if (seq_trace) {
+        sp.trace = static_cast<long long*>(c->seq_flags.need(4 * sizeof(uint32_t) + 16 * sizeof(long long))) + 2;
+        d_flags = static_cast<uint32_t*>(c->seq_flags.p);
+        sp.flags = d_flags;
+        CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t) + 16 * sizeof(long long), c->stream));
+      }
+      wait_windows(UINT32_MAX);
+      CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+      launch_seq_c3(sp, ctas, c->stream);
+      CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+      CUDA_OK(cudaGetLastError());
+      CUDA_OK(cudaEventSynchronize(c->ev[1]));
+      uint32_t hflags[4];
+      CUDA_OK(cudaMemcpy(hflags, d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+      if (hflags[2] != 0) throw ApiError("persistent C3 kernel: a CTA timed out waiting for its peers");
+      if (seq_trace) {  // diagnostics: phase boundaries of round 100 (ns)
+        long long tt[16];
+        CUDA_OK(cudaMemcpy(tt, sp.trace, sizeof(tt), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "seq_c3 round trace (ns): control wait_h %lld fc2 %lld decode %lld ctx %lld conv0 %lld "
+                     "conv1+2 %lld publish %lld | worker1 flat_seen %lld fc1 %lld h_published %lld\n",
+                     tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5],
+                     tt[7] - tt[6], tt[8] - tt[7], tt[9] - tt[8], tt[10] - tt[9]);
+      }
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      const double zero[4] = {0, 0, 0, 0};
+      finish(ms, 1, zero);
+      return;
+    }
+  }
   if (capture_mode && K > chunk) throw ApiError("input capture needs a single chunk");
   if (capture_mode && !fused && xprec == ILSIM_PREC_BF16) throw ApiError("input capture needs f32 inputs");
   const bool profile = cfg.reserved[0] != 0;  // per-kernel event timing, no graphs

@@ -325,4 +325,232 @@ void launch_seq_fc(SeqFcParams p, int ctas, cudaStream_t s) {
                                       smem, s));
 }
 
+// ---------------------------------------------------------------------------
+// The C3 at one sub-trace (simulate_trace with the CNN, fp32): the same
+// persistent structure.  The control CTA keeps the three conv layers' and FC2's
+// weights, the sub-trace state, its processor-queue ring AND the gathered input
+// row in shared memory, so per round it runs K1 (ctx_one writes the row into
+// shared memory), conv0 -> conv1 -> conv2, publishes the 1,024-float flat
+// output, and after the workers' FC1 runs FC2 + decode.  Worker CTAs keep FC1's
+// weight columns for their hidden units.  Every layer is the reference's order
+// (oracle/cnn_restated.cpp gemm_cm): one fma chain per output, k ascending,
+// then bias and ReLU -- bit-identical to the fp32 SIMT rounds.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kC3C = 64;  // channels of every C3 conv layer
+
+// One conv layer on the control CTA: out[j][o] = ReLU(chain_k W[k][o] * in[j][k] + b[o]),
+// in = [npos][kdim] (the previous layer's [2 npos][64] viewed as [npos][128]),
+// W = [kdim][64] (reference column-major).  Thread t: channel t % 64, positions
+// (t / 64) + 4 i, taken four at a time (four independent chains; k in steps of
+// 4, 16-B loads of the input rows).  Positions >= live have an all-+0 input
+// (conv0: columns past the context): their chain is +0 exactly, so their
+// output is ReLU(+0 + b) without the loop.  (Also skipping conv1 / conv2 rows
+// built only from such rows, computing their shared value once, measured
+// slower: the single serial chain it adds outweighs the rows it saves.)
+template <int kPos>
+__device__ __forceinline__ void conv_layer(const float* in, int kdim, const float* w, const float* b, float* out,
+                                           int live) {
+  const int o = threadIdx.x % kC3C, pg = threadIdx.x / kC3C;
+  constexpr int kPer = kPos / 4;
+  const float bo = b[o];
+#pragma unroll 1
+  for (int ib = 0; ib < kPer; ib += 4) {
+    if (pg + 4 * ib >= live) {  // warp-uniform: the rest of this thread's positions are dead
+      for (int i = ib; i < kPer; ++i) out[(pg + 4 * i) * kC3C + o] = fmaxf(0.0f + bo, 0.0f);
+      break;
+    }
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const float* r0 = in + (pg + 4 * ib) * kdim;
+#pragma unroll 2
+    for (int k = 0; k < kdim; k += 4) {
+      const float w0 = w[(k + 0) * kC3C + o], w1 = w[(k + 1) * kC3C + o];
+      const float w2 = w[(k + 2) * kC3C + o], w3 = w[(k + 3) * kC3C + o];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 x = *reinterpret_cast<const float4*>(r0 + 4 * i * kdim + k);
+        acc[i] = fmaf(w0, x.x, acc[i]);
+        acc[i] = fmaf(w1, x.y, acc[i]);
+        acc[i] = fmaf(w2, x.z, acc[i]);
+        acc[i] = fmaf(w3, x.w, acc[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[(pg + 4 * (ib + i)) * kC3C + o] = fmaxf(acc[i] + bo, 0.0f);
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSeqThreads, 1) seq_c3_kernel(SeqC3Params p) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ CtxSmem csm;
+  __shared__ uint32_t s_flag;
+  __shared__ __align__(16) SubState s_sub[1];
+  const int tid = threadIdx.x;
+  const int workers = gridDim.x - 1;
+
+  if (blockIdx.x == 0) {
+    // ------------------------------ control CTA ------------------------------
+    __shared__ double s_lab[6];
+    __shared__ float ys[kFcMaxOut];
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid < 6) s_lab[tid] = tid < 3 ? p.dec.nc->label_mean[tid] : p.dec.nc->label_sd[tid - 3];
+    float* w0 = sm;                        // [100][64]
+    float* w1 = w0 + 100 * kC3C;           // [128][64]
+    float* w2 = w1 + 128 * kC3C;           // [128][64]
+    float* bs = w2 + 128 * kC3C;           // b0 | b1 | b2 (3 x 64)
+    float* w2f = bs + 3 * kC3C;            // FC2 [hidden][od]
+    float* x = w2f + p.hidden * p.od + ((4 - (p.hidden * p.od) % 4) % 4);  // [128 columns][50], 16-B aligned
+    float* a0 = x + 128 * kSlots;          // [64][64]
+    float* a1 = a0 + 64 * kC3C;            // [32][64]
+    float* a2 = a1 + 32 * kC3C;            // [16][64] = flat
+    float* hs = a2 + 16 * kC3C;            // [hidden]
+    RingEntry* s_proc = reinterpret_cast<RingEntry*>(hs + ((p.hidden + 3) & ~3));  // [pcap]
+    const uint32_t pcap = p.ctx.pmask + 1;
+    for (int i = tid; i < 100 * kC3C; i += kSeqThreads) w0[i] = p.w0[i];
+    for (int i = tid; i < 128 * kC3C; i += kSeqThreads) w1[i] = p.w1c[i];
+    for (int i = tid; i < 128 * kC3C; i += kSeqThreads) w2[i] = p.w2c[i];
+    for (int i = tid; i < 3 * kC3C; i += kSeqThreads) bs[i] = (i < kC3C ? p.b0 : (i < 2 * kC3C ? p.b1c : p.b2c))[i % kC3C];
+    for (int i = tid; i < p.hidden * p.od; i += kSeqThreads) w2f[i] = p.w2f[i];
+    for (int i = tid; i < 128 * kSlots; i += kSeqThreads) x[i] = 0.0f;  // padding columns stay +0
+    for (int i = tid; i < static_cast<int>(sizeof(SubState) / 4); i += kSeqThreads)
+      reinterpret_cast<uint32_t*>(s_sub)[i] = reinterpret_cast<const uint32_t*>(p.ctx.state + p.ctx.first)[i];
+    CtxParams cx = p.ctx;
+    cx.state = s_sub - p.ctx.first;
+    cx.proc = s_proc - p.ctx.first * pcap;
+    cx.x = x;  // the gathered row goes to shared memory
+    cx.x_full = 0;
+    __syncthreads();
+    for (uint32_t r = 0; r <= p.rounds; ++r) {
+      long long* tr = (p.trace && r == kTraceRound && tid == 0) ? p.trace : nullptr;
+      if (r > 0) {
+        // FC2 + decode of round r-1
+        if (tr) tr[0] = gtimer();
+        prefetch_context(cx, s_sub, s_proc, pcap, 1);
+        if (tid == 0) s_flag = wait_at_least(p.flags + 1, r * static_cast<uint32_t>(workers), p.flags + 2);
+        __syncthreads();
+        if (s_flag == kExit) break;
+        if (tr) tr[1] = gtimer();
+        for (int i = tid; i < p.hidden; i += kSeqThreads) hs[i] = __ldcg(p.h + i);
+        __syncthreads();
+        if (tid < p.od) {
+          float y = 0.0f;
+#pragma unroll 8
+          for (int k = 0; k < p.hidden; ++k) y = fmaf(w2f[k * p.od + tid], hs[k], y);
+          ys[tid] = y + p.b2f[tid];
+        }
+        __syncthreads();
+        if (tr) tr[2] = gtimer();
+        if (warp == 0) {
+          SubState st = s_sub[0];
+          if (st.status == kOk && st.pos < st.len) {
+            uint32_t t3[3];
+            warp_decode_triple(ys, s_lab, p.dec.class_fetch, p.dec.class_exec, p.dec.class_store,
+                               (st.t_flags & kFlagStore) != 0, t3);
+            apply_decoded_reg(st, t3, p.dec.pred_fetch, p.dec.per_cycle);
+            __syncwarp();
+            if (lane == 0) s_sub[0] = st;
+          }
+        }
+        __syncthreads();
+      }
+      if (tr) tr[3] = gtimer();
+      CtxParams cp = cx;
+      cp.gather = r < p.rounds ? 1 : 0;
+      ctx_one<kSeqThreads>(cp, cp.first, csm);
+      __syncthreads();
+      if (r == p.rounds) break;
+      if (tr) tr[4] = gtimer();
+      if (s_sub[0].status != kOk || s_sub[0].pos >= s_sub[0].len) {
+        // nothing was gathered (an error): publish anyway so the workers' round count stays in step
+      } else {
+        const int live = static_cast<int>(s_sub[0].xcols + 1) / 2;  // conv0 positions with a live column
+        conv_layer<64>(x, 100, w0, bs, a0, live);
+        __syncthreads();
+        if (tr) tr[5] = gtimer();
+        conv_layer<32>(a0, 128, w1, bs + kC3C, a1, 32);
+        __syncthreads();
+        conv_layer<16>(a1, 128, w2, bs + 2 * kC3C, a2, 16);
+        __syncthreads();
+        if (tr) tr[6] = gtimer();
+      }
+      for (int i = tid; i < 16 * kC3C; i += kSeqThreads) p.flat[i] = a2[i];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(p.flags, r + 1);
+      if (tr) tr[7] = gtimer();
+    }
+    __syncthreads();
+    if (tid == 0) st_release(p.flags, kExit);
+    for (int i = tid; i < static_cast<int>(sizeof(SubState) / 4); i += kSeqThreads)
+      reinterpret_cast<uint32_t*>(p.ctx.state + p.ctx.first)[i] = reinterpret_cast<const uint32_t*>(s_sub)[i];
+    return;
+  }
+
+  // ------------------------------ worker CTAs: FC1 ------------------------------
+  const int wid = blockIdx.x - 1;
+  const int o0 = static_cast<int>(static_cast<int64_t>(p.hidden) * wid / workers);
+  const int o1 = static_cast<int>(static_cast<int64_t>(p.hidden) * (wid + 1) / workers);
+  const int outs = o1 - o0;
+  float* w1s = sm;                 // [1024][outs]
+  float* fs = w1s + 1024 * 4;      // flat [1024]
+  for (int i = tid; i < 1024 * outs; i += kSeqThreads) {
+    const int k = i / outs, ol = i % outs;
+    w1s[i] = p.w1f[static_cast<uint64_t>(k) * p.hidden + o0 + ol];
+  }
+  __syncthreads();
+  for (uint32_t r = 0;; ++r) {
+    long long* tr = (p.trace && r == kTraceRound && tid == 0 && blockIdx.x == 1) ? p.trace + 8 : nullptr;
+    if (tid == 0) s_flag = wait_at_least(p.flags, r + 1, p.flags + 2);
+    __syncthreads();
+    if (s_flag == kExit) break;
+    if (tr) tr[0] = gtimer();
+    for (int i = tid; i < 1024 / 4; i += kSeqThreads)
+      reinterpret_cast<float4*>(fs)[i] = __ldcg(reinterpret_cast<const float4*>(p.flat) + i);
+    __syncthreads();
+    if (tid < outs) {  // one chain over K = 1024 (the reference's order), 32 loads in flight per block
+      float acc = 0.0f;
+      for (int k = 0; k < 1024; k += 32) {
+        float xv[32], wv[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          xv[u] = fs[k + u];
+          wv[u] = w1s[(k + u) * outs + tid];
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc = fmaf(wv[u], xv[u], acc);
+      }
+      p.h[o0 + tid] = fmaxf(acc + p.b1f[o0 + tid], 0.0f);
+    }
+    if (tr) tr[1] = gtimer();
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(p.flags + 1, 1u);
+    if (tr) tr[2] = gtimer();
+  }
+}
+
+size_t seq_c3_smem(int hidden, int od, int pcap) {
+  const size_t control = (static_cast<size_t>(100 + 128 + 128) * kC3C + 3 * kC3C + static_cast<size_t>(hidden) * od +
+                          4 + 128 * kSlots + (64 + 32 + 16) * kC3C + ((hidden + 3) & ~3)) * 4 +
+                         static_cast<size_t>(pcap) * sizeof(RingEntry) + 16;
+  const size_t worker = (1024 * 4 + 1024) * 4;
+  return control > worker ? control : worker;
+}
+
+bool seq_c3_fits(int hidden, int od, int ctas, int pcap) {
+  if (ctas < 2 || od > kFcMaxOut || (hidden + ctas - 2) / (ctas - 1) > 4) return false;
+  return seq_c3_smem(hidden, od, pcap) + sizeof(CtxSmem) + 1024 <= 227 * 1024;
+}
+
+void launch_seq_c3(SeqC3Params p, int ctas, cudaStream_t s) {
+  const size_t smem = seq_c3_smem(p.hidden, p.od, static_cast<int>(p.ctx.pmask + 1));
+  CUDA_OK(cudaFuncSetAttribute(seq_c3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  void* args[] = {&p};
+  CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(seq_c3_kernel), dim3(ctas), dim3(kSeqThreads), args,
+                                      smem, s));
+}
+
 }  // namespace simnet

@@ -21,6 +21,23 @@ struct SeqFcParams {
 };
 
 bool seq_fc_fits(int flat, int hidden, int od, int K, int ctas, int pcap);
+
+// The C3 (3 x 64-channel conv, 50 x 128 input) at ONE sub-trace, fp32.
+struct SeqC3Params {
+  CtxParams ctx;         // K1 for the sub-trace [ctx.first, ctx.first + 1); ctx.x is replaced by shared memory
+  DecodeParams dec;      // K3
+  const float *w0, *b0, *w1c, *b1c, *w2c, *b2c;  // conv weights [2 cin][64] (reference layout) and biases
+  const float *w1f, *b1f;                         // FC1 [1024][hidden]
+  const float *w2f, *b2f;                         // FC2 [hidden][od]
+  int32_t hidden, od;
+  float* flat;           // [1024] conv2 output (global, control -> workers)
+  float* h;              // [hidden] FC1 output (global, workers -> control)
+  uint32_t* flags;       // [0] flat published (round + 1, or ~0 = exit), [1] hidden-slice count, [2] error
+  uint32_t rounds;
+  long long* trace;      // diagnostics (SIMNET_SEQ_TRACE): %globaltimer at phase boundaries of one round
+};
+bool seq_c3_fits(int hidden, int od, int ctas, int pcap);
+void launch_seq_c3(SeqC3Params p, int ctas, cudaStream_t s);
 void launch_seq_fc(SeqFcParams p, int ctas, cudaStream_t s);
 
 }  // namespace simnet

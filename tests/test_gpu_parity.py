@@ -804,3 +804,36 @@ def test_scale_parity_against_reference_fixture(gpu, name, precision, exact, min
         assert out["fetch_block_identical_frac"] == 1.0
     else:
         assert out["fetch_block_identical_frac"] >= min_blocks, out
+
+
+@pytest.mark.parametrize("model_name", ["trained", "synthetic"])
+def test_sequential_c3_persistent_kernel(gpu, port, model_name, monkeypatch):
+    """The C3 at one sub-trace (simulate_trace with the CNN, fp32) runs as ONE
+    persistent cooperative launch (seq_c3_kernel): bit for bit the
+    launch-per-layer rounds (SIMNET_NO_SEQ_FC) and the oracle port's
+    sequential simulation (the reference's restated forward order), with the
+    trained C3's narrow margins as well."""
+    import sys
+
+    t = read_trace(GOLD / "mix_3000_s4.trace")
+    if model_name == "trained":
+        m = read_model(GOLD / "c3_trained.model")
+    else:
+        sys.path.insert(0, str(GOLD.parents[1]))
+        from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace
+
+        m = synthetic_model(synthetic_trace(50_000, 101), 1, init_params=port.init_params)
+    g = gpu("fp32")
+    g.load_model(m)
+    pc = pcfg(1, mc=m.config.max_context)
+    g.load_trace(t, pc)
+    monkeypatch.delenv("SIMNET_NO_SEQ_FC", raising=False)
+    a = g.run(pc)
+    assert a.launches == 1  # the persistent kernel ran
+    monkeypatch.setenv("SIMNET_NO_SEQ_FC", "1")
+    b = g.run(pc)
+    assert b.launches > 1000
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
+    want = port.simulate(t, m, sequential=True)
+    assert gpu_subs(a).tolist() == np.asarray(want["subs"]).tolist()
+    assert np.array_equal(a.predicted_fetch, want["predicted_fetch"])
