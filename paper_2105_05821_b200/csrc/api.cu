@@ -533,128 +533,92 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
     for (int q = 0; q < 4; ++q) tot->kernel_ms[q] = kms[q];
     tot->launches = launches;
   };
-  // FC-only predictor, fp32, a handful of sub-traces (the sequential c1
-  // configuration): the whole simulation is one persistent cooperative launch
-  // (seq_fc.cu), bit-identical to the launch-per-layer rounds below
-  // (SIMNET_NO_SEQ_FC=1 forces those, A/B)
-  {
-    const ilsim_cnn_config& mc_cfg = c->model.cfg;
-    int dev = 0, ctas = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    CUDA_OK(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev));
-    const bool seq = !oracle && !capture_mode && cfg.reserved[0] == 0 && c->precision == ILSIM_PREC_FP32 &&
-                     mc_cfg.n_conv == 0 && K == chunk && std::getenv("SIMNET_NO_SEQ_FC") == nullptr &&
-                     seq_fc_fits(c->model.L.flat, mc_cfg.fc_hidden, c->model.L.out_dim, static_cast<int>(K), ctas,
-                                 static_cast<int>(pcap));
-    if (seq) {
-      uint32_t* d_flags = static_cast<uint32_t*>(c->seq_flags.need(4 * sizeof(uint32_t)));
-      CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t), c->stream));
-      SeqFcParams sp{};
-      sp.ctx = make_ctx(0, K, true, 0);
-      sp.dec = decode_params(0, K, fb);
-      const float* P = c->model.params.as<float>();
-      sp.w1 = P + c->model.L.fc1_w;
-      sp.b1 = P + c->model.L.fc1_b;
-      sp.w2 = P + c->model.L.fc2_w;
-      sp.b2 = P + c->model.L.fc2_b;
-      sp.flat = static_cast<int32_t>(c->model.L.flat);
-      sp.hidden = mc_cfg.fc_hidden;
-      sp.od = c->model.L.out_dim;
-      sp.h = fb.act[0];
-      sp.y = fb.y;
-      sp.flags = d_flags;
-      sp.rounds = rounds;
-      const bool seq_trace = std::getenv("SIMNET_SEQ_TRACE") != nullptr && rounds > 200;
-      if (seq_trace) {
-        sp.trace = static_cast<long long*>(c->seq_flags.need(4 * sizeof(uint32_t) + 16 * sizeof(long long))) + 2;
-        d_flags = static_cast<uint32_t*>(c->seq_flags.p);
-        sp.flags = d_flags;
-        CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t) + 16 * sizeof(long long), c->stream));
-      }
-      wait_windows(UINT32_MAX);
-      CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
-      launch_seq_fc(sp, ctas, c->stream);
-      CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
-      CUDA_OK(cudaGetLastError());
-      CUDA_OK(cudaEventSynchronize(c->ev[1]));
-      uint32_t hflags[4];
-      CUDA_OK(cudaMemcpy(hflags, d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
-      if (hflags[2] != 0) throw ApiError("persistent FC kernel: a CTA timed out waiting for its peers");
-      if (seq_trace) {  // diagnostics: phase boundaries of round 100 (ns from the control CTA's wait)
-        long long tt[16];
-        CUDA_OK(cudaMemcpy(tt, sp.trace, sizeof(tt), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "seq_fc round trace (ns): control wait_h %lld stage_h %lld fc2 %lld decode %lld ctx %lld "
-                     "publish %lld | worker1 x_seen %lld stage_x %lld fc1 %lld h_published %lld\n",
-                     tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5],
-                     tt[9] - tt[6], tt[10] - tt[9], tt[11] - tt[10], tt[12] - tt[11]);
-      }
-      float ms = 0;
-      CUDA_OK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-      const double zero[4] = {0, 0, 0, 0};
-      finish(ms, 1, zero);
-      return;
-    }
-  }
-  // the C3 at one sub-trace (simulate_trace with the CNN), fp32: also one
-  // persistent launch (seq_c3_kernel), bit-identical to the rounds below
+  // Persistent kernels for the sequential configurations (seq_fc.cu): the
+  // FC-only predictor at K <= 2 (c1) and the C3 at K = 1 (simulate_trace with
+  // the CNN), fp32.  The whole simulation is one cooperative launch,
+  // bit-identical to the launch-per-layer rounds below (SIMNET_NO_SEQ_FC=1
+  // forces those, A/B; SIMNET_SEQ_TRACE=1 prints one round's phase times).
   {
     const ilsim_cnn_config& mcf = c->model.cfg;
+    const ParamLayout& L = c->model.L;
     int dev = 0, ctas = 0;
     CUDA_OK(cudaGetDevice(&dev));
     CUDA_OK(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev));
+    const bool eligible = !oracle && !capture_mode && cfg.reserved[0] == 0 && c->precision == ILSIM_PREC_FP32 &&
+                          K == chunk && std::getenv("SIMNET_NO_SEQ_FC") == nullptr;
+    const bool fc_seq = eligible && mcf.n_conv == 0 &&
+                        seq_fc_fits(L.flat, mcf.fc_hidden, L.out_dim, static_cast<int>(K), ctas, static_cast<int>(pcap));
     const bool c3_shape = mcf.n_conv == 3 && mcf.conv[0] == 64 && mcf.conv[1] == 64 && mcf.conv[2] == 64 &&
                           mcf.input_channels == kSlots && mcf.sequence_length == 128 && !mcf.residual &&
-                          c->model.L.flat == 1024 && mc + 1 <= 128;
-    const bool seq = !oracle && !capture_mode && cfg.reserved[0] == 0 && c->precision == ILSIM_PREC_FP32 &&
-                     c3_shape && K == 1 && chunk == 1 && std::getenv("SIMNET_NO_SEQ_FC") == nullptr &&
-                     seq_c3_fits(mcf.fc_hidden, c->model.L.out_dim, ctas, static_cast<int>(pcap));
-    if (seq) {
-      uint32_t* d_flags = static_cast<uint32_t*>(c->seq_flags.need(4 * sizeof(uint32_t)));
-      CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t), c->stream));
-      SeqC3Params sp{};
-      sp.ctx = make_ctx(0, K, true, 0);
-      sp.dec = decode_params(0, K, fb);
+                          L.flat == 1024 && mc + 1 <= 128;
+    const bool c3_seq = eligible && c3_shape && K == 1 &&
+                        seq_c3_fits(mcf.fc_hidden, L.out_dim, ctas, static_cast<int>(pcap));
+    if (fc_seq || c3_seq) {
+      // flags [0..3] (+ 16 trace words): zeroed before the launch
+      const bool trace = std::getenv("SIMNET_SEQ_TRACE") != nullptr && rounds > 200;
+      const size_t fbytes = 4 * sizeof(uint32_t) + (trace ? 16 * sizeof(long long) : 0);
+      uint32_t* d_flags = static_cast<uint32_t*>(c->seq_flags.need(fbytes));
+      long long* d_trace = trace ? reinterpret_cast<long long*>(d_flags + 4) : nullptr;
+      CUDA_OK(cudaMemsetAsync(d_flags, 0, fbytes, c->stream));
       const float* P = c->model.params.as<float>();
-      const ParamLayout& L = c->model.L;
-      sp.w0 = P + L.w[0];
-      sp.b0 = P + L.b[0];
-      sp.w1c = P + L.w[1];
-      sp.b1c = P + L.b[1];
-      sp.w2c = P + L.w[2];
-      sp.b2c = P + L.b[2];
-      sp.w1f = P + L.fc1_w;
-      sp.b1f = P + L.fc1_b;
-      sp.w2f = P + L.fc2_w;
-      sp.b2f = P + L.fc2_b;
-      sp.hidden = mcf.fc_hidden;
-      sp.od = L.out_dim;
-      sp.flat = fb.act[2];
-      sp.h = fb.act[3];
-      sp.flags = d_flags;
-      sp.rounds = rounds;
-      const bool seq_trace = std::getenv("SIMNET_SEQ_TRACE") != nullptr && rounds > 200;
-      if (seq_trace) {
-        sp.trace = static_cast<long long*>(c->seq_flags.need(4 * sizeof(uint32_t) + 16 * sizeof(long long))) + 2;
-        d_flags = static_cast<uint32_t*>(c->seq_flags.p);
-        sp.flags = d_flags;
-        CUDA_OK(cudaMemsetAsync(d_flags, 0, 4 * sizeof(uint32_t) + 16 * sizeof(long long), c->stream));
-      }
       wait_windows(UINT32_MAX);
       CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
-      launch_seq_c3(sp, ctas, c->stream);
+      if (fc_seq) {
+        SeqFcParams sp{};
+        sp.ctx = make_ctx(0, K, true, 0);
+        sp.dec = decode_params(0, K, fb);
+        sp.w1 = P + L.fc1_w;
+        sp.b1 = P + L.fc1_b;
+        sp.w2 = P + L.fc2_w;
+        sp.b2 = P + L.fc2_b;
+        sp.flat = static_cast<int32_t>(L.flat);
+        sp.hidden = mcf.fc_hidden;
+        sp.od = L.out_dim;
+        sp.h = fb.act[0];
+        sp.y = fb.y;
+        sp.flags = d_flags;
+        sp.rounds = rounds;
+        sp.trace = d_trace;
+        launch_seq_fc(sp, ctas, c->stream);
+      } else {
+        SeqC3Params sp{};
+        sp.ctx = make_ctx(0, K, true, 0);
+        sp.dec = decode_params(0, K, fb);
+        sp.w0 = P + L.w[0];
+        sp.b0 = P + L.b[0];
+        sp.w1c = P + L.w[1];
+        sp.b1c = P + L.b[1];
+        sp.w2c = P + L.w[2];
+        sp.b2c = P + L.b[2];
+        sp.w1f = P + L.fc1_w;
+        sp.b1f = P + L.fc1_b;
+        sp.w2f = P + L.fc2_w;
+        sp.b2f = P + L.fc2_b;
+        sp.hidden = mcf.fc_hidden;
+        sp.od = L.out_dim;
+        sp.flat = fb.act[2];
+        sp.h = fb.act[3];
+        sp.flags = d_flags;
+        sp.rounds = rounds;
+        sp.trace = d_trace;
+        launch_seq_c3(sp, ctas, c->stream);
+      }
       CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
       CUDA_OK(cudaGetLastError());
       CUDA_OK(cudaEventSynchronize(c->ev[1]));
       uint32_t hflags[4];
       CUDA_OK(cudaMemcpy(hflags, d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
-      if (hflags[2] != 0) throw ApiError("persistent C3 kernel: a CTA timed out waiting for its peers");
-      if (seq_trace) {  // diagnostics: phase boundaries of round 100 (ns)
+      if (hflags[2] != 0) throw ApiError("persistent kernel: a CTA timed out waiting for its peers");
+      if (trace) {  // diagnostics: phase boundaries of round 100 (ns); control words 0-7, worker 1 words 8-15
         long long tt[16];
-        CUDA_OK(cudaMemcpy(tt, sp.trace, sizeof(tt), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "seq_c3 round trace (ns): control wait_h %lld fc2 %lld decode %lld ctx %lld conv0 %lld "
-                     "conv1+2 %lld publish %lld | worker1 flat_seen %lld fc1 %lld h_published %lld\n",
-                     tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5],
-                     tt[7] - tt[6], tt[8] - tt[7], tt[9] - tt[8], tt[10] - tt[9]);
+        CUDA_OK(cudaMemcpy(tt, d_trace, sizeof(tt), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "%s round trace (ns), control:", fc_seq ? "seq_fc" : "seq_c3");
+        for (int i = 1; i < 8; ++i)
+          if (tt[i] != 0) std::fprintf(stderr, " %lld", tt[i] - tt[i - 1]);
+        std::fprintf(stderr, " | worker 1:");
+        for (int i = 9; i < 16; ++i)
+          if (tt[i] != 0) std::fprintf(stderr, " %lld", tt[i] - tt[i - 1]);
+        std::fprintf(stderr, "\n");
       }
       float ms = 0;
       CUDA_OK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
