@@ -837,3 +837,24 @@ def test_sequential_c3_persistent_kernel(gpu, port, model_name, monkeypatch):
     want = port.simulate(t, m, sequential=True)
     assert gpu_subs(a).tolist() == np.asarray(want["subs"]).tolist()
     assert np.array_equal(a.predicted_fetch, want["predicted_fetch"])
+
+
+def test_device_group_concurrent_persistent_kernels(gpu):
+    """Two group members on the same GPU, one sub-trace each, fp32 C3: both
+    run the persistent cooperative kernel at once from their host threads
+    (cooperative grids are gang-scheduled, so one waits for the other; every
+    wait inside is bounded, so a scheduling problem would be an error, not a
+    hang); results equal the single-context launch-per-layer run of K = 2."""
+    from paper_2105_05821_b200 import GpuGroup
+
+    t = read_trace(GOLD / "mix_3000_s4.trace").slice(0, 1200)
+    m = read_model(GOLD / "c3_trained.model")
+    pc = pcfg(2, mc=m.config.max_context)
+    g = gpu("fp32")
+    g.load_model(m)
+    want = g.simulate_parallel(t, pc)
+    with GpuGroup([0, 0], "fp32") as grp:
+        grp.load_model(m)
+        got = grp.simulate_parallel(t, pc)
+        assert gpu_subs(got).tolist() == gpu_subs(want).tolist()
+        assert np.array_equal(got.predicted_fetch, want.predicted_fetch)
