@@ -484,6 +484,18 @@ def main():
                 "frac_of_3xtf32_ceiling": achieved / (peak_val / 3) if args.precision == "tf32x3" else None,
                 "traffic": ncu_traffic(args.precision)}
 
+    # the same kernel against HBM: its DRAM bytes per launch (ncu capture,
+    # cold caches: an upper bound) over the live launch time -- the K1 gather /
+    # K3 decode half of the fused front is memory-latency-bound, not HBM-bound
+    roofline_hbm = None
+    if tc and roofline["traffic"]:
+        hbm_peak = pk.get("hbm_gbs", 6549.8)
+        ach = roofline["traffic"] / (launch_ms / 1e3) / 1e9
+        roofline_hbm = {"bound": "hbm", "kernel": dom_name, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": ach / hbm_peak, "bytes_per_launch": roofline["traffic"],
+                        "source": "dram bytes per launch from the committed ncu --set full capture "
+                                  "(profiles/ncu_traffic.json) / the live event-timed launch"}
+
     # e2e through the public C-ABI with host buffers (pinned), copies inside
     e2e_line = None
     if rank == 0 or world > 1:
@@ -528,6 +540,7 @@ def main():
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "kernels_ms_per_step": k_ms,
         "roofline": roofline,
+        "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu_base,
         "e2e": e2e_line,
         "gpu_launches": launches,
