@@ -141,13 +141,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def ncu_traffic(precision: str):
+NCU_TRAFFIC_SAMPLES = 1024  # the captures in profiles/ncu_traffic.json are launches over 1,024 sub-traces
+
+
+def ncu_traffic(precision: str, samples: int = NCU_TRAFFIC_SAMPLES):
     """DRAM bytes (read + write) per launch of the dominant kernel from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    committed ncu --set full capture (profiles/ncu_traffic.json, a launch over
+    1,024 sub-traces), scaled to a launch over `samples` sub-traces, or None."""
     try:
-        return json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).get(precision)
+        v = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).get(precision)
     except (OSError, ValueError):
         return None
+    return None if v is None else v * samples / NCU_TRAFFIC_SAMPLES
 
 
 def tc_peaks():
@@ -482,7 +487,7 @@ def main():
                 "unit": "TFLOP/s", "frac": achieved / peak_val, "peak_source": peak_src,
                 "algorithmic_flops_per_launch": flops_launch, "launch_us": 1e3 * launch_ms,
                 "frac_of_3xtf32_ceiling": achieved / (peak_val / 3) if args.precision == "tf32x3" else None,
-                "traffic": ncu_traffic(args.precision)}
+                "traffic": ncu_traffic(args.precision, len(results[-1].sub_results))}
 
     # the same kernel against HBM: its DRAM bytes per launch (ncu capture,
     # cold caches: an upper bound) over the live launch time -- the K1 gather /
