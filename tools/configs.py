@@ -109,6 +109,35 @@ def c4(args):
           "drain_cycles": sum(s.drain_cycles for s in r.sub_results), "parity": compare("c4", r, t, m)})
 
 
+def seq(args):
+    """simulate_trace with the C3 (K = 1) on the c2 trace, fp32: the persistent
+    kernel (seq_c3_kernel) against the reference's own single-thread
+    simulate_trace of the same trace and weights (the c5 K = 1 fixture,
+    tools/cpu_long_refs.py c5): CPI error and fetch-block identity."""
+    from scale_parity import block_hashes, model_digest, trace_digest
+
+    n = args.c5_n
+    t = synthetic_trace(n, 101)
+    m = synthetic_model(synthetic_trace(200_000, 101), 1)
+    g = GpuSimulator(0, "fp32")
+    g.load_model(m)
+    r = run(g, t, ParallelConfig(k=1, sim=SimConfig(max_context=m.config.max_context)), reps=1)
+    out = {"config": "sequential C3 (simulate_trace, K = 1)", "precision": "fp32",
+           "path": "persistent cooperative kernel (seq_c3_kernel, 1 launch)" if r.launches == 1 else
+                   f"launch-per-layer rounds ({r.launches} launches)",
+           "instructions": n, "gpu_mips": n / (r.device_ms / 1e3) / 1e6, "us_per_instruction": 1e3 * r.device_ms / n,
+           "gpu_cpi": r.cpi}
+    ref = _k1_ref("c5")
+    if ref and ref["instructions"] == n and ref["trace_digest"] == trace_digest(t) and \
+            ref["model_digest"] == model_digest(m):
+        got = block_hashes(r.predicted_fetch)
+        out.update(ref_cpi=ref["cpi"], ref_mips=ref["cpu_mips"], ref_impl=ref["impl"],
+                   cpi_error_percent=100.0 * (r.cpi - ref["cpi"]) / ref["cpi"],
+                   fetch_block_identical_frac=float((got == np.array(ref["fetch_blocks"], np.uint64)).mean()),
+                   gpu_over_cpu=out["gpu_mips"] / ref["cpu_mips"])
+    emit(out)
+
+
 def c5(args):
     """Sub-trace count sweep on the c2 trace (10M instructions) up to 1M
     sub-traces x warm-up overlap x drain-trim: owned-instruction MIPS vs the
