@@ -309,10 +309,32 @@ size_t seq_fc_smem(int flat, int hidden, int od, int K, int ctas, int pcap) {
   return worker > control ? worker : control;
 }
 
+// A cooperative grid of `ctas` CTAs must be co-resident: one per SM needs the
+// shared memory (and nothing else on the device holding the SMs, e.g. MPS
+// clients).  When the occupancy query says no, the caller takes the
+// launch-per-layer rounds instead.
+bool coresident(const void* kernel, int threads, size_t smem, int ctas) {
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int per_sm = 0, dev = 0, sms = 0, coop = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess ||
+      cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return coop != 0 && per_sm * sms >= ctas;
+}
+
 bool seq_fc_fits(int flat, int hidden, int od, int K, int ctas, int pcap) {
   if (ctas < 2 || K < 1 || K > 8 || hidden < ctas - 1) return false;
-  const size_t need = seq_fc_smem(flat, hidden, od, K, ctas, pcap) + sizeof(CtxSmem) + 8 * kFcMaxOut * 4 + 128;
-  return need <= 227 * 1024;
+  const size_t smem = seq_fc_smem(flat, hidden, od, K, ctas, pcap);
+  const size_t need = smem + sizeof(CtxSmem) + 8 * kFcMaxOut * 4 + 128;
+  return need <= 227 * 1024 && coresident(reinterpret_cast<const void*>(seq_fc_kernel), kSeqThreads, smem, ctas);
 }
 
 void launch_seq_fc(SeqFcParams p, int ctas, cudaStream_t s) {
@@ -542,7 +564,9 @@ size_t seq_c3_smem(int hidden, int od, int pcap) {
 
 bool seq_c3_fits(int hidden, int od, int ctas, int pcap) {
   if (ctas < 2 || od > kFcMaxOut || (hidden + ctas - 2) / (ctas - 1) > 4) return false;
-  return seq_c3_smem(hidden, od, pcap) + sizeof(CtxSmem) + 1024 <= 227 * 1024;
+  const size_t smem = seq_c3_smem(hidden, od, pcap);
+  return smem + sizeof(CtxSmem) + 1024 <= 227 * 1024 &&
+         coresident(reinterpret_cast<const void*>(seq_c3_kernel), kSeqThreads, smem, ctas);
 }
 
 void launch_seq_c3(SeqC3Params p, int ctas, cudaStream_t s) {
