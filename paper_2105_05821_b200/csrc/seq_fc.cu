@@ -1,7 +1,9 @@
-// Persistent kernel for the FC-only predictor at small K (the sequential
-// configuration c1: one sub-trace, K = 1): the whole simulation -- every round
-// of K1 (apply + gather), K2 (FC1 -> ReLU -> FC2) and K3 (decode + clock) --
-// is ONE cooperative launch (SURVEY.md §8(f) rank 1 for this predictor).
+// Persistent kernels for the sequential configurations:
+//   seq_fc_kernel  the FC-only predictor at K <= 2 (config c1: one sub-trace);
+//   seq_c3_kernel  the C3 at one sub-trace (simulate_trace with the CNN), below.
+// The whole simulation -- every round of K1 (apply + gather), K2 (the
+// predictor) and K3 (decode + clock) -- is ONE cooperative launch.  For the
+// FC-only predictor:
 //
 // A round of the launch-per-layer path is six dependent launches (ctx, two
 // split-K GEMV pairs, decode), each a few microseconds of launch latency for
