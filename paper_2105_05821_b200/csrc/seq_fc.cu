@@ -113,14 +113,16 @@ __device__ __forceinline__ void prefetch_context(const CtxParams& cx, const SubS
     const uint32_t n = st.pt - st.ph;
     const uint32_t lines = 2 * (n + 2);  // + the next two targets
     for (uint32_t i = threadIdx.x; i < lines; i += kSeqThreads) {
-      const uint32_t e = i >> 1;
+      const uint32_t e = i >> 1;  // entry e of the context (newest first), then the next two targets
       uint64_t row;
-      if (e < n)
+      if (e < n) {
         row = st.begin + proc_all[s * pcap + ((st.pt - 1 - e) & (pcap - 1))].idx;
-      else
-        row = st.begin + st.pos + (e - n);
-      if (st.pos + (e >= n ? e - n : 0) >= st.len && e >= n) continue;
-      const float* a = cx.stat + row * kStatStride + (i & 1) * 32;
+      } else {
+        const uint32_t pos = st.pos + (e - n);
+        if (pos >= st.len) continue;  // past the sub-trace
+        row = st.begin + pos;
+      }
+      const float* a = cx.stat + row * kStatStride + (i & 1) * 32;  // the row's two 128-B lines
       asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
     }
   }
