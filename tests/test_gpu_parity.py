@@ -859,3 +859,31 @@ def test_device_group_concurrent_persistent_kernels(gpu):
         got = grp.simulate_parallel(t, pc)
         assert gpu_subs(got).tolist() == gpu_subs(want).tolist()
         assert np.array_equal(got.predicted_fetch, want.predicted_fetch)
+
+
+def test_persistent_c3_error_paths(gpu, monkeypatch):
+    """A sub-trace error inside the persistent C3 kernel (an explicit write
+    ring too small for the store queue) ends the run with the same reported
+    error as the launch-per-layer rounds (the kernel keeps its rounds in step
+    and leaves; nothing hangs); with the ring on auto both paths rerun with a
+    larger ring and agree."""
+    t = store_heavy(5, 3000, lat_hi=400)
+    m = read_model(GOLD / "c3_trained.model")
+    g = gpu("fp32")
+    g.load_model(m)
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("SIMNET_NO_SEQ_FC", env)
+        else:
+            monkeypatch.delenv("SIMNET_NO_SEQ_FC", raising=False)
+        pc = pcfg(1, mc=m.config.max_context, write_ring=2)
+        g.load_trace(t, pc)
+        with pytest.raises(IlsimError, match="write queue ring overflow"):
+            g.run(pc)
+    monkeypatch.delenv("SIMNET_NO_SEQ_FC", raising=False)
+    pc = pcfg(1, mc=m.config.max_context)
+    g.load_trace(t, pc)
+    a = g.run(pc)
+    monkeypatch.setenv("SIMNET_NO_SEQ_FC", "1")
+    b = g.run(pc)
+    assert np.array_equal(gpu_subs(a), gpu_subs(b)) and np.array_equal(a.predicted_fetch, b.predicted_fetch)
