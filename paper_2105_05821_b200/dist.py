@@ -57,15 +57,19 @@ def _device(device):
     return device
 
 
-def all_reduce_totals(t: Totals, device=None) -> Totals:
-    """Sum the shard totals over all ranks (exact: integer sums)."""
+def all_reduce_totals(t: Totals, device=None, failed: bool = False, with_failures: bool = False):
+    """Sum the shard totals over all ranks (exact: integer sums).  With
+    ``with_failures`` the same collective also counts the ranks that report
+    ``failed``, and ``(Totals, n_failed)`` is returned."""
     import torch
     import torch.distributed as dist
 
-    v = torch.tensor(t.as_list(), dtype=torch.int64, device=_device(device))
+    v = torch.tensor(t.as_list() + [1 if failed else 0], dtype=torch.int64, device=_device(device))
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
-    return Totals(*[int(x) for x in v.tolist()])
+    vals = [int(x) for x in v.tolist()]
+    tot = Totals(*vals[:-1])
+    return (tot, vals[-1]) if with_failures else tot
 
 
 def max_over_ranks(x: float, device=None) -> float:
@@ -87,13 +91,22 @@ def simulate_sharded(sim, trace, pc, rank: int, world: int, *, oracle: bool = Fa
     this rank's instructions.  A rank with no sub-traces (world > k) still
     joins the one collective with zero totals, so no rank is left waiting."""
     from .api import GpuSimulator, ParallelResult
+    from .errors import IlsimError
 
     n = trace.n if n_total is None else n_total
     k = GpuSimulator._num_sub(pc, n, False)
     shard = shard_range(k, rank, world)
-    if shard[0] == shard[1]:
-        res = ParallelResult([], 0, 0, 0.0, None)
-    else:
-        res = sim.simulate_parallel(trace, pc, oracle=oracle, shard=shard, n_total=n_total, base=base,
-                                    fetch_out=fetch_out)
-    return res, all_reduce_totals(Totals.of(res.sub_results), device="cuda")
+    res, err = ParallelResult([], 0, 0, 0.0, None), None
+    if shard[0] != shard[1]:
+        try:
+            res = sim.simulate_parallel(trace, pc, oracle=oracle, shard=shard, n_total=n_total, base=base,
+                                        fetch_out=fetch_out)
+        except Exception as e:  # still join the collective: no rank is left waiting in it
+            err = e
+    tot, n_failed = all_reduce_totals(Totals.of(res.sub_results), device="cuda", failed=err is not None,
+                                      with_failures=True)
+    if err is not None:
+        raise err
+    if n_failed:
+        raise IlsimError(f"the simulation failed on {n_failed} other rank(s)")
+    return res, tot

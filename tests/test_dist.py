@@ -137,3 +137,46 @@ def test_gloo_gpu_shards_match_single_process(world, k, precision):
     assert pf == full.predicted_fetch.tolist()
     for _, _, _, tot in out:
         assert tot[0] == full.total_cycles and tot[1] == t.n
+
+
+def _failing_worker(rank, world, port, q):
+    """Rank 1's shard simulation raises; every rank must raise, none may hang
+    in the collective."""
+    import torch.distributed as dist
+
+    from paper_2105_05821_b200 import IlsimError, ParallelConfig
+    from paper_2105_05821_b200.api import ParallelResult
+    from paper_2105_05821_b200.dist import simulate_sharded
+    from helpers import random_trace
+
+    class FakeSim:
+        def simulate_parallel(self, trace, pc, **kw):
+            if rank == 1:
+                raise IlsimError("device error on rank 1")
+            return ParallelResult([], 0, 0, 0.0, None)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            simulate_sharded(FakeSim(), random_trace(3, 400), ParallelConfig(k=4), rank, world)
+            q.put((rank, "no error"))
+        except IlsimError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_rank_failure_reaches_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_failing_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[1] == "device error on rank 1"
+    assert out[0] == "the simulation failed on 1 other rank(s)"
