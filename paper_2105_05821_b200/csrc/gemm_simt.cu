@@ -13,7 +13,6 @@ constexpr int BM = 64, BN = 64, BK = 16;
 __global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN];
-  __shared__ float Ps[BK][BN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const uint64_t row0 = static_cast<uint64_t>(blockIdx.x) * BM;
@@ -31,56 +30,50 @@ __global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
   // B-tile loader: k (tid / 16), n chunk (tid % 16) * 4
   const int bk = tid >> 4, bn = (tid & 15) * 4;
 
+  // Residual layers (cnn.cpp:104-107; oracle/cnn_restated.cpp): the W chain,
+  // then the P chain continuing on the same accumulator (the reference adds
+  // P * in into the W product before the bias), i.e. two passes over K.
   float acc[4][4] = {};
-  float acp[4][4] = {};
   float tot[4][4] = {};  // sum of the finished kSgemmChunk chunks (see gemm.cuh)
-  float tpp[4][4] = {};
-  for (int k0 = 0; k0 < g.kdim; k0 += BK) {
-    if (g.chunk > 0 && k0 > 0 && k0 % g.chunk == 0) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          tot[i][j] += acc[i][j];
-          tpp[i][j] += acp[i][j];
-          acc[i][j] = 0.0f;
-          acp[i][j] = 0.0f;
-        }
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int k = k0 + lk + t;
-      As[lk + t][lr] = (arow && k < g.kdim) ? arow[k] : 0.0f;
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int k = k0 + bk, n = col0 + bn + t;
-      const bool ok = k < g.kdim && n < g.n;
-      Bs[bk][bn + t] = ok ? g.w[static_cast<uint64_t>(k) * g.n + n] : 0.0f;
-      if (g.w2) Ps[bk][bn + t] = ok ? g.w2[static_cast<uint64_t>(k) * g.n + n] : 0.0f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-      if (g.w2) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Ps[kk][tx + 16 * j];
+  const int passes = g.w2 ? 2 : 1;
+  for (int pass = 0; pass < passes; ++pass) {
+    const float* wsrc = pass == 0 ? g.w : g.w2;
+    for (int k0 = 0; k0 < g.kdim; k0 += BK) {
+      if (g.chunk > 0 && (pass > 0 || k0 > 0) && k0 % g.chunk == 0) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acp[i][j] = fmaf(a[i], b[j], acp[i][j]);
+          for (int j = 0; j < 4; ++j) {
+            tot[i][j] += acc[i][j];
+            acc[i][j] = 0.0f;
+          }
       }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int k = k0 + lk + t;
+        As[lk + t][lr] = (arow && k < g.kdim) ? arow[k] : 0.0f;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int k = k0 + bk, n = col0 + bn + t;
+        const bool ok = k < g.kdim && n < g.n;
+        Bs[bk][bn + t] = ok ? wsrc[static_cast<uint64_t>(k) * g.n + n] : 0.0f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -91,7 +84,6 @@ __global__ void __launch_bounds__(256) sgemm_kernel(LayerGemm g) {
       const int n = col0 + tx + 16 * j;
       if (n >= g.n) continue;
       float v = tot[i][j] + acc[i][j];
-      if (g.w2) v += tpp[i][j] + acp[i][j];
       v += g.bias[n];
       if (g.relu) v = fmaxf(v, 0.0f);
       g.c[r * g.ldc + n] = v;

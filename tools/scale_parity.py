@@ -55,6 +55,9 @@ WORKLOADS = {
     # the same workloads with the trained C3 (tests/golden/c3_trained.model, tests/golden/train_c3.py)
     "c2t": dict(n=10_000_000, k=1024, kind="mix", regime="trained", seed=101),
     "c4t": dict(n=2_000_000, k=1024, kind="memory", regime="trained", seed=101),
+    "c3st": dict(n=C3_SHARD_N, k=8192, kind="mix", regime="trained", seed=101),
+    # the paper-scale residual model (7 x 384-channel residual conv blocks, 84 MFLOPs per instruction)
+    "rb7": dict(n=200_000, k=1024, kind="mix", regime="default", seed=101, config="rb7"),
 }
 TRAINED_MODEL = ROOT / "tests" / "golden" / "c3_trained.model"
 
@@ -70,8 +73,11 @@ def build_workload(name: str, init_params=None):
 
         model = read_model(TRAINED_MODEL)
     else:
+        from paper_2105_05821_b200.formats import CnnConfig
+
+        cfg = CnnConfig.preset_rb7() if w.get("config") == "rb7" else None
         model = synthetic_model(synthetic_trace(200_000, seed=101, kind=w["kind"]), seed=1, regime=w["regime"],
-                                init_params=init_params)
+                                init_params=init_params, config=cfg)
     return trace, model, w
 
 
