@@ -770,7 +770,8 @@ def test_rb7_teacher_forced_and_free_running(gpu, port, golden, precision, rtol)
 @pytest.mark.parametrize("name,precision,exact,min_blocks", [
     ("c4", "fp32", True, 1.0), ("c2", "tf32x3", False, 0.99), ("c4", "tf32x3", False, 0.99),
     ("c2t", "fp32", True, 1.0), ("c2t", "tf32x3", False, 0.98), ("c4t", "fp32", True, 1.0),
-    ("c4t", "tf32x3", False, 0.98), ("c3st", "fp32", True, 1.0)])
+    ("c4t", "tf32x3", False, 0.98), ("c3st", "fp32", True, 1.0), ("rb7", "fp32", True, 1.0),
+    ("rb7", "tf32x3", False, 0.99)])
 def test_scale_parity_against_reference_fixture(gpu, name, precision, exact, min_blocks):
     """The reference's simulate_parallel (oracle/_ref) was run once on the exact
     bench workloads (tools/scale_parity.py, tests/golden/scale/; c2t: the c2
