@@ -78,6 +78,8 @@ struct TcGemmParams {
   int tma_multi;              // f32 split-K partials through tmOut for CTAs that loop over M tiles: two
                               // 16 KB staging buffers past the A ring, one 32-column group at a time
   int stg_bufs;               // tma_multi staging buffers (2, or 1 to make room for a deeper A ring)
+  int stream_w;               // weights streamed through the ring with A (chunk by chunk, all of K in
+                              // one CTA): no resident slice, no split-K planes (large-M conv layers)
 };
 
 template <int kMode, bool kAInTmem = false>
@@ -89,13 +91,17 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   constexpr bool kSplit = kMode == kTF32x3;
   uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
   const uint32_t bBytes = static_cast<uint32_t>(p.n) * 128;
-  uint8_t* sW = base;                                      // [chunks][n x 128 B]
-  uint8_t* sWlo = sW + p.chunks * bBytes;                  // tf32x3 only
-  uint8_t* sA = sWlo + (kSplit ? p.chunks * bBytes : 0);   // [stages][16 KB]
+  const bool sw = p.stream_w != 0;
+  uint8_t* sW = base;                                      // [chunks][n x 128 B] (resident slice)
+  uint8_t* sWlo = sW + (sw ? 0 : p.chunks * bBytes);       // tf32x3 only
+  uint8_t* sA = sWlo + (kSplit && !sw ? p.chunks * bBytes : 0);  // [stages][16 KB]
   const int ns = p.stages > 0 ? p.stages : kStages;       // A ring depth
   uint8_t* sAlo = sA + ns * kAChunk;                       // tf32x3 only
   // tma_multi: 2 x 16 KB epilogue staging past the A ring (and its lo plane)
   uint8_t* sStg = sAlo + (kSplit && !kAInTmem ? ns * kAChunk : 0);
+  // stream_w: the weight chunks ride in the ring, [stages][n x 128 B] (+ lo)
+  uint8_t* sWr = sStg;
+  uint8_t* sWrlo = sWr + ns * bBytes;
 
   __shared__ __align__(8) uint64_t bar_w;
   __shared__ __align__(8) uint64_t bar_full[kMaxStages], bar_split[kMaxStages], bar_empty[kMaxStages];
@@ -272,7 +278,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {
       // resident weights for this CTA's (N tile, K split)
-      if (p.diag_skip_w) {
+      if (p.diag_skip_w || sw) {
         mbar_arrive(&bar_w);
       } else {
         mbar_expect_tx(&bar_w, p.chunks * bBytes * (kSplit ? 2u : 1u));
@@ -288,12 +294,16 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
         for (int c = 0; c < p.chunks; ++c) {
           mbar_wait(a_tmem ? &bar_sfree[stage] : &bar_empty[stage], phase ^ 1);
-          mbar_expect_tx(&bar_full[stage], kAChunk);
+          mbar_expect_tx(&bar_full[stage], kAChunk + (sw ? bBytes * (kSplit ? 2u : 1u) : 0u));
           const int kx = (kc0 + c) * elems;
           if (p.a3d)
             tma_load_3d(sA + stage * kAChunk, &tmA, &bar_full[stage], kx, 0, t * p.a_samples_box);
           else
             tma_load_2d(sA + stage * kAChunk, &tmA, &bar_full[stage], kx, t * kBM);
+          if (sw) {  // this chunk's weights with it (released with the stage)
+            tma_load_2d(sWr + stage * bBytes, &tmB, &bar_full[stage], kx, ntile * p.n);
+            if (kSplit) tma_load_2d(sWrlo + stage * bBytes, &tmBlo, &bar_full[stage], kx, ntile * p.n);
+          }
           if (++stage == ns) {
             stage = 0;
             phase ^= 1;
@@ -335,13 +345,14 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mma_commit(&bar_tfree[g & 3u]);  // the TMEM slot is free once these MMAs retire
           }
           for (int j = 0; j < steps && !a_tmem; ++j) {
-            const uint32_t aoff = stage * kAChunk + j * 32, boff = c * bBytes + j * 32;
+            const uint32_t aoff = stage * kAChunk + j * 32;
+            const uint32_t boff = (sw ? stage : c) * bBytes + j * 32;
             const uint64_t ad = smem_desc_sw128(su32(sA) + aoff);
-            const uint64_t bd = smem_desc_sw128(su32(sW) + boff);
+            const uint64_t bd = smem_desc_sw128(su32(sw ? sWr : sW) + boff);
             const uint32_t first = (c == 0 && j == 0) ? 0u : 1u;
             if (kSplit) {
               mma<kMode>(d, smem_desc_sw128(su32(sAlo) + aoff), bd, idesc, first);  // small terms first
-              mma<kMode>(d, ad, smem_desc_sw128(su32(sWlo) + boff), idesc, 1);
+              mma<kMode>(d, ad, smem_desc_sw128(su32(sw ? sWrlo : sWlo) + boff), idesc, 1);
               mma<kMode>(d, ad, bd, idesc, 1);
             } else {
               mma<kMode>(d, ad, bd, idesc, first);
@@ -742,10 +753,12 @@ void upload_weights(TcWeights& w, const float* src, int n, int k, int mode, int 
 }
 
 size_t smem_bytes(int mode, int n, int chunks, int stages, bool a_tmem = false, bool tma_multi = false,
-                  int stg_bufs = 2) {
-  const size_t w = static_cast<size_t>(chunks) * n * 128 * (mode == kTF32x3 ? 2 : 1);
-  const size_t a =
-      static_cast<size_t>(stages > 0 ? stages : kStages) * kAChunk * (mode == kTF32x3 && !a_tmem ? 2 : 1);
+                  int stg_bufs = 2, bool stream_w = false) {
+  const size_t ns = static_cast<size_t>(stages > 0 ? stages : kStages);
+  const size_t planes = mode == kTF32x3 ? 2 : 1;
+  // resident slice, or (stream_w) one weight chunk per ring stage
+  const size_t w = stream_w ? ns * n * 128 * planes : static_cast<size_t>(chunks) * n * 128 * planes;
+  const size_t a = ns * kAChunk * (mode == kTF32x3 && !a_tmem ? 2 : 1);
   return w + a + (tma_multi ? static_cast<size_t>(stg_bufs) * kAChunk : 0) + 1024;
 }
 
@@ -795,7 +808,8 @@ void launch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const CUt
   int gx = std::max(1, std::min(p.m_tiles, std::max(1, g_num_sms / groups)));
   if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(ny), static_cast<unsigned>(nz));
-  const size_t sm = smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0, p.stg_bufs);
+  const size_t sm =
+      smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, p.tma_multi != 0, p.stg_bufs, p.stream_w != 0);
   if (mode == kFP8)
     launch_pdl_tag("layer_bf16", tc_layer_kernel<kFP8>, grid, dim3(kLayerThreads), sm, s, a, b, blo, out, p);
   else if (mode == kBF16)
@@ -1161,11 +1175,26 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
     // over grid z, f32 partial planes, then a fixed-order reduce + bias + ReLU.
     // K past the tensor (the last split's tail) is TMA zero fill: exact zeros.
     const int total_chunks = (k * esz + 127) / 128;
-    const int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
-    p.chunks = nsplit > 1 ? kMaxChunks : total_chunks;
-    p.ksteps_last = nsplit > 1 ? 4 : ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
+    int nsplit = (total_chunks + kMaxChunks - 1) / kMaxChunks;
+    // Layers with tens of thousands of rows (paper-scale models at K >= ~1k
+    // sub-traces): stream the weight chunks through the ring with A instead of
+    // splitting K -- one CTA per output tile accumulates all of K in TMEM, so
+    // no partial planes go through HBM and no reduce kernel runs
+    // (SIMNET_NO_STREAM_W: split-K, A/B)
+    const bool stream = nsplit > 1 && p.m_tiles >= 64 && std::getenv("SIMNET_NO_STREAM_W") == nullptr;
+    if (stream) {
+      nsplit = 1;
+      p.stream_w = 1;
+      p.chunks = total_chunks;
+      p.ksteps_last = ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
+    } else {
+      p.chunks = nsplit > 1 ? kMaxChunks : total_chunks;
+      p.ksteps_last = nsplit > 1 ? 4 : ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
+    }
     p.stages = kStages;
-    while (p.stages > 2 && smem_bytes(mode, p.n, p.chunks, p.stages) > 226 * 1024) --p.stages;
+    while (p.stages > 2 &&
+           smem_bytes(mode, p.n, p.chunks, p.stages, false, false, 2, p.stream_w != 0) > 226 * 1024)
+      --p.stages;
     p.ldo = cout;
     const uint64_t plane = m_rows * static_cast<uint64_t>(cout);
     if (nsplit == 1) {
