@@ -312,9 +312,13 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // MMA issuer: the whole warp runs the loop (warp-uniform operands) and the
+    // *_w forms elect the issuing thread inside the asm (tc_common.cuh)
+    const bool t0 = tr && lane == 0;
+    {
       mbar_wait(&bar_w, 0);
-      if (tr) tr[1] = clock64();
+      __syncwarp();
+      if (t0) tr[1] = clock64();
       const uint32_t idesc = instr_desc(mode_fmt(kMode), p.n);
       int stage = 0;
       uint32_t phase = 0;
@@ -324,11 +328,13 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&bar_acc_empty[acc], acc_phase ^ 1);
+        __syncwarp();
         tc_fence_after();
         const uint32_t d = tmem + acc * p.n;
         for (int c = 0; c < p.chunks; ++c) {
           mbar_wait(kSplit ? &bar_split[stage] : &bar_full[stage], phase);
-          if (tr && it == 0 && c < 4) tr[c == 0 ? 2 : 4 + c] = clock64();  // chunk c ready (5, 6, 7: chunks 1-3)
+          __syncwarp();
+          if (t0 && it == 0 && c < 4) tr[c == 0 ? 2 : 4 + c] = clock64();  // chunk c ready (5, 6, 7: chunks 1-3)
           tc_fence_after();
           const int steps = c == p.chunks - 1 ? p.ksteps_last : 4;
           const long long t_issue = tr ? clock64() : 0;
@@ -338,11 +344,11 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               const uint32_t boff = c * bBytes + j * 32;
               const uint64_t bd = smem_desc_sw128(su32(sW) + boff);
               const uint32_t first = (c == 0 && j == 0) ? 0u : 1u;
-              mma_ts<kMode>(d, slot + 32 + j * 8, bd, idesc, first);  // small terms first
-              mma_ts<kMode>(d, slot + j * 8, smem_desc_sw128(su32(sWlo) + boff), idesc, 1);
-              mma_ts<kMode>(d, slot + j * 8, bd, idesc, 1);
+              mma_ts_w<kMode>(d, slot + 32 + j * 8, bd, idesc, first);  // small terms first
+              mma_ts_w<kMode>(d, slot + j * 8, smem_desc_sw128(su32(sWlo) + boff), idesc, 1);
+              mma_ts_w<kMode>(d, slot + j * 8, bd, idesc, 1);
             }
-            mma_commit(&bar_tfree[g & 3u]);  // the TMEM slot is free once these MMAs retire
+            mma_commit_w(&bar_tfree[g & 3u]);  // the TMEM slot is free once these MMAs retire
           }
           for (int j = 0; j < steps && !a_tmem; ++j) {
             const uint32_t aoff = stage * kAChunk + j * 32;
@@ -351,24 +357,24 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const uint64_t bd = smem_desc_sw128(su32(sw ? sWr : sW) + boff);
             const uint32_t first = (c == 0 && j == 0) ? 0u : 1u;
             if (kSplit) {
-              mma<kMode>(d, smem_desc_sw128(su32(sAlo) + aoff), bd, idesc, first);  // small terms first
-              mma<kMode>(d, ad, smem_desc_sw128(su32(sw ? sWrlo : sWlo) + boff), idesc, 1);
-              mma<kMode>(d, ad, bd, idesc, 1);
+              mma_w<kMode>(d, smem_desc_sw128(su32(sAlo) + aoff), bd, idesc, first);  // small terms first
+              mma_w<kMode>(d, ad, smem_desc_sw128(su32(sw ? sWrlo : sWlo) + boff), idesc, 1);
+              mma_w<kMode>(d, ad, bd, idesc, 1);
             } else {
-              mma<kMode>(d, ad, bd, idesc, first);
+              mma_w<kMode>(d, ad, bd, idesc, first);
             }
           }
-          if (!a_tmem) mma_commit(&bar_empty[stage]);  // the stage is free once these MMAs retire
+          if (!a_tmem) mma_commit_w(&bar_empty[stage]);  // the stage is free once these MMAs retire
           ++g;
-          if (tr && it == 0) tr[15] += clock64() - t_issue;  // diagnostics: cycles spent issuing
+          if (t0 && it == 0) tr[15] += clock64() - t_issue;  // diagnostics: cycles spent issuing
           if (++stage == ns) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&bar_acc_full[acc]);
-        if (tr && it < 1) tr[3] = clock64();
-        if (tr && it < 8) tr[21 + it] = clock64();  // diagnostics: tile it's MMAs all issued
+        mma_commit_w(&bar_acc_full[acc]);
+        if (t0 && it < 1) tr[3] = clock64();
+        if (t0 && it < 8) tr[21 + it] = clock64();  // diagnostics: tile it's MMAs all issued
       }
     }
     __syncwarp();

@@ -138,6 +138,39 @@ __device__ __forceinline__ void mma_ts(uint32_t tmem, uint32_t a_tmem, uint64_t 
         "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc));
   }
 }
+// Warp-issued forms: the whole warp executes the call (warp-uniform operands)
+// and elect.sync inside the asm picks the one issuing thread.  Issued from a
+// single thread under `if (lane == 0)`, ptxas wraps every UTCHMMA in a
+// waterfall loop (ELECT / BRA.U.ANY) plus R2UR moves; measured
+// (tools/probes/tc_peak.py, M = 128 tf32): N = 64 102 -> 48, N = 128 107 -> 64,
+// N = 256 171 -> 128 cycles per MMA in a loop with a run-time branch.
+#define SIMNET_MMA_W(KIND, AOP, ACONS)                                                                   \
+  asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"     \
+               "@e tcgen05.mma.cta_group::1.kind::" KIND " [%0], " AOP ", %2, %3, p;\n\t}" ::"r"(tmem), \
+               ACONS(a), "l"(bd), "r"(idesc), "r"(acc))
+template <int kMode>
+__device__ __forceinline__ void mma_w(uint32_t tmem, uint64_t a, uint64_t bd, uint32_t idesc, uint32_t acc) {
+#define SIMNET_L(x) "l"(x)
+  if constexpr (kMode == kFP8) SIMNET_MMA_W("f8f6f4", "%1", SIMNET_L);
+  else if constexpr (kMode == kBF16) SIMNET_MMA_W("f16", "%1", SIMNET_L);
+  else SIMNET_MMA_W("tf32", "%1", SIMNET_L);
+#undef SIMNET_L
+}
+template <int kMode>
+__device__ __forceinline__ void mma_ts_w(uint32_t tmem, uint32_t a, uint64_t bd, uint32_t idesc, uint32_t acc) {
+#define SIMNET_R(x) "r"(x)
+  if constexpr (kMode == kBF16) SIMNET_MMA_W("f16", "[%1]", SIMNET_R);
+  else SIMNET_MMA_W("tf32", "[%1]", SIMNET_R);
+#undef SIMNET_R
+}
+#undef SIMNET_MMA_W
+// tcgen05.commit by one elected thread of a converged warp (one arrival)
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(bar))
+      : "memory");
+}
 // 32 consecutive 32-bit columns of this thread's TMEM lane (warp lane quarter).
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
   asm volatile(

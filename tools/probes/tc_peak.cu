@@ -56,7 +56,7 @@ __device__ __forceinline__ void teardown(uint32_t tmem) {
 }
 
 template <int kMode>
-__global__ void mma_loop(int n, int count, int nacc, long long* out) {
+__global__ void mma_loop(int n, int count, int nacc, long long* out, int a_tmem = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t bar;
@@ -71,7 +71,10 @@ __global__ void mma_loop(int n, int count, int nacc, long long* out) {
     long long t0 = clock64();
     for (int i = 0; i < count; ++i) {
       const uint32_t d = tmem + (i & (nacc - 1)) * stride;  // nacc: 1, 2 or 4
-      mma<kMode>(d, ad + ((i & 3) * 2), bd, idesc, i >= nacc);
+      if (a_tmem)  // A from tensor memory (columns 384+, left as allocated)
+        mma_ts<kMode>(d, tmem + 384 + (i & 3) * 8, bd, idesc, i >= nacc);
+      else
+        mma<kMode>(d, ad + ((i & 3) * 2), bd, idesc, i >= nacc);
     }
     long long t1 = clock64();
     mma_commit(&bar);
@@ -85,11 +88,66 @@ __global__ void mma_loop(int n, int count, int nacc, long long* out) {
   teardown(tmem);
 }
 
+// The same loop issued by a whole warp with elect.sync inside the asm (the
+// issuing thread chosen per instruction), instead of one thread under
+// `if (threadIdx.x == 0)`: ptxas then needs no per-MMA waterfall loop
+// (ELECT / BRA.U.ANY) around UTCHMMA.
+__device__ __forceinline__ void mma_tf32_elect(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__global__ void mma_loop_warp(int n, int count, int nacc, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  setup<kTF32>(base, &bar, &slot);
+  const uint32_t tmem = slot;
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = instr_desc(mode_fmt(kTF32), n);
+    const uint64_t ad = smem_desc_sw128(su32(base));
+    const uint64_t bd = smem_desc_sw128(su32(base + 32 * 1024));
+    const int stride = n <= 128 ? 128 : 256;
+    long long t0 = clock64();
+    for (int i = 0; i < count; ++i) {
+      const uint32_t d = tmem + (i & (nacc - 1)) * stride;
+      mma_tf32_elect(d, ad + ((i & 3) * 2), bd, idesc, i >= nacc);
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) {
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+    }
+    __syncwarp();
+    long long t2 = clock64();
+    if (out && blockIdx.x == 0 && threadIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  }
+  teardown(tmem);
+}
+extern "C" int issue_cost_warp(int n, int count, int nacc, long long* host) {
+  long long* d;
+  cudaMalloc(&d, 16 * sizeof(long long));
+  const size_t sm = 100 * 1024;
+  cudaFuncSetAttribute(mma_loop_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  mma_loop_warp<<<1, 128, sm>>>(n, count, nacc, d);
+  int e = cudaGetLastError();
+  if (!e) e = cudaDeviceSynchronize();
+  cudaMemcpy(host, d, 2 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
 template <int kMode>
-static int launch(int grid, int n, int count, int nacc, long long* d) {
+static int launch(int grid, int n, int count, int nacc, long long* d, int a_tmem = 0) {
   const size_t sm = 100 * 1024;
   cudaFuncSetAttribute(mma_loop<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  mma_loop<kMode><<<grid, 128, sm>>>(n, count, nacc, d);
+  mma_loop<kMode><<<grid, 128, sm>>>(n, count, nacc, d, a_tmem);
   return cudaGetLastError();
 }
 
@@ -104,6 +162,17 @@ extern "C" int issue_cost(int mode, int n, int count, int nacc, long long* host)
   long long* d;
   cudaMalloc(&d, 16 * sizeof(long long));
   int e = launch_mode(mode, 1, n, count, nacc, d);
+  if (!e) e = cudaDeviceSynchronize();
+  cudaMemcpy(host, d, 2 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
+// the same with A read from tensor memory (tcgen05.mma [d], [a_tmem], b_desc): FC1's form
+extern "C" int issue_cost_ts(int mode, int n, int count, int nacc, long long* host) {
+  long long* d;
+  cudaMalloc(&d, 16 * sizeof(long long));
+  int e = mode == kBF16 ? launch<kBF16>(1, n, count, nacc, d, 1) : launch<kTF32>(1, n, count, nacc, d, 1);
   if (!e) e = cudaDeviceSynchronize();
   cudaMemcpy(host, d, 2 * sizeof(long long), cudaMemcpyDeviceToHost);
   cudaFree(d);
