@@ -99,6 +99,14 @@ __device__ __forceinline__ void mma_tf32_elect(uint32_t tmem, uint64_t ad, uint6
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void mma_ts_tf32_elect(uint32_t tmem, uint32_t a, uint64_t bd, uint32_t idesc,
+                                                  uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+      "r"(a), "l"(bd), "r"(idesc), "r"(acc));
+}
+template <bool kTs>
 __global__ void mma_loop_warp(int n, int count, int nacc, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
@@ -114,7 +122,10 @@ __global__ void mma_loop_warp(int n, int count, int nacc, long long* out) {
     long long t0 = clock64();
     for (int i = 0; i < count; ++i) {
       const uint32_t d = tmem + (i & (nacc - 1)) * stride;
-      mma_tf32_elect(d, ad + ((i & 3) * 2), bd, idesc, i >= nacc);
+      if constexpr (kTs)
+        mma_ts_tf32_elect(d, tmem + 384 + (i & 3) * 8, bd, idesc, i >= nacc);
+      else
+        mma_tf32_elect(d, ad + ((i & 3) * 2), bd, idesc, i >= nacc);
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) {
@@ -130,12 +141,17 @@ __global__ void mma_loop_warp(int n, int count, int nacc, long long* out) {
   }
   teardown(tmem);
 }
-extern "C" int issue_cost_warp(int n, int count, int nacc, long long* host) {
+extern "C" int issue_cost_warp(int n, int count, int nacc, long long* host, int ts) {
   long long* d;
   cudaMalloc(&d, 16 * sizeof(long long));
   const size_t sm = 100 * 1024;
-  cudaFuncSetAttribute(mma_loop_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  mma_loop_warp<<<1, 128, sm>>>(n, count, nacc, d);
+  if (ts) {
+    cudaFuncSetAttribute(mma_loop_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    mma_loop_warp<true><<<1, 128, sm>>>(n, count, nacc, d);
+  } else {
+    cudaFuncSetAttribute(mma_loop_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    mma_loop_warp<false><<<1, 128, sm>>>(n, count, nacc, d);
+  }
   int e = cudaGetLastError();
   if (!e) e = cudaDeviceSynchronize();
   cudaMemcpy(host, d, 2 * sizeof(long long), cudaMemcpyDeviceToHost);

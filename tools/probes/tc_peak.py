@@ -23,7 +23,7 @@ if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
 L = C.CDLL(so)
 L.issue_cost.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
 L.issue_cost_ts.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
-L.issue_cost_warp.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+L.issue_cost_warp.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]
 L.dense_peak.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 MODES = {"tf32": 1, "bf16": 0, "fp8": 3}  # tc_common.cuh kTF32 / kBF16 / kFP8
 K = {"tf32": 8, "bf16": 16, "fp8": 32}
@@ -54,18 +54,19 @@ def main():
                 res["issue_cycles"][f"{name}_n{n}_acc{nacc}"] = per
                 print(f"{name:5s} M=128 N={n:3d} acc={nacc}: {per:6.1f} cycles/MMA "
                       f"({2 * 128 * n * K[name] / per / 1e3:6.2f} kFLOP/cycle/SM)", flush=True)
-    for n in (64, 128, 256):  # whole-warp issue loop, elect.sync inside the asm
-        for nacc in (1, 2):
+    for ts, n, nacc in [(ts, n, nacc) for ts in (0, 1) for n in (64, 128, 256) for nacc in (1, 2)]:
+        if True:  # whole-warp issue loop, elect.sync inside the asm; ts: A from tensor memory
             if n == 256 and nacc == 2:
                 continue
             r = []
             for count in ((64, 256) if a.short else (256, 1024)):
-                e = L.issue_cost_warp(n, count, nacc, out.ctypes.data)
+                e = L.issue_cost_warp(n, count, nacc, out.ctypes.data, ts)
                 assert e == 0, e
                 r.append((count, int(out[1])))
             per = (r[1][1] - r[0][1]) / (r[1][0] - r[0][0])
-            res["issue_cycles"][f"tf32_warp_n{n}_acc{nacc}"] = per
-            print(f"tf32  warp-elect M=128 N={n:3d} acc={nacc}: {per:6.1f} cycles/MMA", flush=True)
+            res["issue_cycles"][f"tf32_warp{'_ts' if ts else ''}_n{n}_acc{nacc}"] = per
+            print(f"tf32  warp-elect{' A-from-TMEM' if ts else ''} M=128 N={n:3d} acc={nacc}: {per:6.1f} cycles/MMA",
+                  flush=True)
     for name in ("tf32", "bf16"):  # A from tensor memory (FC1's form at c3)
         for n in (64, 128, 256):
             for nacc in (1, 2):
