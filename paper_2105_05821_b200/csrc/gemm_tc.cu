@@ -78,6 +78,8 @@ struct TcGemmParams {
   int tma_multi;              // f32 split-K partials through tmOut for CTAs that loop over M tiles: two
                               // 16 KB staging buffers past the A ring, one 32-column group at a time
   int stg_bufs;               // tma_multi staging buffers (2, or 1 to make room for a deeper A ring)
+  int diag_a_early;           // diagnostics (SIMNET_DIAG_FC1_A_EARLY, timing only: results are garbage):
+                              // A loads issued without the dependency wait
   int stream_w;               // weights streamed through the ring with A (chunk by chunk, all of K in
                               // one CTA): no resident slice, no split-K planes (large-M conv layers)
 };
@@ -287,7 +289,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (kSplit) tma_load_2d(sWlo + c * bBytes, &tmBlo, &bar_w, (kc0 + c) * elems, ntile * p.n);
         }
       }
-      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (!p.diag_a_early) asm volatile("griddepcontrol.wait;" ::: "memory");
       if (tr) tr[12] = global_ns();  // the previous kernel's results are visible
       int stage = 0;
       uint32_t phase = 0;
@@ -974,15 +976,19 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.chunks = per;
     p.ksteps_last = 4;
     // A ring depth that fits next to the resident W slice (226 KB dynamic smem)
-    // A in TMEM pays off when CTAs loop over several M tiles (the split runs a
-    // chunk ahead of the MMAs); with one tile per CTA the split sits on the
-    // critical path and A from shared memory is faster (measured at K = 1024 / 8192)
+    // 3xTF32: the split warps write A hi / lo into tensor memory and the MMAs
+    // read only W from shared memory. With A in shared memory an N = 128 MMA
+    // reads 8 KB per 64 cycles, all of the shared-memory bandwidth, and the
+    // split's stores compete with it. (With single-thread MMA issue A from
+    // shared memory was faster for CTAs with one M tile; with the warp-issued
+    // MMAs A in TMEM is faster there too: c2 27.75 -> 27.40 us per round,
+    // profiles/r02zo_fc1_tmem_a_c2.txt.)  SIMNET_FC1_SS: A from shared memory (A/B)
     const int groups = (t.fc1.npad / fc_tile) * nsplit;
     static const int fc1_gx = std::getenv("SIMNET_FC1_GX") ? std::atoi(std::getenv("SIMNET_FC1_GX")) : 0;
     p.gx_max = fc1_gx;
     int gx = std::max(1, std::min(p.m_tiles, std::max(1, num_sms() / groups)));
     if (p.gx_max > 0) gx = std::min(gx, p.gx_max);
-    p.a_tmem = mode == kTF32x3 && p.n <= 128 && p.m_tiles > gx && !std::getenv("SIMNET_FC1_SS");
+    p.a_tmem = mode == kTF32x3 && p.n <= 128 && !std::getenv("SIMNET_FC1_SS");
     // CTAs that loop over M tiles TMA-store their partial tiles through two
     // staging buffers when those fit next to a full A ring (SIMNET_FC1_MULTI_DIRECT: row stores, A/B)
     const bool multi_direct = std::getenv("SIMNET_FC1_MULTI_DIRECT") != nullptr;
@@ -1008,6 +1014,7 @@ uint64_t tc_fc(const DevModel& m, const void* in, uint64_t samples, const Forwar
     p.out_scale = t.fc1.inv_scale;
     p.trace = chain_trace_active();
     p.diag_skip_w = std::getenv("SIMNET_DIAG_FC1_SKIP_W") != nullptr;
+    p.diag_a_early = std::getenv("SIMNET_DIAG_FC1_A_EARLY") != nullptr;
     // a last plane with fewer chunks reads TMA zero fill past the flat dim (exact zeros)
     if (nsplit > kMaxSplit) throw ApiError("tensor-core path: flat dim too large for the FC tail");
     // partial planes as a 3-D tensor [nsplit][samples][hidden]: the TMA store

@@ -1,0 +1,3 @@
+PRECS=tf32x3 timeout 300 python tools/fc1_trace.py 2>&1 | head -12
+SIMNET_DIAG_FC1_A_EARLY=1 PRECS=tf32x3 timeout 300 python tools/fc1_trace.py 2>&1 | head -12
+SIMNET_DIAG_FC1_SKIP_W=1 PRECS=tf32x3 timeout 300 python tools/fc1_trace.py 2>&1 | head -12
