@@ -296,6 +296,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
         for (int c = 0; c < p.chunks; ++c) {
           mbar_wait(a_tmem ? &bar_sfree[stage] : &bar_empty[stage], phase ^ 1);
+          if (a_tmem && sw) mbar_wait(&bar_empty[stage], phase ^ 1);  // the stage's W chunk: MMAs done
           mbar_expect_tx(&bar_full[stage], kAChunk + (sw ? bBytes * (kSplit ? 2u : 1u) : 0u));
           const int kx = (kc0 + c) * elems;
           if (p.a3d)
@@ -343,11 +344,11 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if constexpr (a_tmem) {  // A hi / lo in TMEM slot g % 4 (columns: hi 32 | lo 32), W from SMEM
             const uint32_t slot = tmem + kATmem + (g & 3u) * 64u;
             for (int j = 0; j < steps; ++j) {
-              const uint32_t boff = c * bBytes + j * 32;
-              const uint64_t bd = smem_desc_sw128(su32(sW) + boff);
+              const uint32_t boff = (sw ? stage : c) * bBytes + j * 32;  // stream_w: the stage's W chunk
+              const uint64_t bd = smem_desc_sw128(su32(sw ? sWr : sW) + boff);
               const uint32_t first = (c == 0 && j == 0) ? 0u : 1u;
               mma_ts_w<kMode>(d, slot + 32 + j * 8, bd, idesc, first);  // small terms first
-              mma_ts_w<kMode>(d, slot + j * 8, smem_desc_sw128(su32(sWlo) + boff), idesc, 1);
+              mma_ts_w<kMode>(d, slot + j * 8, smem_desc_sw128(su32(sw ? sWrlo : sWlo) + boff), idesc, 1);
               mma_ts_w<kMode>(d, slot + j * 8, bd, idesc, 1);
             }
             mma_commit_w(&bar_tfree[g & 3u]);  // the TMEM slot is free once these MMAs retire
@@ -366,7 +367,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               mma_w<kMode>(d, ad, bd, idesc, first);
             }
           }
-          if (!a_tmem) mma_commit_w(&bar_empty[stage]);  // the stage is free once these MMAs retire
+          if (!a_tmem || sw) mma_commit_w(&bar_empty[stage]);  // the stage is free once these MMAs retire
           ++g;
           if (t0 && it == 0) tr[15] += clock64() - t_issue;  // diagnostics: cycles spent issuing
           if (++stage == ns) {
@@ -1205,8 +1206,11 @@ uint64_t tc_forward(const DevModel& m, int precision, const void* x, uint32_t x_
       p.ksteps_last = nsplit > 1 ? 4 : ((k * esz + 31) / 32) - 4 * (p.chunks - 1);
     }
     p.stages = kStages;
+    // 3xTF32: A hi / lo split into tensor memory, the MMAs read only W from
+    // shared memory (as FC1; SIMNET_LAYER_SS: A from shared memory, A/B)
+    p.a_tmem = mode == kTF32x3 && p.n <= 128 && !std::getenv("SIMNET_LAYER_SS");
     while (p.stages > 2 &&
-           smem_bytes(mode, p.n, p.chunks, p.stages, false, false, 2, p.stream_w != 0) > 226 * 1024)
+           smem_bytes(mode, p.n, p.chunks, p.stages, p.a_tmem != 0, false, 2, p.stream_w != 0) > 226 * 1024)
       --p.stages;
     p.ldo = cout;
     const uint64_t plane = m_rows * static_cast<uint64_t>(cout);
