@@ -14,6 +14,7 @@ Errors raise :class:`IlsimError` with the reference's messages.
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -66,6 +67,46 @@ class SimResult:
     overflow_stall_cycles: int = 0
     empty: bool = False
     predicted_fetch: np.ndarray | None = None
+
+
+class SubResults(Sequence):
+    """``ParallelResult::sub_results``: a sequence of ``SimResult`` over the
+    C-ABI's ``ilsim_sub_result`` array, each built on first access (and kept,
+    so edits stick). Building 65,536 Python objects up front cost ~0.2 s of a
+    2 s c3 call; ``array`` is the raw structured array for vectorised use."""
+
+    def __init__(self, array: np.ndarray, pf: np.ndarray | None):
+        self.array = array
+        self._pf = pf
+        self._off = None
+        self._cache: dict[int, SimResult] = {}
+
+    def __len__(self) -> int:
+        return len(self.array)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        i = int(i)
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        r = self._cache.get(i)
+        if r is None:
+            s = self.array[i]
+            r = SimResult(int(s["total_cycles"]), int(s["instructions"]), 0.0, int(s["sum_fetch"]), int(s["delta"]),
+                          int(s["drain_cycles"]), int(s["overflow_stall_cycles"]), bool(s["empty"]))
+            r.cpi = 0.0 if r.instructions == 0 else r.total_cycles / r.instructions
+            if self._pf is not None:
+                if self._off is None:  # the sub-traces' fetch series are consecutive in trace order
+                    self._off = np.concatenate(([0], np.cumsum(self.array["instructions"], dtype=np.uint64)))
+                r.predicted_fetch = self._pf[int(self._off[i]):int(self._off[i + 1])]
+            self._cache[i] = r
+        return r
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, Sequence) and len(self) == len(other) and all(a == b for a, b in zip(self, other))
 
 
 @dataclass
@@ -338,20 +379,11 @@ class GpuSimulator:
 
     @staticmethod
     def _collect(subs, nsub, pf, owned, tot, starts, sb, pc) -> ParallelResult:
-        out = []
-        off = 0
-        for j in range(nsub):
-            s = subs[j]
-            r = SimResult(int(s.total_cycles), int(s.instructions), 0.0, int(s.sum_fetch), int(s.delta),
-                          int(s.drain_cycles), int(s.overflow_stall_cycles), bool(s.empty))
-            r.cpi = 0.0 if r.instructions == 0 else r.total_cycles / r.instructions
-            if pf is not None:
-                r.predicted_fetch = pf[off:off + r.instructions]
-                off += r.instructions
-            out.append(r)
-        total = sum(r.total_cycles for r in out)
-        n = sum(r.instructions for r in out)
-        return ParallelResult(out, total, n, total / n if n else 0.0, pf[:owned] if pf is not None else None,
+        arr = np.ctypeslib.as_array(subs)[:nsub].copy()  # structured view of ilsim_sub_result[nsub]
+        total = int(arr["total_cycles"].sum())
+        n = int(arr["instructions"].sum())
+        return ParallelResult(SubResults(arr, pf), total, n, total / n if n else 0.0,
+                              pf[:owned] if pf is not None else None,
                               float(tot.device_ms), tuple(tot.kernel_ms), int(tot.launches), int(tot.rounds))
 
     def simulate_parallel(self, trace: Trace, pc: ParallelConfig | None = None, *, oracle=False,

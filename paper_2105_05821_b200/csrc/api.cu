@@ -245,6 +245,8 @@ void run_impl(ilsim_gpu_ctx* c, const ilsim_sim_config& cfg, ilsim_sub_result* s
   uint32_t win_rounds = 0, n_win = 0;
   if (c->deferred) {
     win_rounds = std::max<uint32_t>(16, ((rounds + 15) / 16 + 15) / 16 * 16);
+    if (const char* e = std::getenv("SIMNET_WIN_ROUNDS"))  // A/B: window size in rounds
+      win_rounds = std::max<uint32_t>(16, static_cast<uint32_t>(std::atoi(e)) / 16 * 16);
     n_win = (rounds + win_rounds - 1) / win_rounds;
     struct Group { uint64_t first_begin, stride, count; uint32_t len; };
     std::vector<Group> groups;

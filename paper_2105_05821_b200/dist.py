@@ -35,6 +35,10 @@ class Totals:
     @staticmethod
     def of(subs) -> "Totals":
         t = Totals()
+        if hasattr(subs, "array"):  # api.SubResults: sum the columns
+            for f in TOTAL_FIELDS:
+                setattr(t, f, int(subs.array[f].sum()))
+            return t
         for s in subs:
             for f in TOTAL_FIELDS:
                 setattr(t, f, getattr(t, f) + int(getattr(s, f) if not isinstance(s, dict) else s[f]))

@@ -1,6 +1,6 @@
 # diagnostics: where the e2e time goes (load_trace = H2D + pack; run = capture + rounds + D2H)
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, ".")
 import torch
 from paper_2105_05821_b200 import GpuSimulator, ParallelConfig, SimConfig
 from paper_2105_05821_b200.synth import synthetic_model, synthetic_trace
