@@ -128,14 +128,19 @@ def _err(buf) -> str:
     return buf.value.decode(errors="replace")
 
 
-def partition_starts(n: int, k: int) -> list[int]:
-    """``partition(n, k).starts`` (parallel.cpp:9-24)."""
+def _partition_array(n: int, k: int) -> np.ndarray:
+    """``partition(n, k).starts`` as a uint64 array (no per-sub-trace Python ints)."""
     L = _lib.lib()
     starts = np.zeros(max(k, 1), dtype=np.uint64)
     err = C.create_string_buffer(_ERRLEN)
     if L.ilsim_gpu_partition(n, k, starts.ctypes.data, err, _ERRLEN) != 0:
         raise IlsimError(_err(err))
-    return [int(s) for s in starts[:k]]
+    return starts[:k]
+
+
+def partition_starts(n: int, k: int) -> list[int]:
+    """``partition(n, k).starts`` (parallel.cpp:9-24)."""
+    return [int(s) for s in _partition_array(n, k)]
 
 
 def _cnn_cfg(c: CnnConfig) -> _lib.CnnCfg:
@@ -342,9 +347,9 @@ class GpuSimulator:
             sb, se = 0, k
         nsub = max(se - sb, 1)
         subs = (_lib.SubResult * nsub)()
-        starts = partition_starts(n, k) if n > 0 else [0]
-        own0 = starts[sb] if n > 0 else 0
-        own1 = (starts[se] if se < k else n) if n > 0 else 0
+        starts = _partition_array(n, k) if n > 0 else [0]
+        own0 = int(starts[sb]) if n > 0 else 0
+        own1 = (int(starts[se]) if se < k else n) if n > 0 else 0
         if not pc.sim.record_fetch:
             pf = None
         elif fetch_out is not None:
@@ -484,7 +489,7 @@ class GpuGroup:
                                                              pf.ctypes.data if pf is not None else None,
                                                              C.byref(tot)))
         del keep
-        starts = partition_starts(n, k) if n > 0 else [0]
+        starts = _partition_array(n, k) if n > 0 else [0]
         return GpuSimulator._collect(subs, int(tot.sub_traces), pf, n, tot, starts, 0, pc)
 
 
