@@ -389,9 +389,11 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       int stage = 0;
       uint32_t phase = 0;
       uint32_t g = 0;
+      const bool st0 = tr && threadIdx.x == 64;  // diagnostics: split of chunks 0 / 1 (first tile)
       for (int t = blockIdx.x; t < p.m_tiles; t += gridDim.x) {
         for (int c = 0; c < p.chunks; ++c, ++g) {
           mbar_wait(&bar_full[stage], phase);
+          if (st0 && g < 2) tr[g == 0 ? 11 : 30] = clock64();  // chunk 0 / 1 landed
           if (g >= 4) mbar_wait(&bar_tfree[g & 3u], ((g >> 2) - 1) & 1u);  // chunk g-4's MMAs done
           tc_fence_after();
           const uint8_t* row = sA + stage * kAChunk + r * 128;
@@ -414,6 +416,7 @@ tc_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           tc_fence_before();
           mbar_arrive(&bar_sfree[stage]);  // SMEM stage read
           mbar_arrive(&bar_split[stage]);  // TMEM slot written
+          if (st0 && g < 2) tr[g == 0 ? 29 : 31] = clock64();  // chunk 0 / 1 split into TMEM
           if (++stage == ns) {
             stage = 0;
             phase ^= 1;

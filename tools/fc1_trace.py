@@ -23,7 +23,8 @@ for prec in os.environ.get("PRECS", "tf32x3,bf16").split(","):
     _lib.lib().simnet_debug_chain_trace_full(C.c_void_p(buf.ctypes.data), C.c_int(buf.size))
     tr = buf[148 * 32:].reshape(256, 32)[:128].astype(np.float64)
     rel = tr - tr[:, :1]
-    names = {0: "start", 1: "W landed", 2: "A chunk0 ready", 5: "A chunk1 ready", 6: "A chunk2 ready",
+    names = {0: "start", 1: "W landed", 11: "split: chunk0 landed", 29: "split: chunk0 in TMEM", 30: "split: chunk1 landed",
+             31: "split: chunk1 in TMEM", 2: "A chunk0 ready", 5: "A chunk1 ready", 6: "A chunk2 ready",
              7: "A chunk3 ready", 3: "tile0 MMAs issued", 14: "accumulator done", 16: "epi: tmem ld", 17: "epi: staged",
              18: "epi: fenced", 19: "epi: TMA issued", 20: "epi: staging read", 4: "tile0 epilogue done"}
     print(prec)
