@@ -220,3 +220,36 @@ def test_cpp_dropin_on_gpu(precision, k, devices):
     assert r["group"]["same_subs"] == r["group"]["subs"] == k and r["group"]["same_fetch"] == 3000
     o = r["oracle_gpu"]
     assert o["total_cycles"] == r["oracle_cpu"]["total_cycles"] and o["same_subs"] == k and o["same_fetch"] == 3000
+
+
+def test_sub_results_sequence_over_the_abi_array():
+    """ParallelResult.sub_results (api.SubResults) over an ilsim_sub_result
+    array, as GpuSimulator._collect builds it: sequence behaviour, per-sub-trace
+    fetch slices in trace order, edits that stick, vectorised totals."""
+    import numpy as np
+
+    from paper_2105_05821_b200 import _lib
+    from paper_2105_05821_b200.api import GpuSimulator
+    from paper_2105_05821_b200.dist import Totals
+
+    subs = (_lib.SubResult * 4)()
+    for j, (n, c) in enumerate([(3, 10), (0, 0), (2, 9), (4, 7)]):
+        subs[j].instructions, subs[j].total_cycles, subs[j].sum_fetch = n, c, c - 1
+        subs[j].empty = int(n == 0)
+    pf = np.arange(9, dtype=np.uint32)
+
+    class Tot:
+        device_ms, kernel_ms, launches, rounds = 1.5, (0.0, 0.0, 0.0, 0.0), 3, 4
+
+    r = GpuSimulator._collect(subs, 4, pf, 9, Tot, None, 0, None)
+    s = r.sub_results
+    assert (r.total_cycles, r.instructions, len(s)) == (26, 9, 4)
+    assert s[1].empty and s[1].cpi == 0.0 and s[-1] is s[3] and s[0].cpi == 10 / 3
+    assert [x.predicted_fetch.tolist() for x in s] == [[0, 1, 2], [], [3, 4], [5, 6, 7, 8]]
+    assert [x.total_cycles for x in s[1:3]] == [0, 9] and [x.instructions for x in s] == [3, 0, 2, 4]
+    with pytest.raises(IndexError):
+        s[4]
+    t = Totals.of(s)
+    assert (t.total_cycles, t.instructions, t.sum_fetch) == (26, 9, 22)
+    s[2].total_cycles += 5  # edits stick on the cached object
+    assert s[2].total_cycles == 14
